@@ -1,0 +1,320 @@
+"""Benchmark: DirectLiNGAM causal-order search (arXiv 2403.03772 hot path) on B200.
+
+Metric (BASELINE.json): causal-order wall seconds and pair-evaluations/s at d=2000,
+n=10000 (config C5), on N GPUs, beside the reference CPU path on the host cores.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c5]
+    torchrun --nproc-per-node N bench.py --gpus N ...       (one process per GPU)
+
+A step is one full causal_order over the synthetic matrix. `value` is measured with the
+matrix already resident in HBM (device time from CUDA events on the engine stream, max
+over ranks); `e2e` is the same metric through the public API with the matrix in pinned
+host memory (H2D copy and D2H of the order inside the timed region).
+pair-evals = P(d) = (d+1) d (d-1) / 3 ordered (i, j) evaluations of Alg. 1 per fit.
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (d, n, generator description)
+    "c1": (10, 1000, "two-level DAG (gen_two_level_dag), U(0,1) noise, seed 42000"),
+    "c2": (100, 10000, "sparse ER DAG (avg 2 parents, |w| in [0.5,1.5]), Laplace(0,1) noise, seed 1"),
+    "c3": (1000, 10000, "sparse ER DAG (avg 2 parents), Student-t3 noise, seed 1 (Perturb-seq shaped)"),
+    "c5": (2000, 10000, "sparse ER DAG (avg 2 parents, |w| in [0.5,1.5]), Laplace(0,1) noise, seed 1"),
+}
+FP64_OPS_PER_EDE = 32     # FP64-pipe instructions per EDE in the pair kernel (cuobjdump SASS)
+LIBDEVICE_OPS_PER_EDE = 70  # SURVEY.md §8d algorithmic basis (libdevice exp/log1p)
+FP64_PEAK_TFLOPS = 33.85  # measured DFMA microbenchmark on this pool's B200 (tools/probe/fp64_peak.cu)
+
+
+def pair_evals(d: int) -> int:
+    return (d + 1) * d * (d - 1) // 3
+
+
+def make_input(name: str):
+    import paper_2403_03772_b200 as plg
+
+    d, n, _ = CONFIGS[name]
+    if name == "c1":
+        dag = plg.gen_two_level_dag(d, seed=42000)
+        return plg.sample_lingam(dag, n, seed=42000)
+    kind = "t3" if name == "c3" else "laplace"
+    dag = plg.gen_sparse_dag(d, avg_parents=2.0, seed=1)
+    return plg.sample_lingam(dag, n, seed=1, noise=(0.0, 1.0), kind=kind)
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "200",
+                 "-i", str(self.device)], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait(timeout=10)
+
+    def summary(self):
+        rows = []
+        try:
+            for line in open(self.path):
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 9 and parts[1].replace(".", "").isdigit():
+                    rows.append(parts)
+        except OSError:
+            pass
+        finally:
+            if self.path and os.path.exists(self.path):
+                os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = np.array([float(r[1]) for r in rows])
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(float(r[2]) for r in rows)),
+                "reasons": reasons, "samples": len(rows),
+                "power_w_max": float(max(float(r[3]) for r in rows if r[3].replace(".", "").isdigit()))}
+
+
+def load_ncu_traffic():
+    """dram bytes per pair-kernel launch from the committed ncu --set full summary, if any."""
+    for path in sorted(
+            [os.path.join(ROOT, "profiles", f) for f in os.listdir(os.path.join(ROOT, "profiles"))]
+            if os.path.isdir(os.path.join(ROOT, "profiles")) else [], reverse=True):
+        if path.endswith("pair_kernel_ncu.json"):
+            try:
+                return json.load(open(path)).get("dram_bytes_per_launch")
+            except (OSError, ValueError):
+                return None
+    return None
+
+
+def cpu_baseline(X: np.ndarray, target_seconds: float = 15.0):
+    """The reference CPU path (faithful oracle port: both residual directions per ordered
+    pair, static thread partition, -O3 -ffp-contract=off) on a bounded sample: one search
+    round over the first S columns at the full n, S sized for ~target_seconds."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_lib
+
+    cores = os.cpu_count() or 1
+    n = X.shape[0]
+    S = min(48, X.shape[1])
+    t0 = time.perf_counter()
+    oracle_lib.search_causal_order(np.asfortranarray(X[:, :S]), list(range(S)), workers=cores)
+    dt = time.perf_counter() - t0
+    rate = S * (S - 1) / dt
+    S2 = int(min(X.shape[1], max(S, (target_seconds * rate) ** 0.5)))
+    if S2 > S:
+        t0 = time.perf_counter()
+        oracle_lib.search_causal_order(np.asfortranarray(X[:, :S2]), list(range(S2)), workers=cores)
+        dt = time.perf_counter() - t0
+        rate = S2 * (S2 - 1) / dt
+        S = S2
+    return {"value": rate, "unit": "pair-evals/s", "cores": cores, "kind": "port",
+            "sample": f"one search round over the first {S} columns at n={n} ({S * (S - 1)} ordered pair-evals, "
+                      f"{dt:.1f} s); faithful oracle (reference cannot build: Eigen3 absent)",
+            "seconds": dt}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def allreduce_max(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world: int):
+    import torch
+
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    d, n, desc = CONFIGS[args.config]
+    X = make_input(args.config)
+    for _ in range(args.warmup if args.warmup < 1 else 1):
+        pass
+    samples = [cpu_baseline(X, target_seconds=args.cpu_seconds) for _ in range(max(1, args.steps))]
+    rate = float(np.median([s["value"] for s in samples]))
+    wall = pair_evals(d) / rate
+    line = {
+        "metric": "causal-order pair-evals/s (and wall s) at d=2000,n=10k",
+        "impl": "reference", "value": rate, "unit": "pair-evals/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": wall * 1e3, "wall_s_extrapolated": wall,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic: {desc}",
+        "config": {"workload": f"{args.config.upper()} d={d} n={n}", "d": d, "n": n},
+        "cpu_baseline": {k: samples[-1][k] for k in ("unit", "cores", "kind", "sample")} | {"value": rate},
+        "e2e": {"value": rate, "unit": "pair-evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, world, rank, local):
+    import torch
+
+    import paper_2403_03772_b200 as plg
+
+    d, n, desc = CONFIGS[args.config]
+    if world > 1:
+        import torch.distributed as dist
+
+        obj = [plg.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        eng = plg.Engine.distributed(local, rank, world, obj[0])
+    else:
+        torch.cuda.set_device(local)
+        eng = plg.Engine(local)
+    X = make_input(args.config)
+    dX = torch.from_numpy(np.ascontiguousarray(X.T)).to(f"cuda:{local}")  # column j contiguous
+    ptr = dX.data_ptr()
+    for _ in range(args.warmup):
+        order = eng.causal_order_device(ptr, n, d, n)
+    barrier(world)
+
+    dev_ms, pair_ms, launches = [], [], 0
+    with ClockSampler(local) as clocks:
+        barrier(world)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            order = eng.causal_order_device(ptr, n, d, n)
+            st = eng.stats()
+            dev_ms.append(st["total_ms"])
+            pair_ms.append(st["pair_ms"])
+            launches += st["launches"]
+        barrier(world)
+        wall = time.perf_counter() - t0
+    clk = clocks.summary()
+    dev_s = allreduce_max(sum(dev_ms) / 1e3, world)
+    wall = allreduce_max(wall, world)
+    P = pair_evals(d)
+    value = P * args.steps / dev_s
+
+    # e2e: the public API with the matrix in pinned host memory
+    pinned = torch.empty((d, n), dtype=torch.float64, pin_memory=True)
+    pinned.copy_(torch.from_numpy(np.ascontiguousarray(X.T)))
+    Xh = pinned.numpy().T  # F-contiguous (n, d) view, zero-copy into the binding
+    e2e_orders = []
+    barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        e2e_orders.append(eng.causal_order(Xh))
+    barrier(world)
+    e2e_s = allreduce_max(time.perf_counter() - t0, world)
+    st_e2e = eng.stats()
+    assert all(o == order for o in e2e_orders), "host and device entry points disagree"
+
+    if rank != 0:
+        return
+    ede = n * P
+    pair_s = sum(pair_ms) / 1e3 / args.steps
+    # the pair kernel's share of the step and its FP64-pipe roofline
+    achieved = FP64_OPS_PER_EDE * 2 * ede / (pair_s * world) / 1e12 if pair_s > 0 else None
+    line = {
+        "metric": "causal-order pair-evals/s (and wall s) at d=2000,n=10k",
+        "value": value, "unit": "pair-evals/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dev_s * 1e3 / args.steps, "causal_order_wall_s": dev_s / args.steps,
+        "host_wall_ms_per_step": wall * 1e3 / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic: {desc}; generated on host, random DAG weights",
+        "config": {"workload": f"{args.config.upper()} d={d} n={n}", "d": d, "n": n,
+                   "parallelism": f"pair tiles sharded over {world} GPU(s), one ncclAllGather per round"
+                   if world > 1 else "single GPU",
+                   "l2": "input larger than L2 (FP64 matrix %.0f MB vs 126 MB L2)" % (8 * n * d / 1e6)},
+        "roofline": {"bound": "fp64", "kernel": "pair_kernel+finalize", "unit": "TFLOP/s",
+                     "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
+                     "frac": achieved / FP64_PEAK_TFLOPS if achieved else None,
+                     "traffic": load_ncu_traffic(),
+                     "basis": f"{FP64_OPS_PER_EDE} FP64-pipe instructions per EDE (SASS) x 2 flops, "
+                              f"EDE = n * pair-evals; peak = measured DFMA rate (no FP64 figure in "
+                              f"MEASURED_PEAKS.json)",
+                     "libdevice_basis_frac": (LIBDEVICE_OPS_PER_EDE * 2 * ede / (pair_s * world) / 1e12)
+                     / FP64_PEAK_TFLOPS if pair_s > 0 else None,
+                     "pair_share_of_step": pair_s / (dev_s / args.steps)},
+        "e2e": {"value": P * args.steps / e2e_s, "unit": "pair-evals/s",
+                "h2d_bytes_per_step": int(st_e2e["h2d_bytes"]), "d2h_bytes_per_step": int(st_e2e["d2h_bytes"]),
+                "wall_s_per_step": e2e_s / args.steps},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    if world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(X, target_seconds=args.cpu_seconds)
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c5")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    world, rank, local = dist_setup(args)
+    try:
+        if args.impl == "reference":
+            run_reference(args, world, rank)
+        else:
+            run_ours(args, world, rank, local)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,142 @@
+/*
+ * plingam_b200.h — C-ABI of the B200 DirectLiNGAM causal-order engine
+ * (libplingam_b200.so). Plain pointers and sizes; no exceptions cross this boundary;
+ * the caller owns every buffer, the library copies inputs and never retains pointers.
+ *
+ * Each entry point replaces one reference interface (paths relative to
+ * /root/reference/proj); see INTEGRATION.md for the bindings a maintainer would add.
+ *
+ * Matrices are column-major FP64 (each variable contiguous), n samples x d variables,
+ * leading dimension ld >= n — the layout of plingam::DataMatrix (include/plingam/types.hpp:14-30).
+ *
+ * Status: code 0 = ok, otherwise 1 + ordinal of plingam::ErrorCode
+ * (include/plingam/error.hpp:10-27); row/col carry the reference's Error::row()/col()
+ * (-1 when not meaningful). Every function returns st->code.
+ */
+#ifndef PLINGAM_B200_H
+#define PLINGAM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct plg_status {
+  int32_t code;
+  int64_t row;
+  int64_t col;
+  char msg[256];
+} plg_status;
+
+enum plg_error_code {
+  PLG_OK = 0,
+  PLG_NonFinite = 1,
+  PLG_ZeroVariance = 2,
+  PLG_TooFewSamples = 3,
+  PLG_TooShort = 4,
+  PLG_LengthMismatch = 5,
+  PLG_DimensionMismatch = 6,
+  PLG_EmptyCandidates = 7,
+  PLG_SingularDesign = 8,
+  PLG_InsufficientRows = 9,
+  PLG_UnstableSystem = 10,
+  PLG_OutOfRange = 11,
+  PLG_InvalidIndex = 12,
+  PLG_CudaError = 100, /* device/runtime failure (no reference counterpart) */
+  PLG_NcclError = 101
+};
+
+/* Per-call measurements of the last causal_order / search on this context. */
+typedef struct plg_stats {
+  double total_ms;      /* device time of the whole call (CUDA events on the engine stream) */
+  double pair_ms;       /* sum over rounds of pair kernel + finalize device time */
+  double h2d_ms;        /* host->device copy of X (host entry points only) */
+  int64_t pair_evals;   /* ordered (i, j) pair evaluations of the reference's Alg. 1 */
+  int64_t ede;          /* element-direction evaluations (= n * pair_evals) */
+  int64_t launches;     /* kernels launched by the call */
+  int32_t rounds;
+  int32_t world;
+  int64_t h2d_bytes;
+  int64_t d2h_bytes;
+} plg_stats;
+
+typedef struct plg_ctx plg_ctx;
+
+/* Library version string, e.g. "plingam_b200 0.1.0 (sm_100a)". */
+const char* plg_version(void);
+
+/* One engine on one device (replaces the CPU worker pool of ordering.cpp:114-146). */
+int plg_ctx_create(int32_t device, plg_ctx** out, plg_status* st);
+
+/* Multi-GPU: one process per GPU. Every rank passes the same 128-byte NCCL unique id
+ * (from plg_nccl_unique_id on rank 0). The data are replicated; rank r evaluates its
+ * contiguous share of the pair tiles and one ncclAllGather per round exchanges the
+ * entropies, so every rank holds the identical order. */
+int plg_nccl_unique_id(void* out_128_bytes, plg_status* st);
+int plg_ctx_create_dist(int32_t device, int32_t rank, int32_t world, const void* nccl_uid_128,
+                        plg_ctx** out, plg_status* st);
+void plg_ctx_destroy(plg_ctx* ctx);
+
+/* plingam::causal_order(X, parallel, workers) — ordering.hpp:42, ordering.cpp:213-244.
+ * X in host memory; order_out: d ints. */
+int plg_causal_order(plg_ctx* ctx, const double* X, int64_t n, int32_t d, int64_t ld,
+                     int32_t* order_out, plg_status* st);
+
+/* Same, with X already resident in device memory of ctx's device. */
+int plg_causal_order_device(plg_ctx* ctx, const double* dX, int64_t n, int32_t d, int64_t ld,
+                            int32_t* order_out, plg_status* st);
+
+/* plingam::search_causal_order(X, U) — ordering.hpp:27, ordering.cpp:101-168.
+ * scores_out: d doubles, -inf for non-candidates, -k for candidates. */
+int plg_search(plg_ctx* ctx, const double* X, int64_t n, int32_t d, int64_t ld, const int32_t* U,
+               int32_t u, int32_t* chosen_out, double* scores_out, plg_status* st);
+
+/* plingam::regress_out(X, exog, remaining) — ordering.hpp:38, ordering.cpp:178-211.
+ * out: n x r column-major (ld = n). */
+int plg_regress_out(plg_ctx* ctx, const double* X, int64_t n, int32_t d, int64_t ld, int32_t exog,
+                    const int32_t* remaining, int32_t r, double* out, plg_status* st);
+
+/* Adjacency weights of DirectLingam::fit (direct_lingam.cpp:46-70) given an order:
+ * B (d x d, column-major, B[target + d * pred]) from the centred covariance, every
+ * predecessor regression at once through one Cholesky of the order-permuted
+ * covariance. used_pinv is set (and a pseudo-inverse solution used) when a predecessor
+ * design is rank deficient. */
+int plg_fit_weights(plg_ctx* ctx, const double* X, int64_t n, int32_t d, int64_t ld,
+                    const int32_t* order, double* B_out, int32_t* used_pinv, plg_status* st);
+
+/* Round schedule (host-only, no device needed): the rank's contiguous share of the pair
+ * tiles and the round's sample segmentation. The segmentation depends only on (u, n), so
+ * every pair entropy has the same bits for any world size. */
+typedef struct plg_round_plan {
+  int32_t nb;             /* 32-wide position blocks: ceil(u / 32) */
+  int32_t ntiles;         /* upper-triangle tiles nb (nb + 1) / 2 */
+  int32_t tiles_per_rank; /* ceil(ntiles / world); rank r owns [r * tpr, min(ntiles, (r+1) * tpr)) */
+  int32_t tile_begin;
+  int32_t tile_count;
+  int32_t nseg;
+  int32_t seg_len;
+} plg_round_plan;
+int plg_plan_round(int32_t u, int64_t n, int32_t rank, int32_t world, plg_round_plan* out);
+/* tile index -> (bi, bj), bi <= bj, row-major over the upper triangle */
+int plg_tile_decode(int32_t t, int32_t nb, int32_t* bi, int32_t* bj);
+
+/* Stats of the last call on ctx. */
+int plg_last_stats(plg_ctx* ctx, plg_stats* out);
+
+/* Sampled-round state: run the first `rounds` rounds of causal_order and
+ * return the working state the next round would search: the active variables (ascending)
+ * and their current working columns (n x u_active, column-major). Scale-equivalent to
+ * the reference's `working` matrix columns (standardisation absorbs the scale). */
+int plg_round_state(plg_ctx* ctx, const double* X, int64_t n, int32_t d, int64_t ld,
+                    int32_t rounds, int32_t* active_out, int32_t* n_active, double* cols_out,
+                    int32_t* order_prefix_out, plg_status* st);
+
+/* Test hook: element functions on device for a host vector u (n values): out[4i..4i+3] =
+ * {log cosh (table path), u e^{-u^2/2} (table path), libdevice log cosh, libdevice pdf}. */
+int plg_math_probe(plg_ctx* ctx, const double* u, int64_t n, double* out, plg_status* st);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,828 @@
+// engine.cu — the C-ABI (include/plingam_b200.h) and the device-resident round loop.
+//
+// causal_order (reference proj/src/ordering.cpp:213-244) runs here as:
+//   standardise once (bit-identical to the reference's round-0 standardize)
+//   Gram C = W^T W / n once
+//   per round (u active):  column entropies H -> pair kernel (this rank's tiles) ->
+//     finalize -> [ncclAllGather of entropy tiles] -> k reduce -> argmin/commit ->
+//     rank-1 Gram update + in-place residualisation of the u-1 remaining columns
+// Everything is enqueued on one stream without host synchronisation; the host only
+// knows u = d - round, which fixes every grid. Errors are recorded on the device in the
+// reference's raising order and reported once at the end.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <vector>
+
+#include "../../include/plingam_b200.h"
+#include "plg_kernels.h"
+#include "plg_math.cuh"
+
+namespace {
+
+using plg::kBT;
+using plg::kTilePairs;
+
+constexpr double kZeroVarTol = 1e-12;  // partial variance relative to the standardised 1.0
+constexpr int kTargetCtas = 4 * 148 * 8;  // sized so 8 ranks still get several waves
+
+int set_status(plg_status* st, int32_t code, int64_t row, int64_t col, const char* fmt, ...) {
+  if (st) {
+    st->code = code;
+    st->row = row;
+    st->col = col;
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(st->msg, sizeof(st->msg), fmt, ap);
+    va_end(ap);
+  }
+  return code;
+}
+
+int ok(plg_status* st) {
+  if (st) {
+    st->code = 0;
+    st->row = -1;
+    st->col = -1;
+    st->msg[0] = '\0';
+  }
+  return 0;
+}
+
+#define PLG_CUDA(call)                                                                  \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return set_status(st, PLG_CudaError, -1, -1, "%s: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+// ---- NCCL, resolved at run time (the process may already hold torch's libnccl.so.2) ----
+struct NcclApi {
+  bool loaded = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  if (!api.loaded) {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+      api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
+      api.AllGather = reinterpret_cast<decltype(api.AllGather)>(dlsym(h, "ncclAllGather"));
+      api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+      api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+      api.loaded = api.GetUniqueId && api.CommInitRank && api.AllGather && api.CommDestroy;
+    }
+  }
+  return api;
+}
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t cap = 0;
+  cudaError_t reserve(size_t count) {
+    if (count <= cap) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    cudaError_t e = cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T));
+    if (e == cudaSuccess) cap = count;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+struct SegPlan {
+  int nseg;
+  int seg_len;
+};
+
+// Sample segmentation of a round: a pure function of (u, n), so the per-pair reduction
+// order — and with it every entropy bit — is independent of the rank count.
+SegPlan seg_plan(int u, int64_t n) {
+  const int nb = (u + kBT - 1) / kBT;
+  const int ntiles = nb * (nb + 1) / 2;
+  int nseg = (kTargetCtas + ntiles - 1) / ntiles;
+  const int cap = static_cast<int>(std::max<int64_t>(1, n / plg::kSegMin));
+  nseg = std::max(1, std::min(nseg, cap));
+  const int64_t seg_len = round_up((n + nseg - 1) / nseg, plg::kCH);
+  return {static_cast<int>((n + seg_len - 1) / seg_len), static_cast<int>(seg_len)};
+}
+
+}  // namespace
+
+struct plg_ctx {
+  int device = 0;
+  int rank = 0;
+  int world = 1;
+  cudaStream_t stream = nullptr;
+  ncclComm_t comm = nullptr;
+  bool timing = true;
+
+  double* g_exp = nullptr;
+  double2* g_log = nullptr;
+
+  DevBuf<double> Xd, W, C, part, epack, H, k, scores, msd;
+  DevBuf<int> act0, act1, colvar, order, stat, idx, nz;
+  DevBuf<plg::RoundState> rs;
+  DevBuf<unsigned long long> err;
+  std::vector<cudaEvent_t> ev;  // pool: [0]=start [1]=end [2]=h2d end, then 2 per round
+  plg_stats last{};
+  int64_t launches = 0;
+
+  cudaError_t events(size_t count) {
+    while (ev.size() < count) {
+      cudaEvent_t e;
+      cudaError_t r = cudaEventCreate(&e);
+      if (r != cudaSuccess) return r;
+      ev.push_back(e);
+    }
+    return cudaSuccess;
+  }
+};
+
+namespace {
+
+int make_tables(plg_ctx* ctx, plg_status* st) {
+  std::vector<double> e(plg::kExpN);
+  std::vector<double2> l(plg::kLogN);
+  for (int j = 0; j < plg::kExpN; ++j) e[j] = static_cast<double>(exp2l(static_cast<long double>(j) / plg::kExpN));
+  const long double ln2 = logl(2.0L);
+  for (int j = 0; j < plg::kLogN; ++j) {
+    const double c = (j == plg::kLogN - 1)
+                         ? 0.5
+                         : static_cast<double>(1.0L / (1.0L + (static_cast<long double>(j) + 0.5L) /
+                                                                  (plg::kLogN - 1)));
+    l[j] = make_double2(c, static_cast<double>(-logl(static_cast<long double>(c)) - ln2));
+  }
+  PLG_CUDA(cudaMalloc(&ctx->g_exp, e.size() * sizeof(double)));
+  PLG_CUDA(cudaMalloc(&ctx->g_log, l.size() * sizeof(double2)));
+  PLG_CUDA(cudaMemcpy(ctx->g_exp, e.data(), e.size() * sizeof(double), cudaMemcpyHostToDevice));
+  PLG_CUDA(cudaMemcpy(ctx->g_log, l.data(), l.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  return 0;
+}
+
+int ctx_init(plg_ctx* ctx, int device, plg_status* st) {
+  ctx->device = device;
+  PLG_CUDA(cudaSetDevice(device));
+  PLG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+  if (int rc = make_tables(ctx, st)) return rc;
+  PLG_CUDA(ctx->err.reserve(1));
+  PLG_CUDA(ctx->rs.reserve(1));
+  return ok(st);
+}
+
+// Decode the device error key into the reference's exception.
+int report_error(unsigned long long key, const int* /*unused*/, plg_status* st) {
+  const unsigned kind = static_cast<unsigned>((key >> 32) & 0xff);
+  const int col = static_cast<int>(key & 0xffffffffu) - 1;
+  if (kind == plg::kErrColZeroVar)
+    return set_status(st, PLG_ZeroVariance, -1, col,
+                      "search_causal_order: column %d has zero variance", col);
+  return set_status(st, PLG_ZeroVariance, -1, -1,
+                    "entropy_of_normalized: zero residual (exactly collinear pair)");
+}
+
+struct RoundPlan {
+  int nb, ntiles, tpr, tb, ntl;
+  SegPlan seg;
+};
+
+RoundPlan plan_round(int u, int64_t n, int rank, int world) {
+  RoundPlan p;
+  p.nb = (u + kBT - 1) / kBT;
+  p.ntiles = p.nb * (p.nb + 1) / 2;
+  p.tpr = (p.ntiles + world - 1) / world;
+  p.tb = std::min(p.ntiles, rank * p.tpr);
+  p.ntl = std::min(p.ntiles, p.tb + p.tpr) - p.tb;
+  p.seg = seg_plan(u, n);
+  return p;
+}
+
+// One search round over the active list act_cur (u >= 2): H, pairs, exchange, k.
+int search_round(plg_ctx* c, int64_t n, int64_t ldw, int ldc, int u, const int* act_cur,
+                 int round, size_t ev_base, plg_status* st) {
+  const RoundPlan rp = plan_round(u, n, c->rank, c->world);
+  plg::launch_colent(c->W.p, ldw, n, c->C.p, ldc, act_cur, u, c->H.p, c->g_exp, c->g_log, c->nz.p,
+                     c->colvar.p, round, c->err.p, c->stream);
+  ++c->launches;
+  plg::PairLaunch a;
+  a.W = c->W.p;
+  a.ldw = ldw;
+  a.n = n;
+  a.C = c->C.p;
+  a.ldc = ldc;
+  a.act = act_cur;
+  a.u = u;
+  a.nb = rp.nb;
+  a.tile_begin = rp.tb;
+  a.ntiles = rp.ntl;
+  a.seg_len = rp.seg.seg_len;
+  a.nseg = rp.seg.nseg;
+  a.part = c->part.p;
+  a.epack = c->epack.p;
+  a.g_exp = c->g_exp;
+  a.g_log = c->g_log;
+  a.err = c->err.p;
+  a.round = round;
+  if (c->timing) cudaEventRecord(c->ev[ev_base], c->stream);
+  if (rp.ntl > 0) {
+    plg::launch_pair(a, c->stream);
+    plg::launch_finalize(a, c->stream);
+    c->launches += 2;
+  }
+  if (c->timing) cudaEventRecord(c->ev[ev_base + 1], c->stream);
+  if (c->world > 1) {
+    const size_t cnt = static_cast<size_t>(rp.tpr) * 2 * kTilePairs;
+    ncclResult_t r = nccl().AllGather(c->epack.p + static_cast<size_t>(c->rank) * cnt, c->epack.p, cnt,
+                                      ncclDouble, c->comm, c->stream);
+    if (r != ncclSuccess)
+      return set_status(st, PLG_NcclError, -1, -1, "ncclAllGather: %s", nccl().GetErrorString(r));
+  }
+  plg::launch_kreduce(c->epack.p, c->H.p, u, rp.nb, c->k.p, c->err.p, c->stream);
+  ++c->launches;
+  return 0;
+}
+
+// Reserve every buffer a run over `ncols` columns needs (no allocation inside the loop).
+int reserve_run(plg_ctx* c, int64_t n, int ncols, int64_t ldw, plg_status* st) {
+  size_t part_max = 0, epack_max = 0;
+  for (int u = ncols; u >= 2; --u) {
+    const RoundPlan rp = plan_round(u, n, c->rank, c->world);
+    part_max = std::max(part_max, static_cast<size_t>(rp.ntl) * rp.seg.nseg * kTilePairs * 4);
+    epack_max = std::max(epack_max, static_cast<size_t>(rp.tpr) * c->world * 2 * kTilePairs);
+  }
+  PLG_CUDA(c->W.reserve(static_cast<size_t>(ncols) * ldw));
+  PLG_CUDA(c->C.reserve(static_cast<size_t>(ncols) * ncols));
+  PLG_CUDA(c->part.reserve(part_max));
+  PLG_CUDA(c->epack.reserve(epack_max));
+  PLG_CUDA(c->H.reserve(ncols));
+  PLG_CUDA(c->k.reserve(ncols));
+  PLG_CUDA(c->scores.reserve(ncols));
+  PLG_CUDA(c->act0.reserve(ncols));
+  PLG_CUDA(c->act1.reserve(ncols));
+  PLG_CUDA(c->colvar.reserve(ncols));
+  PLG_CUDA(c->order.reserve(ncols));
+  PLG_CUDA(c->stat.reserve(2 * static_cast<size_t>(ncols)));
+  PLG_CUDA(c->msd.reserve(2 * static_cast<size_t>(ncols)));
+  PLG_CUDA(c->idx.reserve(ncols));
+  PLG_CUDA(c->nz.reserve(ncols));
+  PLG_CUDA(c->events(3 + 2 * static_cast<size_t>(std::max(ncols, 1))));
+  return 0;
+}
+
+int upload_iota(plg_ctx* c, int* dst, int count, const int* values, plg_status* st) {
+  std::vector<int> v(count);
+  for (int i = 0; i < count; ++i) v[i] = values ? values[i] : i;
+  PLG_CUDA(cudaMemcpyAsync(dst, v.data(), count * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  PLG_CUDA(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+// Validation (types.cpp:21-47) + standardisation of the source columns into W.
+int standardize_validate(plg_ctx* c, const double* dX, int64_t ldx, int64_t n, int ncol,
+                         const int* d_colmap, const int* h_colmap, int64_t ldw, bool validate,
+                         plg_status* st) {
+  plg::launch_standardize(dX, ldx, n, d_colmap, ncol, c->W.p, ldw, c->stat.p, c->msd.p,
+                          validate ? 1 : 0, c->stream);
+  ++c->launches;
+  std::vector<int> stat(2 * static_cast<size_t>(ncol));
+  PLG_CUDA(cudaMemcpyAsync(stat.data(), c->stat.p, stat.size() * sizeof(int), cudaMemcpyDeviceToHost,
+                           c->stream));
+  PLG_CUDA(cudaStreamSynchronize(c->stream));
+  for (int j = 0; j < ncol; ++j) {
+    const int col = h_colmap ? h_colmap[j] : j;
+    if (validate && stat[2 * j] >= 0)
+      return set_status(st, PLG_NonFinite, stat[2 * j], col,
+                        "validate: non-finite entry at row %d, column x%d", stat[2 * j], col);
+    if (stat[2 * j + 1]) {
+      if (validate)
+        return set_status(st, PLG_ZeroVariance, -1, col, "validate: column x%d has zero variance", col);
+      return set_status(st, PLG_ZeroVariance, -1, col,
+                        "search_causal_order: column %d has zero variance", col);
+    }
+  }
+  return 0;
+}
+
+void finish_stats(plg_ctx* c, int64_t n, int d, int rounds, bool host_in) {
+  plg_stats& s = c->last;
+  s.rounds = rounds;
+  s.world = c->world;
+  s.launches = c->launches;
+  int64_t pairs = 0;
+  for (int u = d; u >= 2 && d - u < rounds; --u) pairs += static_cast<int64_t>(u) * (u - 1);
+  s.pair_evals = pairs;
+  s.ede = pairs * n;
+  if (!c->timing) return;
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
+  s.total_ms = ms;
+  if (host_in) {
+    cudaEventElapsedTime(&ms, c->ev[0], c->ev[2]);
+    s.h2d_ms = ms;
+  }
+  double pair_ms = 0.0;
+  for (int r = 0; r < rounds; ++r) {
+    if (cudaEventElapsedTime(&ms, c->ev[3 + 2 * r], c->ev[4 + 2 * r]) == cudaSuccess) pair_ms += ms;
+  }
+  s.pair_ms = pair_ms;
+}
+
+// The recursive loop (ordering.cpp:213-244) on device-resident X.
+int causal_order_impl(plg_ctx* c, const double* dX, int64_t ldx, int64_t n, int d, int max_rounds,
+                      int32_t* order_out, bool host_in, plg_status* st) {
+  const int64_t ldw = round_up(std::max<int64_t>(n, 2), 16);
+  if (int rc = reserve_run(c, n, d, ldw, st)) return rc;
+  if (int rc = standardize_validate(c, dX, ldx, n, d, nullptr, nullptr, ldw, true, st)) return rc;
+  if (d == 1) {
+    order_out[0] = 0;
+    return ok(st);
+  }
+  if (int rc = upload_iota(c, c->act0.p, d, nullptr, st)) return rc;
+  if (int rc = upload_iota(c, c->colvar.p, d, nullptr, st)) return rc;
+  PLG_CUDA(cudaMemsetAsync(c->err.p, 0xff, sizeof(unsigned long long), c->stream));
+  plg::launch_gram(c->W.p, ldw, n, d, c->C.p, d, c->stream);
+  ++c->launches;
+  const int rounds = (max_rounds < 0) ? d - 1 : std::min(max_rounds, d - 1);
+  for (int r = 0; r < rounds; ++r) {
+    const int u = d - r;
+    int* act_cur = (r & 1) ? c->act1.p : c->act0.p;
+    int* act_nxt = (r & 1) ? c->act0.p : c->act1.p;
+    if (int rc = search_round(c, n, ldw, d, u, act_cur, r, 3 + 2 * static_cast<size_t>(r), st)) return rc;
+    plg::launch_commit(c->k.p, act_cur, act_nxt, u, c->colvar.p, c->order.p, r, nullptr, c->rs.p,
+                       c->err.p, c->stream);
+    ++c->launches;
+    if (u - 1 >= 2 || (u - 1 == 1 && max_rounds >= 0)) {
+      // the next round's build_cache check only exists when it has >= 2 candidates
+      plg::launch_update_gram(c->C.p, d, act_nxt, u - 1, c->rs.p, c->err.p, c->stream);
+      plg::launch_residualize(c->W.p, ldw, n, c->C.p, d, act_nxt, u - 1, c->rs.p, c->nz.p, r + 1,
+                              c->err.p, c->stream);
+      c->launches += 2;
+    }
+  }
+  if (c->timing) cudaEventRecord(c->ev[1], c->stream);
+  unsigned long long key = 0;
+  PLG_CUDA(cudaMemcpyAsync(&key, c->err.p, sizeof(key), cudaMemcpyDeviceToHost, c->stream));
+  const int nout = (rounds == d - 1) ? d : rounds;
+  PLG_CUDA(cudaMemcpyAsync(order_out, c->order.p, nout * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                           c->stream));
+  PLG_CUDA(cudaStreamSynchronize(c->stream));
+  PLG_CUDA(cudaGetLastError());
+  finish_stats(c, n, d, rounds, host_in);
+  c->last.d2h_bytes = nout * sizeof(int32_t);
+  if (key != plg::kNoError) return report_error(key, nullptr, st);
+  return ok(st);
+}
+
+int begin_call(plg_ctx* c, plg_status* st) {
+  PLG_CUDA(cudaSetDevice(c->device));
+  c->launches = 0;
+  c->last = plg_stats{};
+  if (c->timing) {
+    PLG_CUDA(c->events(3));
+    PLG_CUDA(cudaEventRecord(c->ev[0], c->stream));
+  }
+  return 0;
+}
+
+int upload_x(plg_ctx* c, const double* X, int64_t n, int d, int64_t ld, plg_status* st) {
+  PLG_CUDA(c->Xd.reserve(static_cast<size_t>(n) * d));
+  PLG_CUDA(cudaMemcpy2DAsync(c->Xd.p, n * sizeof(double), X, ld * sizeof(double), n * sizeof(double), d,
+                             cudaMemcpyHostToDevice, c->stream));
+  if (c->timing) PLG_CUDA(cudaEventRecord(c->ev[2], c->stream));
+  c->last.h2d_bytes = n * d * static_cast<int64_t>(sizeof(double));
+  return 0;
+}
+
+int check_shape(int64_t n, int d, int64_t ld, plg_status* st) {
+  if (d < 1) return set_status(st, PLG_DimensionMismatch, -1, -1, "validate: need at least 1 variable");
+  if (n < 2) return set_status(st, PLG_TooFewSamples, -1, -1, "validate: need at least 2 samples");
+  if (ld < n) return set_status(st, PLG_DimensionMismatch, -1, -1, "leading dimension smaller than n");
+  if (n > (int64_t{1} << 31))
+    return set_status(st, PLG_OutOfRange, -1, -1, "n beyond the engine's 2^31 sample limit");
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* plg_version(void) { return "plingam_b200 0.1.0 (sm_100a)"; }
+
+int plg_ctx_create(int32_t device, plg_ctx** out, plg_status* st) {
+  if (!out) return set_status(st, PLG_OutOfRange, -1, -1, "null output pointer");
+  plg_ctx* c = new plg_ctx();
+  if (int rc = ctx_init(c, device, st)) {
+    plg_ctx_destroy(c);
+    *out = nullptr;
+    return rc;
+  }
+  *out = c;
+  return ok(st);
+}
+
+int plg_nccl_unique_id(void* out_128_bytes, plg_status* st) {
+  NcclApi& api = nccl();
+  if (!api.loaded) return set_status(st, PLG_NcclError, -1, -1, "libnccl.so.2 not loadable");
+  ncclUniqueId id;
+  ncclResult_t r = api.GetUniqueId(&id);
+  if (r != ncclSuccess) return set_status(st, PLG_NcclError, -1, -1, "ncclGetUniqueId: %s", api.GetErrorString(r));
+  memcpy(out_128_bytes, &id, sizeof(id));
+  return ok(st);
+}
+
+int plg_ctx_create_dist(int32_t device, int32_t rank, int32_t world, const void* nccl_uid_128,
+                        plg_ctx** out, plg_status* st) {
+  if (!out) return set_status(st, PLG_OutOfRange, -1, -1, "null output pointer");
+  if (world < 1 || rank < 0 || rank >= world)
+    return set_status(st, PLG_OutOfRange, -1, -1, "invalid rank %d / world %d", rank, world);
+  plg_ctx* c = new plg_ctx();
+  int rc = ctx_init(c, device, st);
+  if (!rc && world > 1) {
+    NcclApi& api = nccl();
+    if (!api.loaded) {
+      rc = set_status(st, PLG_NcclError, -1, -1, "libnccl.so.2 not loadable");
+    } else {
+      ncclUniqueId id;
+      memcpy(&id, nccl_uid_128, sizeof(id));
+      ncclResult_t r = api.CommInitRank(&c->comm, world, id, rank);
+      if (r != ncclSuccess)
+        rc = set_status(st, PLG_NcclError, -1, -1, "ncclCommInitRank: %s", api.GetErrorString(r));
+    }
+  }
+  if (rc) {
+    plg_ctx_destroy(c);
+    *out = nullptr;
+    return rc;
+  }
+  c->rank = rank;
+  c->world = world;
+  *out = c;
+  return ok(st);
+}
+
+void plg_ctx_destroy(plg_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->comm && nccl().loaded) nccl().CommDestroy(c->comm);
+  for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
+  c->Xd.release();
+  c->W.release();
+  c->C.release();
+  c->part.release();
+  c->epack.release();
+  c->H.release();
+  c->k.release();
+  c->scores.release();
+  c->act0.release();
+  c->act1.release();
+  c->colvar.release();
+  c->order.release();
+  c->stat.release();
+  c->msd.release();
+  c->idx.release();
+  c->nz.release();
+  c->rs.release();
+  c->err.release();
+  if (c->g_exp) cudaFree(c->g_exp);
+  if (c->g_log) cudaFree(c->g_log);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+int plg_causal_order(plg_ctx* c, const double* X, int64_t n, int32_t d, int64_t ld,
+                     int32_t* order_out, plg_status* st) {
+  if (!c) return set_status(st, PLG_OutOfRange, -1, -1, "null context");
+  if (int rc = check_shape(n, d, ld, st)) return rc;
+  if (int rc = begin_call(c, st)) return rc;
+  if (int rc = upload_x(c, X, n, d, ld, st)) return rc;
+  return causal_order_impl(c, c->Xd.p, n, n, d, -1, order_out, true, st);
+}
+
+int plg_causal_order_device(plg_ctx* c, const double* dX, int64_t n, int32_t d, int64_t ld,
+                            int32_t* order_out, plg_status* st) {
+  if (!c) return set_status(st, PLG_OutOfRange, -1, -1, "null context");
+  if (int rc = check_shape(n, d, ld, st)) return rc;
+  if (int rc = begin_call(c, st)) return rc;
+  return causal_order_impl(c, dX, ld, n, d, -1, order_out, false, st);
+}
+
+int plg_search(plg_ctx* c, const double* X, int64_t n, int32_t d, int64_t ld, const int32_t* U,
+               int32_t u, int32_t* chosen_out, double* scores_out, plg_status* st) {
+  if (!c) return set_status(st, PLG_OutOfRange, -1, -1, "null context");
+  // sorted_candidates (ordering.cpp:16-33)
+  if (u <= 0) return set_status(st, PLG_EmptyCandidates, -1, -1, "search_causal_order: empty candidate set");
+  std::vector<int> us(U, U + u);
+  std::sort(us.begin(), us.end());
+  for (int p = 0; p < u; ++p) {
+    if (us[p] < 0 || us[p] >= d)
+      return set_status(st, PLG_InvalidIndex, -1, us[p], "search_causal_order: candidate index out of range");
+    if (p > 0 && us[p] == us[p - 1])
+      return set_status(st, PLG_InvalidIndex, -1, us[p], "search_causal_order: duplicate candidate index");
+  }
+  for (int j = 0; j < d; ++j) scores_out[j] = -std::numeric_limits<double>::infinity();
+  if (u == 1) {  // ordering.cpp:107-110
+    scores_out[us[0]] = 0.0;
+    *chosen_out = us[0];
+    return ok(st);
+  }
+  if (n < 2) return set_status(st, PLG_TooShort, -1, -1, "standardize: need at least 2 samples");
+  if (ld < n) return set_status(st, PLG_DimensionMismatch, -1, -1, "leading dimension smaller than n");
+  if (int rc = begin_call(c, st)) return rc;
+  if (int rc = upload_x(c, X, n, d, ld, st)) return rc;
+  const int64_t ldw = round_up(n, 16);
+  if (int rc = reserve_run(c, n, u, ldw, st)) return rc;
+  if (int rc = upload_iota(c, c->colvar.p, u, us.data(), st)) return rc;
+  if (int rc = standardize_validate(c, c->Xd.p, n, n, u, c->colvar.p, us.data(), ldw, false, st)) return rc;
+  if (int rc = upload_iota(c, c->act0.p, u, nullptr, st)) return rc;
+  PLG_CUDA(cudaMemsetAsync(c->err.p, 0xff, sizeof(unsigned long long), c->stream));
+  plg::launch_gram(c->W.p, ldw, n, u, c->C.p, u, c->stream);
+  ++c->launches;
+  if (int rc = search_round(c, n, ldw, u, u, c->act0.p, 0, 3, st)) return rc;
+  PLG_CUDA(c->scores.reserve(d));
+  std::vector<double> ninf(d, -std::numeric_limits<double>::infinity());
+  PLG_CUDA(cudaMemcpyAsync(c->scores.p, ninf.data(), d * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  plg::launch_commit(c->k.p, c->act0.p, nullptr, u, c->colvar.p, nullptr, 0, c->scores.p, c->rs.p,
+                     c->err.p, c->stream);
+  ++c->launches;
+  if (c->timing) cudaEventRecord(c->ev[1], c->stream);
+  unsigned long long key = 0;
+  plg::RoundState rs{};
+  PLG_CUDA(cudaMemcpyAsync(&key, c->err.p, sizeof(key), cudaMemcpyDeviceToHost, c->stream));
+  PLG_CUDA(cudaMemcpyAsync(&rs, c->rs.p, sizeof(rs), cudaMemcpyDeviceToHost, c->stream));
+  PLG_CUDA(cudaMemcpyAsync(scores_out, c->scores.p, d * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  PLG_CUDA(cudaStreamSynchronize(c->stream));
+  PLG_CUDA(cudaGetLastError());
+  finish_stats(c, n, u, 1, true);
+  if (key != plg::kNoError) return report_error(key, nullptr, st);
+  *chosen_out = us[rs.chosen_col];
+  return ok(st);
+}
+
+int plg_regress_out(plg_ctx* c, const double* X, int64_t n, int32_t d, int64_t ld, int32_t exog,
+                    const int32_t* remaining, int32_t r, double* out, plg_status* st) {
+  if (!c) return set_status(st, PLG_OutOfRange, -1, -1, "null context");
+  if (exog < 0 || exog >= d)
+    return set_status(st, PLG_InvalidIndex, -1, exog, "regress_out: exog index out of range");
+  if (int rc = begin_call(c, st)) return rc;
+  if (r == 0) return ok(st);
+  if (int rc = upload_x(c, X, n, d, ld, st)) return rc;
+  PLG_CUDA(c->idx.reserve(r));
+  PLG_CUDA(c->stat.reserve(1));
+  PLG_CUDA(c->W.reserve(static_cast<size_t>(n) * r));
+  // index checks in the reference's order; the exog variance decides whether the first
+  // valid remaining column already throws ZeroVariance(exog) (kernels.cpp:112-115)
+  int zero_var = 0;
+  if (n >= 2) {
+    std::vector<int> safe(remaining, remaining + r);
+    for (int& v : safe)
+      if (v < 0 || v >= d || v == exog) v = (exog + 1) % d;  // placeholder column, result unused
+    PLG_CUDA(cudaMemcpyAsync(c->idx.p, safe.data(), r * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    PLG_CUDA(cudaMemsetAsync(c->stat.p, 0, sizeof(int), c->stream));
+    plg::launch_regress_out(c->Xd.p, n, n, exog, c->idx.p, r, c->W.p, n, c->stat.p, c->stream);
+    ++c->launches;
+    PLG_CUDA(cudaMemcpyAsync(&zero_var, c->stat.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    PLG_CUDA(cudaStreamSynchronize(c->stream));
+  }
+  for (int p = 0; p < r; ++p) {
+    const int v = remaining[p];
+    if (v < 0 || v >= d)
+      return set_status(st, PLG_InvalidIndex, -1, v, "regress_out: remaining index out of range");
+    if (v == exog)
+      return set_status(st, PLG_InvalidIndex, -1, v, "regress_out: exog cannot appear in remaining");
+    if (n < 2) return set_status(st, PLG_TooShort, -1, -1, "residual: need at least 2 samples");
+    if (zero_var)
+      return set_status(st, PLG_ZeroVariance, -1, exog, "regress_out: exogenous column %d has zero variance", exog);
+  }
+  PLG_CUDA(cudaMemcpyAsync(out, c->W.p, static_cast<size_t>(n) * r * sizeof(double), cudaMemcpyDeviceToHost,
+                           c->stream));
+  PLG_CUDA(cudaStreamSynchronize(c->stream));
+  PLG_CUDA(cudaGetLastError());
+  return ok(st);
+}
+
+int plg_plan_round(int32_t u, int64_t n, int32_t rank, int32_t world, plg_round_plan* out) {
+  if (!out || u < 2 || n < 1 || world < 1 || rank < 0 || rank >= world) return PLG_OutOfRange;
+  const RoundPlan rp = plan_round(u, n, rank, world);
+  out->nb = rp.nb;
+  out->ntiles = rp.ntiles;
+  out->tiles_per_rank = rp.tpr;
+  out->tile_begin = rp.tb;
+  out->tile_count = rp.ntl;
+  out->nseg = rp.seg.nseg;
+  out->seg_len = rp.seg.seg_len;
+  return 0;
+}
+
+int plg_tile_decode(int32_t t, int32_t nb, int32_t* bi, int32_t* bj) {
+  if (!bi || !bj || nb < 1 || t < 0 || t >= nb * (nb + 1) / 2) return PLG_OutOfRange;
+  int a = 0, b = 0;
+  plg::tile_decode(t, nb, a, b);
+  *bi = a;
+  *bj = b;
+  return 0;
+}
+
+int plg_last_stats(plg_ctx* c, plg_stats* out) {
+  if (!c || !out) return PLG_OutOfRange;
+  *out = c->last;
+  return 0;
+}
+
+int plg_round_state(plg_ctx* c, const double* X, int64_t n, int32_t d, int64_t ld, int32_t rounds,
+                    int32_t* active_out, int32_t* n_active, double* cols_out, int32_t* order_prefix_out,
+                    plg_status* st) {
+  if (!c) return set_status(st, PLG_OutOfRange, -1, -1, "null context");
+  if (int rc = check_shape(n, d, ld, st)) return rc;
+  if (rounds < 0 || rounds > d - 1) return set_status(st, PLG_OutOfRange, -1, -1, "rounds out of range");
+  if (int rc = begin_call(c, st)) return rc;
+  if (int rc = upload_x(c, X, n, d, ld, st)) return rc;
+  std::vector<int32_t> prefix(std::max(d, 1));
+  if (int rc = causal_order_impl(c, c->Xd.p, n, n, d, rounds, prefix.data(), true, st)) return rc;
+  const int ua = d - rounds;
+  const int* act = (rounds & 1) ? c->act1.p : c->act0.p;
+  if (d == 1) {
+    active_out[0] = 0;
+  } else {
+    PLG_CUDA(cudaMemcpy(active_out, act, ua * sizeof(int), cudaMemcpyDeviceToHost));
+  }
+  *n_active = ua;
+  const int64_t ldw = round_up(std::max<int64_t>(n, 2), 16);
+  for (int p = 0; p < ua; ++p)
+    PLG_CUDA(cudaMemcpy(cols_out + static_cast<int64_t>(p) * n, c->W.p + static_cast<int64_t>(active_out[p]) * ldw,
+                        n * sizeof(double), cudaMemcpyDeviceToHost));
+  if (order_prefix_out) memcpy(order_prefix_out, prefix.data(), rounds * sizeof(int32_t));
+  return ok(st);
+}
+
+int plg_math_probe(plg_ctx* c, const double* u, int64_t n, double* out, plg_status* st) {
+  if (!c) return set_status(st, PLG_OutOfRange, -1, -1, "null context");
+  if (int rc = begin_call(c, st)) return rc;
+  PLG_CUDA(c->Xd.reserve(static_cast<size_t>(n) * 5));
+  PLG_CUDA(cudaMemcpyAsync(c->Xd.p, u, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  plg::launch_math_probe(c->Xd.p, n, c->Xd.p + n, c->g_exp, c->g_log, c->stream);
+  PLG_CUDA(cudaMemcpyAsync(out, c->Xd.p + n, 4 * n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  PLG_CUDA(cudaStreamSynchronize(c->stream));
+  PLG_CUDA(cudaGetLastError());
+  return ok(st);
+}
+
+}  // extern "C"
+
+namespace {
+
+// Minimum-norm solution of the consistent symmetric system A x = b (A = X^T X / n of a
+// rank-deficient design) via cyclic Jacobi eigen-decomposition; equals the minimum-norm
+// least-squares solution of the design (Eigen CompleteOrthogonalDecomposition,
+// direct_lingam.cpp:58-62).
+void pinv_solve_sym(std::vector<double> A, int q, const double* b, double* x) {
+  std::vector<double> V(static_cast<size_t>(q) * q, 0.0);
+  for (int i = 0; i < q; ++i) V[static_cast<size_t>(i) * q + i] = 1.0;
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    double off = 0.0, diag = 0.0;
+    for (int i = 0; i < q; ++i)
+      for (int j = 0; j < q; ++j) (i == j ? diag : off) += A[static_cast<size_t>(i) * q + j] * A[static_cast<size_t>(i) * q + j];
+    if (off <= 1e-30 * diag) break;
+    for (int p = 0; p < q; ++p)
+      for (int r = p + 1; r < q; ++r) {
+        const double apr = A[static_cast<size_t>(p) * q + r];
+        if (apr == 0.0) continue;
+        const double app = A[static_cast<size_t>(p) * q + p], arr = A[static_cast<size_t>(r) * q + r];
+        const double theta = (arr - app) / (2.0 * apr);
+        const double t = (theta >= 0 ? 1.0 : -1.0) / (std::fabs(theta) + std::sqrt(theta * theta + 1.0));
+        const double cs = 1.0 / std::sqrt(t * t + 1.0), sn = t * cs;
+        for (int k = 0; k < q; ++k) {  // A <- A J (columns p, r)
+          const double akp = A[static_cast<size_t>(k) * q + p], akr = A[static_cast<size_t>(k) * q + r];
+          A[static_cast<size_t>(k) * q + p] = cs * akp - sn * akr;
+          A[static_cast<size_t>(k) * q + r] = sn * akp + cs * akr;
+        }
+        for (int k = 0; k < q; ++k) {  // A <- J^T A (rows p, r)
+          const double apk = A[static_cast<size_t>(p) * q + k], ark = A[static_cast<size_t>(r) * q + k];
+          A[static_cast<size_t>(p) * q + k] = cs * apk - sn * ark;
+          A[static_cast<size_t>(r) * q + k] = sn * apk + cs * ark;
+        }
+        for (int k = 0; k < q; ++k) {
+          const double vkp = V[static_cast<size_t>(k) * q + p], vkr = V[static_cast<size_t>(k) * q + r];
+          V[static_cast<size_t>(k) * q + p] = cs * vkp - sn * vkr;
+          V[static_cast<size_t>(k) * q + r] = sn * vkp + cs * vkr;
+        }
+      }
+  }
+  double lmax = 0.0;
+  for (int i = 0; i < q; ++i) lmax = std::max(lmax, std::fabs(A[static_cast<size_t>(i) * q + i]));
+  const double tol = 1e-12 * lmax;
+  for (int j = 0; j < q; ++j) x[j] = 0.0;
+  for (int e = 0; e < q; ++e) {
+    const double lam = A[static_cast<size_t>(e) * q + e];
+    if (!(std::fabs(lam) > tol)) continue;
+    double proj = 0.0;
+    for (int k = 0; k < q; ++k) proj += V[static_cast<size_t>(k) * q + e] * b[k];
+    proj /= lam;
+    for (int j = 0; j < q; ++j) x[j] += proj * V[static_cast<size_t>(j) * q + e];
+  }
+}
+
+}  // namespace
+
+extern "C" int plg_fit_weights(plg_ctx* c, const double* X, int64_t n, int32_t d, int64_t ld,
+                               const int32_t* order, double* B_out, int32_t* used_pinv,
+                               plg_status* st) {
+  // DirectLingam::fit weights (direct_lingam.cpp:40-70): every predecessor regression of
+  // the centred data at once. With S = P^T Sigma P (order-permuted covariance) = L L^T,
+  // the coefficients of position p on positions 0..p-1 are -T[p, 0:p] / T[p, p], T = L^-1.
+  // The covariance comes from the device Gram of the standardised columns.
+  if (!c) return set_status(st, PLG_OutOfRange, -1, -1, "null context");
+  if (int rc = check_shape(n, d, ld, st)) return rc;
+  std::vector<int> seen(d, 0);
+  for (int p = 0; p < d; ++p) {
+    if (order[p] < 0 || order[p] >= d || seen[order[p]]++)
+      return set_status(st, PLG_DimensionMismatch, -1, -1, "fit_weights: order is not a permutation");
+  }
+  if (int rc = begin_call(c, st)) return rc;
+  if (int rc = upload_x(c, X, n, d, ld, st)) return rc;
+  const int64_t ldw = round_up(n, 16);
+  if (int rc = reserve_run(c, n, d, ldw, st)) return rc;
+  if (int rc = standardize_validate(c, c->Xd.p, n, n, d, nullptr, nullptr, ldw, true, st)) return rc;
+  plg::launch_gram(c->W.p, ldw, n, d, c->C.p, d, c->stream);
+  std::vector<double> C(static_cast<size_t>(d) * d), msd(2 * static_cast<size_t>(d));
+  PLG_CUDA(cudaMemcpyAsync(C.data(), c->C.p, C.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  PLG_CUDA(cudaMemcpyAsync(msd.data(), c->msd.p, msd.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  PLG_CUDA(cudaStreamSynchronize(c->stream));
+  // L (row-major, lower) of the permuted correlation; S[p][q] = C[order[p]][order[q]]
+  std::vector<double> L(static_cast<size_t>(d) * d, 0.0);
+  int deficient_from = d;  // first position whose pivot vanishes
+  for (int j = 0; j < d; ++j) {
+    const double* Cj = &C[static_cast<size_t>(order[j]) * d];
+    double djj = Cj[order[j]];
+    for (int k = 0; k < j; ++k) djj -= L[static_cast<size_t>(j) * d + k] * L[static_cast<size_t>(j) * d + k];
+    if (!(djj > kZeroVarTol * Cj[order[j]])) {
+      deficient_from = j;
+      break;
+    }
+    const double ljj = std::sqrt(djj);
+    L[static_cast<size_t>(j) * d + j] = ljj;
+    for (int i = j + 1; i < d; ++i) {
+      double s = C[static_cast<size_t>(order[i]) * d + order[j]];
+      const double* Li = &L[static_cast<size_t>(i) * d];
+      const double* Lj = &L[static_cast<size_t>(j) * d];
+      for (int k = 0; k < j; ++k) s -= Li[k] * Lj[k];
+      L[static_cast<size_t>(i) * d + j] = s / ljj;
+    }
+  }
+  // Regressions of positions p <= deficient_from use the full-rank leading block:
+  // beta solves L_p^T beta = l_p (l_p = L[p, 0:p]), then rescale to original units.
+  for (int i = 0; i < d * d; ++i) B_out[i] = 0.0;
+  *used_pinv = 0;
+  std::vector<double> beta(d);
+  const int full = std::min(d, deficient_from + 1);
+  for (int p = 1; p < full; ++p) {
+    const double* lp = &L[static_cast<size_t>(p) * d];
+    for (int i = p - 1; i >= 0; --i) {
+      double s = lp[i];
+      for (int k = i + 1; k < p; ++k) s -= L[static_cast<size_t>(k) * d + i] * beta[k];
+      beta[i] = s / L[static_cast<size_t>(i) * d + i];
+    }
+    const int t = order[p];
+    for (int q = 0; q < p; ++q) B_out[t + static_cast<int64_t>(d) * order[q]] = beta[q] * msd[2 * t + 1] / msd[2 * order[q] + 1];
+  }
+  // Rank-deficient predecessor designs: minimum-norm solution on the unscaled covariance.
+  for (int p = full; p < d; ++p) {
+    *used_pinv = 1;
+    std::vector<double> A(static_cast<size_t>(p) * p), b(p), x(p);
+    const int t = order[p];
+    for (int i = 0; i < p; ++i) {
+      const int oi = order[i];
+      for (int j = 0; j < p; ++j) {
+        const int oj = order[j];
+        A[static_cast<size_t>(i) * p + j] = C[static_cast<size_t>(oi) * d + oj] * msd[2 * oi + 1] * msd[2 * oj + 1];
+      }
+      b[i] = C[static_cast<size_t>(oi) * d + t] * msd[2 * oi + 1] * msd[2 * t + 1];
+    }
+    pinv_solve_sym(A, p, b.data(), x.data());
+    for (int q = 0; q < p; ++q) B_out[t + static_cast<int64_t>(d) * order[q]] = x[q];
+  }
+  return ok(st);
+}

@@ -1,0 +1,327 @@
+// pymodule.cpp — Python bindings `paper_2403_03772_b200._core`, mirroring the reference's
+// `plingam._core` (proj/bindings/pymodule.cpp:103-144) for the causal-order path, plus
+// an `Engine` handle on the C-ABI for device-resident benchmarking and multi-GPU ranks.
+// numpy arrays are taken column-major (zero-copy when already Fortran-ordered); the GIL is
+// released around every device call.
+#include <pybind11/numpy.h>
+#include <pybind11/pybind11.h>
+#include <pybind11/stl.h>
+
+#include <limits>
+
+#include "../../../include/plingam_b200.h"
+#include "plingam/plingam.hpp"
+#include "plingam/simgen.hpp"
+
+namespace py = pybind11;
+using namespace plingam;
+
+namespace {
+
+using FArray = py::array_t<double, py::array::f_style | py::array::forcecast>;
+
+PyObject* g_error_type = nullptr;
+
+DataMatrix to_data(const FArray& X) {
+  if (X.ndim() != 2) throw Error(ErrorCode::DimensionMismatch, "X must be a 2-D array (samples x variables)");
+  const auto m = static_cast<std::int64_t>(X.shape(0));
+  const auto d = static_cast<std::int64_t>(X.shape(1));
+  std::vector<double> v(X.data(), X.data() + m * d);
+  return DataMatrix(std::move(v), m, d);
+}
+
+py::array_t<double> colmajor_array(const std::vector<double>& v, std::int64_t rows, std::int64_t cols) {
+  py::array_t<double, py::array::f_style> out({rows, cols});
+  std::copy(v.begin(), v.end(), out.mutable_data());
+  return out;
+}
+
+struct Engine {
+  plg_ctx* ctx = nullptr;
+  ~Engine() {
+    if (ctx) plg_ctx_destroy(ctx);
+  }
+};
+
+std::vector<int> engine_causal_order(Engine& e, const FArray& X) {
+  const auto n = static_cast<std::int64_t>(X.shape(0));
+  const auto d = static_cast<int32_t>(X.shape(1));
+  std::vector<int> order(static_cast<std::size_t>(std::max(d, 1)));
+  plg_status st{};
+  int rc;
+  {
+    py::gil_scoped_release rel;
+    rc = plg_causal_order(e.ctx, X.data(), n, d, std::max<std::int64_t>(n, 1), order.data(), &st);
+  }
+  gpu::check(rc, &st);
+  order.resize(static_cast<std::size_t>(d));
+  return order;
+}
+
+}  // namespace
+
+PYBIND11_MODULE(_core, m) {
+  m.doc() = "B200 DirectLiNGAM causal-order engine (sm_100a) behind the plingam API";
+  m.attr("__version__") = "0.1.0";
+  m.attr("engine_version") = plg_version();
+
+  static py::exception<Error> exc(m, "Error");
+  g_error_type = exc.ptr();
+  py::register_exception_translator([](std::exception_ptr p) {
+    try {
+      if (p) std::rethrow_exception(p);
+    } catch (const Error& e) {
+      py::object inst = py::reinterpret_borrow<py::object>(g_error_type)(e.what());
+      inst.attr("code") = to_string(e.code());
+      inst.attr("row") = e.row();
+      inst.attr("col") = e.col();
+      PyErr_SetObject(g_error_type, inst.ptr());
+    }
+  });
+
+  py::class_<WeightedDag>(m, "WeightedDag")
+      .def_property_readonly("weights", [](const WeightedDag& d) { return colmajor_array(d.weights, d.d, d.d); })
+      .def_property_readonly("order", [](const WeightedDag& d) { return d.order.order; })
+      .def_readonly("used_pinv", &WeightedDag::used_pinv)
+      .def("__repr__", [](const WeightedDag& d) { return "<WeightedDag dims=" + std::to_string(d.d) + ">"; });
+
+  // ---- ordering (pymodule.cpp:103-118) ----
+  m.def(
+      "causal_order",
+      [](const FArray& X, bool parallel, int workers) {
+        DataMatrix data = to_data(X);
+        py::gil_scoped_release rel;
+        return causal_order(data, parallel, workers).order;
+      },
+      py::arg("X"), py::arg("parallel") = false, py::arg("workers") = 1,
+      "Recursive causal ordering on the GPU engine (ordering.cpp:213-244).");
+  m.def(
+      "search_causal_order",
+      [](const FArray& X, const std::vector<int>& U, int workers) {
+        DataMatrix data = to_data(X);
+        SearchResult res;
+        {
+          py::gil_scoped_release rel;
+          res = workers > 1 ? search_causal_order_parallel(data, U, workers) : search_causal_order(data, U);
+        }
+        return py::make_tuple(res.chosen, res.scores.scores);
+      },
+      py::arg("X"), py::arg("U"), py::arg("workers") = 1);
+  m.def(
+      "search_causal_order_parallel",
+      [](const FArray& X, const std::vector<int>& U, int workers) {
+        DataMatrix data = to_data(X);
+        SearchResult res;
+        {
+          py::gil_scoped_release rel;
+          res = search_causal_order_parallel(data, U, workers);
+        }
+        return py::make_tuple(res.chosen, res.scores.scores);
+      },
+      py::arg("X"), py::arg("U"), py::arg("workers"));
+  m.def(
+      "regress_out",
+      [](const FArray& X, int exog, const std::vector<int>& remaining) {
+        DataMatrix data = to_data(X);
+        DataMatrix out;
+        {
+          py::gil_scoped_release rel;
+          out = regress_out(data, exog, remaining);
+        }
+        return colmajor_array(out.values, out.rows, out.cols);
+      },
+      py::arg("X"), py::arg("exog"), py::arg("remaining"));
+
+  // ---- DirectLiNGAM (pymodule.cpp:121-135) ----
+  m.def(
+      "fit_direct_lingam",
+      [](const FArray& X, bool parallel, int workers, double edge_threshold) {
+        DataMatrix data = to_data(X);
+        DirectLingamConfig cfg;
+        cfg.parallel = parallel;
+        cfg.workers = workers;
+        cfg.edge_threshold = edge_threshold;
+        DirectLingam model(cfg);
+        py::gil_scoped_release rel;
+        return model.fit(data);
+      },
+      py::arg("X"), py::arg("parallel") = false, py::arg("workers") = 1, py::arg("edge_threshold") = 0.05);
+  m.def(
+      "to_edges",
+      [](const WeightedDag& dag, double threshold) {
+        const EdgeSet e = to_edges(dag, threshold);
+        return std::vector<std::pair<int, int>>(e.edges.begin(), e.edges.end());
+      },
+      py::arg("dag"), py::arg("threshold") = 0.05);
+
+  // ---- device selection / multi-GPU ranks ----
+  m.def("set_device", &gpu::set_device, py::arg("device"));
+  m.def("reset", &gpu::reset);
+  m.def("nccl_unique_id", []() { return py::bytes(gpu::nccl_unique_id()); });
+  m.def(
+      "init_distributed",
+      [](int device, int rank, int world, const py::bytes& uid) {
+        gpu::init_distributed(device, rank, world, std::string(uid));
+      },
+      py::arg("device"), py::arg("rank"), py::arg("world"), py::arg("uid"));
+
+  // ---- synthetic inputs (support; simgen.cpp semantics) ----
+  py::class_<sim::Dag>(m, "SimDag")
+      .def_property_readonly("weights", [](const sim::Dag& d) { return colmajor_array(d.weights, d.d, d.d); })
+      .def_readonly("order", &sim::Dag::order)
+      .def_readonly("dims", &sim::Dag::d);
+  m.def("gen_two_level_dag", &sim::gen_two_level_dag, py::arg("dims"), py::arg("seed") = 0,
+        py::arg("edge_prob") = 0.5);
+  m.def("gen_sparse_dag", &sim::gen_sparse_dag, py::arg("dims"), py::arg("avg_parents") = 2.0,
+        py::arg("seed") = 0, py::arg("wmin") = 0.5, py::arg("wmax") = 1.5);
+  m.def(
+      "sample_lingam",
+      [](const sim::Dag& dag, std::int64_t samples, std::uint64_t seed, std::pair<double, double> noise,
+         const std::string& kind) {
+        sim::NoiseSpec spec;
+        spec.lo = noise.first;
+        spec.hi = noise.second;
+        if (kind == "uniform") spec.kind = sim::NoiseKind::Uniform;
+        else if (kind == "laplace") spec.kind = sim::NoiseKind::Laplace;
+        else if (kind == "t3") spec.kind = sim::NoiseKind::StudentT3;
+        else throw Error(ErrorCode::OutOfRange, "sample_lingam: unknown noise kind " + kind);
+        std::vector<double> X;
+        {
+          py::gil_scoped_release rel;
+          X = sim::sample_lingam(dag, samples, seed, spec);
+        }
+        return colmajor_array(X, samples, dag.d);
+      },
+      py::arg("dag"), py::arg("samples"), py::arg("seed") = 0,
+      py::arg("noise") = std::pair<double, double>{0.0, 1.0}, py::arg("kind") = "uniform");
+
+  // ---- low-level engine handle (bench, sampled-round parity, math probe) ----
+  py::class_<Engine>(m, "Engine")
+      .def(py::init([](int device) {
+             auto e = std::make_unique<Engine>();
+             plg_status st{};
+             gpu::check(plg_ctx_create(device, &e->ctx, &st), &st);
+             return e;
+           }),
+           py::arg("device") = 0)
+      .def_static(
+          "distributed",
+          [](int device, int rank, int world, const py::bytes& uid) {
+            auto e = std::make_unique<Engine>();
+            const std::string id(uid);
+            if (id.size() != 128) throw Error(ErrorCode::OutOfRange, "NCCL id must be 128 bytes");
+            plg_status st{};
+            int rc;
+            {
+              py::gil_scoped_release rel;
+              rc = plg_ctx_create_dist(device, rank, world, id.data(), &e->ctx, &st);
+            }
+            gpu::check(rc, &st);
+            return e;
+          },
+          py::arg("device"), py::arg("rank"), py::arg("world"), py::arg("uid"))
+      .def("causal_order", &engine_causal_order, py::arg("X"))
+      .def(
+          "causal_order_device",
+          [](Engine& e, std::uintptr_t ptr, std::int64_t n, int32_t d, std::int64_t ld) {
+            std::vector<int> order(static_cast<std::size_t>(std::max(d, 1)));
+            plg_status st{};
+            int rc;
+            {
+              py::gil_scoped_release rel;
+              rc = plg_causal_order_device(e.ctx, reinterpret_cast<const double*>(ptr), n, d, ld, order.data(), &st);
+            }
+            gpu::check(rc, &st);
+            order.resize(static_cast<std::size_t>(d));
+            return order;
+          },
+          py::arg("ptr"), py::arg("n"), py::arg("d"), py::arg("ld"))
+      .def(
+          "search",
+          [](Engine& e, const FArray& X, const std::vector<int>& U) {
+            const auto n = static_cast<std::int64_t>(X.shape(0));
+            const auto d = static_cast<int32_t>(X.shape(1));
+            std::vector<double> scores(static_cast<std::size_t>(d));
+            int chosen = -1;
+            plg_status st{};
+            int rc;
+            {
+              py::gil_scoped_release rel;
+              rc = plg_search(e.ctx, X.data(), n, d, std::max<std::int64_t>(n, 1), U.data(),
+                              static_cast<int32_t>(U.size()), &chosen, scores.data(), &st);
+            }
+            gpu::check(rc, &st);
+            return py::make_tuple(chosen, scores);
+          },
+          py::arg("X"), py::arg("U"))
+      .def(
+          "fit_weights",
+          [](Engine& e, const FArray& X, const std::vector<int>& order) {
+            const auto n = static_cast<std::int64_t>(X.shape(0));
+            const auto d = static_cast<int32_t>(X.shape(1));
+            if (static_cast<int32_t>(order.size()) != d) throw Error(ErrorCode::DimensionMismatch, "order size != d");
+            std::vector<double> B(static_cast<std::size_t>(d) * d);
+            int32_t pinv = 0;
+            plg_status st{};
+            int rc;
+            {
+              py::gil_scoped_release rel;
+              rc = plg_fit_weights(e.ctx, X.data(), n, d, n, order.data(), B.data(), &pinv, &st);
+            }
+            gpu::check(rc, &st);
+            return py::make_tuple(colmajor_array(B, d, d), pinv != 0);
+          },
+          py::arg("X"), py::arg("order"))
+      .def(
+          "round_state",
+          [](Engine& e, const FArray& X, int rounds) {
+            const auto n = static_cast<std::int64_t>(X.shape(0));
+            const auto d = static_cast<int32_t>(X.shape(1));
+            std::vector<int> active(static_cast<std::size_t>(d)), prefix(static_cast<std::size_t>(std::max(rounds, 1)));
+            std::vector<double> cols(static_cast<std::size_t>(n) * d);
+            int32_t na = 0;
+            plg_status st{};
+            int rc;
+            {
+              py::gil_scoped_release rel;
+              rc = plg_round_state(e.ctx, X.data(), n, d, n, rounds, active.data(), &na, cols.data(), prefix.data(), &st);
+            }
+            gpu::check(rc, &st);
+            active.resize(static_cast<std::size_t>(na));
+            cols.resize(static_cast<std::size_t>(n) * na);
+            prefix.resize(static_cast<std::size_t>(rounds));
+            return py::make_tuple(active, colmajor_array(cols, n, na), prefix);
+          },
+          py::arg("X"), py::arg("rounds"))
+      .def(
+          "math_probe",
+          [](Engine& e, const py::array_t<double, py::array::c_style | py::array::forcecast>& u) {
+            const auto n = static_cast<std::int64_t>(u.size());
+            py::array_t<double> out({n, static_cast<std::int64_t>(4)});
+            plg_status st{};
+            int rc;
+            {
+              py::gil_scoped_release rel;
+              rc = plg_math_probe(e.ctx, u.data(), n, out.mutable_data(), &st);
+            }
+            gpu::check(rc, &st);
+            return out;
+          },
+          py::arg("u"))
+      .def("stats", [](Engine& e) {
+        plg_stats s{};
+        plg_last_stats(e.ctx, &s);
+        py::dict d;
+        d["total_ms"] = s.total_ms;
+        d["pair_ms"] = s.pair_ms;
+        d["h2d_ms"] = s.h2d_ms;
+        d["pair_evals"] = s.pair_evals;
+        d["ede"] = s.ede;
+        d["launches"] = s.launches;
+        d["rounds"] = s.rounds;
+        d["world"] = s.world;
+        d["h2d_bytes"] = s.h2d_bytes;
+        d["d2h_bytes"] = s.d2h_bytes;
+        return d;
+      });
+}

@@ -1,0 +1,351 @@
+// pair_kernel.cu — the all-pairs residual-entropy kernel and its per-round companions.
+//
+// Replaces the reference's candidate_score inner loop (proj/src/ordering.cpp:78-99 →
+// kernels.cpp:65-85,134-148): for every unordered pair {i, j} of active columns, both
+// residual entropies E(i|j) and E(j|i) are evaluated once (the reference evaluates each
+// twice, once per ordered pair). The pair's slopes and residual standard deviations come
+// from the maintained Gram C (b = C_ij/C_jj, sd = sqrt(C_ii - C_ij b)), so the per-sample
+// work is one residual, two exponentials and one log1p per direction.
+//
+// Work decomposition: a CTA owns one 32x32 tile of (i-block, j-block) positions and one
+// sample segment. 256 threads, each 2x2 pairs x 2 directions = 8 EDE per sample, with
+// per-thread left-to-right sums (the reduction order depends only on (u, n), never on
+// the tile schedule or the GPU count). Column chunks of 64 samples are staged in shared
+// memory by cp.async.bulk (one bulk copy per column chunk, mbarrier complete_tx,
+// double-buffered).
+#include <cuda_runtime.h>
+
+#include "plg_kernels.h"
+#include "plg_math.cuh"
+
+namespace plg {
+
+namespace {
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_addr(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+
+constexpr int kDataDoubles = kStages * 2 * kBT * kCHS;
+constexpr size_t kPairSmem =
+    static_cast<size_t>(kTableBytes) + kDataDoubles * sizeof(double) + 64 + 2 * kBT * sizeof(int);
+
+__global__ void __launch_bounds__(kPairThreads, 1)
+    pair_kernel(const PairLaunch a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  double* s_exp = reinterpret_cast<double*>(smem);
+  double2* s_log = reinterpret_cast<double2*>(smem + kExpN * kExpRep * 8);
+  double* s_data = reinterpret_cast<double*>(smem + kTableBytes);
+  uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + kTableBytes + kDataDoubles * sizeof(double));
+  int* s_col = reinterpret_cast<int*>(s_bar + 8);
+  __shared__ int s_abort;
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  const int tl = blockIdx.x / a.nseg;        // tile within this launch
+  const int seg = blockIdx.x - tl * a.nseg;  // sample segment
+  int bi, bj;
+  tile_decode(a.tile_begin + tl, a.nb, bi, bj);
+  const bool diag = (bi == bj);
+
+  if (tid == 0) s_abort = (*a.err != kNoError);
+  if (tid < 2 * kBT) {
+    const int p = (tid < kBT ? bi : bj) * kBT + (tid & (kBT - 1));
+    s_col[tid] = (p < a.u) ? a.act[p] : -1;
+  }
+  if (tid == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  load_tables(s_exp, s_log, a.g_exp, a.g_log);
+  __syncthreads();
+  if (s_abort) return;
+
+  const int ncols = diag ? kBT : 2 * kBT;
+  // Rows of columns past the active set are zero so they contribute exact zeros.
+  for (int idx = tid; idx < kStages * ncols * kCHS; idx += kPairThreads) {
+    const int st = idx / (ncols * kCHS);
+    const int row = (idx / kCHS) % ncols;
+    if (s_col[row] < 0) s_data[st * 2 * kBT * kCHS + row * kCHS + idx % kCHS] = 0.0;
+  }
+
+  const int64_t t_seg0 = static_cast<int64_t>(seg) * a.seg_len;
+  const int64_t t_seg1 = min(a.n, t_seg0 + a.seg_len);
+  const int nch = static_cast<int>((t_seg1 - t_seg0 + kCH - 1) / kCH);
+
+  auto issue = [&](int c) {  // warp 0: stage chunk c
+    const int st = c & 1;
+    const int64_t t0 = t_seg0 + static_cast<int64_t>(c) * kCH;
+    const int len = static_cast<int>(lmin(kCH, t_seg1 - t0));
+    const uint32_t bytes = static_cast<uint32_t>(((len + 1) & ~1) * sizeof(double));
+    int nvalid = 0;
+    for (int r = 0; r < ncols; ++r) nvalid += (s_col[r] >= 0);
+    if (lane == 0) mbar_expect_tx(&s_bar[st], bytes * nvalid);
+    __syncwarp();
+    for (int r = lane; r < ncols; r += 32) {
+      const int col = s_col[r];
+      if (col >= 0)
+        bulk_g2s(s_data + st * 2 * kBT * kCHS + r * kCHS, a.W + static_cast<int64_t>(col) * a.ldw + t0,
+                 bytes, &s_bar[st]);
+    }
+  };
+
+  // Per-thread pairs: i positions {ti, ti+16}, j positions {tj, tj+16} within the tile.
+  const int ti = (warp >> 1) * 4 + (lane >> 3);
+  const int tj = (warp & 1) * 8 + (lane & 7);
+  double s1[4], bs1[4], s2[4], bs2[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int pi = ti + 16 * (q >> 1);
+    const int pj = tj + 16 * (q & 1);
+    const int ci = s_col[pi];
+    const int cj = s_col[diag ? pj : kBT + pj];
+    const bool valid = (ci >= 0) && (cj >= 0) && (!diag || pi < pj);
+    s1[q] = bs1[q] = s2[q] = bs2[q] = 0.0;
+    if (valid) {
+      const double cii = a.C[static_cast<int64_t>(ci) * a.ldc + ci];
+      const double cjj = a.C[static_cast<int64_t>(cj) * a.ldc + cj];
+      const double cij = a.C[static_cast<int64_t>(ci) * a.ldc + cj];
+      const double b1 = cij / cjj;  // slope of i on j (ordering.cpp:89, cov / col_var[q])
+      const double v1 = cii - cij * b1;
+      const double b2 = cij / cii;  // slope of j on i (ordering.cpp:90)
+      const double v2 = cjj - cij * b2;
+      if (!(v1 > 0.0) || !(v2 > 0.0)) {
+        // exactly collinear pair (e.g. bit-identical standardised columns): the residual
+        // is identically zero and entropy_of_normalized throws (kernels.cpp:136-139)
+        atomicMin(a.err, err_key(a.round, kErrPairCollinear, -1));
+      } else {
+        s1[q] = 1.0 / sqrt(v1);
+        bs1[q] = b1 * s1[q];
+        s2[q] = 1.0 / sqrt(v2);
+        bs2[q] = b2 * s2[q];
+      }
+    }
+  }
+  double lc1[4] = {0, 0, 0, 0}, pd1[4] = {0, 0, 0, 0}, lc2[4] = {0, 0, 0, 0}, pd2[4] = {0, 0, 0, 0};
+  const double* exp_row = s_exp + (lane & (kExpRep - 1));
+  const double2* log_row = s_log + (lane & (kLogRep - 1));
+  const int jrow = diag ? 0 : kBT;
+
+  __syncthreads();  // zero-fill visible before the first chunk is consumed
+  if (warp == 0) {
+    issue(0);
+    if (nch > 1) issue(1);
+  }
+  for (int c = 0; c < nch; ++c) {
+    const int st = c & 1;
+    mbar_wait(&s_bar[st], (c >> 1) & 1);
+    const double* base = s_data + st * 2 * kBT * kCHS;
+    const double* xi0p = base + ti * kCHS;
+    const double* xi1p = base + (ti + 16) * kCHS;
+    const double* xj0p = base + (jrow + tj) * kCHS;
+    const double* xj1p = base + (jrow + tj + 16) * kCHS;
+    const int len = static_cast<int>(lmin(kCH, t_seg1 - (t_seg0 + static_cast<int64_t>(c) * kCH)));
+#pragma unroll 1
+    for (int t = 0; t < len; ++t) {
+      const double xi[2] = {xi0p[t], xi1p[t]};
+      const double xj[2] = {xj0p[t], xj1p[t]};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double x = xi[q >> 1];
+        const double y = xj[q & 1];
+        const double u1 = fma(y, -bs1[q], x * s1[q]);  // (x_i - b_ij x_j) / sd_ij
+        const double u2 = fma(x, -bs2[q], y * s2[q]);  // (x_j - b_ji x_i) / sd_ji
+        ede_accumulate(u1, lc1[q], pd1[q], exp_row, log_row);
+        ede_accumulate(u2, lc2[q], pd2[q], exp_row, log_row);
+      }
+    }
+    __syncthreads();
+    if (warp == 0 && c + 2 < nch) issue(c + 2);
+  }
+
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int slot = (ti + 16 * (q >> 1)) * kBT + tj + 16 * (q & 1);
+    double2* dst = reinterpret_cast<double2*>(
+        a.part + ((static_cast<int64_t>(tl) * a.nseg + seg) * kTilePairs + slot) * 4);
+    dst[0] = make_double2(lc1[q], pd1[q]);
+    dst[1] = make_double2(lc2[q], pd2[q]);
+  }
+}
+
+// Sum the segment partials (ascending) and form both residual entropies of each pair:
+// epack[tile][0][x][y] = E(a_x | b_y), epack[tile][1][y][x] = E(b_y | a_x).
+__global__ void finalize_kernel(const PairLaunch a) {
+  if (*a.err != kNoError) return;
+  const int tl = blockIdx.x;
+  const int slot = blockIdx.y * blockDim.x + threadIdx.x;
+  const int x = slot / kBT, y = slot % kBT;
+  int bi, bj;
+  tile_decode(a.tile_begin + tl, a.nb, bi, bj);
+  const bool valid = (bi * kBT + x < a.u) && (bj * kBT + y < a.u) && (bi != bj || x < y);
+  double e1 = 0.0, e2 = 0.0;
+  if (valid) {
+    double l1 = 0.0, p1 = 0.0, l2 = 0.0, p2 = 0.0;
+    const double* src = a.part + (static_cast<int64_t>(tl) * a.nseg * kTilePairs + slot) * 4;
+    for (int s = 0; s < a.nseg; ++s) {
+      const double2 v1 = reinterpret_cast<const double2*>(src)[0];
+      const double2 v2 = reinterpret_cast<const double2*>(src)[1];
+      l1 += v1.x;
+      p1 += v1.y;
+      l2 += v2.x;
+      p2 += v2.y;
+      src += static_cast<int64_t>(kTilePairs) * 4;
+    }
+    const double inv_n = 1.0 / static_cast<double>(a.n);
+    e1 = entropy_from_sums(l1, p1, inv_n);
+    e2 = entropy_from_sums(l2, p2, inv_n);
+  }
+  double* tile = a.epack + static_cast<int64_t>(a.tile_begin + tl) * 2 * kTilePairs;
+  tile[x * kBT + y] = e1;
+  tile[kTilePairs + y * kBT + x] = e2;
+}
+
+constexpr int kColentThreads = 256;
+
+// H_p = entropy_approx(standardised column) (ordering.cpp:65; kernels.cpp:123-132).
+__global__ void __launch_bounds__(kColentThreads)
+    colent_kernel(const double* W, int64_t ldw, int64_t n, const double* C, int64_t ldc,
+                  const int* act, int u, double* H, const double* g_exp, const double2* g_log,
+                  const int* nz, const int* col_var, int round, unsigned long long* err) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  double* s_exp = reinterpret_cast<double*>(smem);
+  double2* s_log = reinterpret_cast<double2*>(smem + kExpN * kExpRep * 8);
+  __shared__ double s_red[2][kColentThreads / 32];
+  if (*err != kNoError) return;
+  load_tables(s_exp, s_log, g_exp, g_log);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double* exp_row = s_exp + (lane & (kExpRep - 1));
+  const double2* log_row = s_log + (lane & (kLogRep - 1));
+  for (int p = blockIdx.x; p < u; p += gridDim.x) {
+    const int col = act[p];
+    const double ccc = C[static_cast<int64_t>(col) * ldc + col];
+    if (round > 0 && threadIdx.x == 0 && (nz[col] != round || !(ccc > 0.0)))
+      atomicMin(err, err_key(round, kErrColZeroVar, col_var[col]));  // ordering.cpp:56-62
+    const double inv_sd = 1.0 / sqrt(ccc);
+    const double* w = W + static_cast<int64_t>(col) * ldw;
+    double lc = 0.0, pd = 0.0;
+    for (int64_t t = threadIdx.x; t < n; t += kColentThreads) ede_accumulate(w[t] * inv_sd, lc, pd, exp_row, log_row);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      lc += __shfl_xor_sync(0xffffffffu, lc, o);
+      pd += __shfl_xor_sync(0xffffffffu, pd, o);
+    }
+    if (lane == 0) {
+      s_red[0][warp] = lc;
+      s_red[1][warp] = pd;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double l = 0.0, q = 0.0;
+      for (int w2 = 0; w2 < kColentThreads / 32; ++w2) {
+        l += s_red[0][w2];
+        q += s_red[1][w2];
+      }
+      H[p] = entropy_from_sums(l, q, 1.0 / static_cast<double>(n));
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void math_probe_kernel(const double* u, int64_t n, double* out, const double* g_exp,
+                                  const double2* g_log) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  double* s_exp = reinterpret_cast<double*>(smem);
+  double2* s_log = reinterpret_cast<double2*>(smem + kExpN * kExpRep * 8);
+  load_tables(s_exp, s_log, g_exp, g_log);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double v = u[i];
+    double lc = 0.0, pd = 0.0;
+    ede_accumulate(v, lc, pd, s_exp + (lane & (kExpRep - 1)), s_log + (lane & (kLogRep - 1)));
+    const double a = fabs(v);
+    out[4 * i + 0] = lc;
+    out[4 * i + 1] = pd;
+    out[4 * i + 2] = a + (log1p(exp(-2.0 * a)) - kLn2);  // libdevice, kernels.cpp:22-23
+    out[4 * i + 3] = v * exp(-0.5 * (v * v));            // kernels.cpp:24
+  }
+}
+
+}  // namespace
+
+void launch_pair(const PairLaunch& a, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(kPairSmem));
+    attr = true;
+  }
+  pair_kernel<<<a.ntiles * a.nseg, kPairThreads, kPairSmem, s>>>(a);
+}
+
+void launch_finalize(const PairLaunch& a, cudaStream_t s) {
+  finalize_kernel<<<dim3(a.ntiles, kTilePairs / 256), 256, 0, s>>>(a);
+}
+
+void launch_colent(const double* W, int64_t ldw, int64_t n, const double* C, int64_t ldc,
+                   const int* act, int u, double* H, const double* g_exp, const double2* g_log,
+                   const int* nz, const int* col_var, int round, unsigned long long* err,
+                   cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(colent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTableBytes);
+    attr = true;
+  }
+  const int grid = u < 4 * 148 ? u : 4 * 148;
+  colent_kernel<<<grid, kColentThreads, kTableBytes, s>>>(W, ldw, n, C, ldc, act, u, H, g_exp,
+                                                          g_log, nz, col_var, round, err);
+}
+
+void launch_math_probe(const double* u, int64_t n, double* out, const double* g_exp,
+                       const double2* g_log, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(math_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kTableBytes);
+    attr = true;
+  }
+  int grid = static_cast<int>((n + 255) / 256);
+  if (grid > 1184) grid = 1184;
+  if (grid < 1) grid = 1;
+  math_probe_kernel<<<grid, 256, kTableBytes, s>>>(u, n, out, g_exp, g_log);
+}
+
+}  // namespace plg

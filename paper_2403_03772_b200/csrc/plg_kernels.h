@@ -1,0 +1,119 @@
+// plg_kernels.h — launchers for the sm_100a kernels of the causal-order engine.
+// Internal to libplingam_b200.so (the C-ABI in include/plingam_b200.h is the boundary).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace plg {
+
+constexpr int kBT = 32;           // active positions per tile side
+constexpr int kTilePairs = kBT * kBT;
+constexpr int kPairThreads = 256;
+constexpr int kCH = 64;           // samples per shared-memory stage
+constexpr int kCHS = kCH + 2;     // padded column stride in shared memory (doubles)
+constexpr int kStages = 2;
+constexpr int kSegMin = 256;      // smallest sample segment per CTA
+
+// Error key: first error in the reference's raising order (ordering.cpp build_cache
+// before candidate_score, rounds ascending). key = round<<40 | kind<<32 | (col+1).
+constexpr unsigned long long kNoError = ~0ull;
+enum ErrKind : unsigned { kErrColZeroVar = 0, kErrPairCollinear = 1 };
+
+__host__ __device__ inline unsigned long long err_key(int round, unsigned kind, int col) {
+  return (static_cast<unsigned long long>(round) << 40) |
+         (static_cast<unsigned long long>(kind) << 32) | static_cast<unsigned>(col + 1);
+}
+
+struct RoundState {  // device-resident per-round scalars
+  int chosen_pos;
+  int chosen_col;
+};
+
+// Column-major tile upper triangle: tile index -> (bi, bj), bi <= bj.
+__host__ __device__ inline void tile_decode(int t, int nb, int& bi, int& bj) {
+  int row = 0, start = 0;
+  while (t >= start + (nb - row)) {
+    start += nb - row;
+    ++row;
+  }
+  bi = row;
+  bj = row + (t - start);
+}
+
+struct PairLaunch {
+  const double* W;
+  int64_t ldw;
+  int64_t n;
+  const double* C;
+  int64_t ldc;
+  const int* act;
+  int u;
+  int nb;
+  int tile_begin;  // global tile index of this launch's first tile
+  int ntiles;      // tiles in this launch
+  int seg_len;
+  int nseg;
+  double* part;    // [ntiles][nseg][kTilePairs][4]
+  double* epack;   // [global tiles][2][kBT][kBT]
+  const double* g_exp;
+  const double2* g_log;
+  unsigned long long* err;
+  int round;
+};
+
+void launch_pair(const PairLaunch& a, cudaStream_t s);
+void launch_finalize(const PairLaunch& a, cudaStream_t s);
+
+// H[p] = entropy(w_col / sqrt(C_col,col)) for active positions p < u. For round > 0 it
+// is also build_cache's ZeroVariance(col) check (ordering.cpp:56-62): a column whose
+// residualisation left it identically zero (nz[col] != round) or whose partial variance
+// is not positive.
+void launch_colent(const double* W, int64_t ldw, int64_t n, const double* C, int64_t ldc,
+                   const int* act, int u, double* H, const double* g_exp, const double2* g_log,
+                   const int* nz, const int* col_var, int round, unsigned long long* err,
+                   cudaStream_t s);
+
+// Validation + round-0 standardisation with the reference's left-to-right sums
+// (types.cpp:21-47, kernels.cpp:44-57,92-104). col_map[c] = source column of local c.
+// stat[c] = {first non-finite row or -1, zero-variance flag}.
+// msd (optional): {mean, sd} per column.
+void launch_standardize(const double* X, int64_t ldx, int64_t n, const int* col_map, int ncol,
+                        double* W, int64_t ldw, int* stat, double* msd, int check_finite,
+                        cudaStream_t s);
+
+// C = W^T W / n (FP64, symmetric, deterministic order).
+void launch_gram(const double* W, int64_t ldw, int64_t n, int ncol, double* C, int64_t ldc,
+                 cudaStream_t s);
+
+// k[p] = sum_{q != p} min(0, M_pq)^2 with M_pq = (H_q + E(p|q)) - (H_p + E(q|p)).
+void launch_kreduce(const double* epack, const double* H, int u, int nb, double* k,
+                    const unsigned long long* err, cudaStream_t s);
+
+// argmin over k (lowest position on ties), order/score bookkeeping, active-list compaction.
+void launch_commit(const double* k, const int* act_cur, int* act_nxt, int u, const int* col_var,
+                   int* order, int round, double* scores, RoundState* rs,
+                   const unsigned long long* err, cudaStream_t s);
+
+// Rank-1 Schur update of the remaining Gram block.
+void launch_update_gram(double* C, int64_t ldc, const int* act_nxt, int ur, const RoundState* rs,
+                        const unsigned long long* err, cudaStream_t s);
+
+// In-place residualisation w_r -= (C_rm / C_mm) w_m of the remaining columns; nz[r] = tag
+// when the new column has a nonzero entry.
+void launch_residualize(double* W, int64_t ldw, int64_t n, const double* C, int64_t ldc,
+                        const int* act_nxt, int ur, const RoundState* rs, int* nz, int tag,
+                        const unsigned long long* err, cudaStream_t s);
+
+// Reference regress_out (ordering.cpp:178-211): raw columns, fresh means, bit-exact.
+void launch_regress_out(const double* X, int64_t ldx, int64_t n, int exog, const int* remaining,
+                        int r, double* out, int64_t ldo, int* zero_var_flag, cudaStream_t s);
+
+// Test hook: evaluate lc/pdf element functions on a vector (custom and libdevice).
+void launch_math_probe(const double* u, int64_t n, double* out, const double* g_exp,
+                       const double2* g_log, cudaStream_t s);
+
+}  // namespace plg
+
+namespace plg {
+__host__ __device__ inline int64_t lmin(int64_t a, int64_t b) { return a < b ? a : b; }
+}  // namespace plg

@@ -1,0 +1,221 @@
+"""ctypes wrapper of the CPU oracle (oracle/liboracle.so) — test infrastructure only.
+
+The oracle restates the reference hot path (proj/src/kernels.cpp, ordering.cpp,
+types.cpp, direct_lingam.cpp) in C; see oracle/plingam_oracle.h. Only tests/,
+__graft_entry__.smoke() and bench.py's CPU-baseline leg load it.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ORACLE_DIR = os.path.join(ROOT, "oracle")
+LIB_PATH = os.path.join(ORACLE_DIR, "liboracle.so")
+
+ERROR_NAMES = [
+    "NonFinite", "ZeroVariance", "TooFewSamples", "TooShort", "LengthMismatch",
+    "DimensionMismatch", "EmptyCandidates", "SingularDesign", "InsufficientRows",
+    "UnstableSystem", "OutOfRange", "InvalidIndex",
+]
+
+
+class OracleError(Exception):
+    def __init__(self, code: int, row: int, col: int, msg: str):
+        super().__init__(msg)
+        self.code = ERROR_NAMES[code - 1] if 1 <= code <= len(ERROR_NAMES) else str(code)
+        self.row = row
+        self.col = col
+
+
+class _Status(ctypes.Structure):
+    _fields_ = [("code", ctypes.c_int32), ("row", ctypes.c_int64), ("col", ctypes.c_int64),
+                ("msg", ctypes.c_char * 256)]
+
+
+_D = ctypes.POINTER(ctypes.c_double)
+_I = ctypes.POINTER(ctypes.c_int32)
+
+
+def build() -> str:
+    src = [os.path.join(ORACLE_DIR, f) for f in ("plingam_oracle.c", "plingam_oracle.h", "Makefile")]
+    if not os.path.exists(LIB_PATH) or any(os.path.getmtime(s) > os.path.getmtime(LIB_PATH) for s in src):
+        subprocess.run(["make", "-C", ORACLE_DIR], check=True, capture_output=True)
+    return LIB_PATH
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        L = ctypes.CDLL(build())
+        L.orc_gaussian_entropy.restype = ctypes.c_double
+        for name in ("orc_mean", "orc_variance_pop", "orc_std_pop", "orc_entropy_approx"):
+            getattr(L, name).restype = ctypes.c_double
+            getattr(L, name).argtypes = [_D, ctypes.c_int64]
+        L.orc_covariance_pop.restype = ctypes.c_double
+        L.orc_covariance_pop.argtypes = [_D, _D, ctypes.c_int64]
+        L.orc_log_cosh.restype = ctypes.c_double
+        L.orc_log_cosh.argtypes = [ctypes.c_double]
+        _lib = L
+    return _lib
+
+
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(_D)
+
+
+def _ip(a: np.ndarray):
+    return a.ctypes.data_as(_I)
+
+
+def _check(rc: int, st: _Status):
+    if rc:
+        raise OracleError(st.code, st.row, st.col, st.msg.decode())
+
+
+def _col(x) -> np.ndarray:
+    return np.ascontiguousarray(x, dtype=np.float64)
+
+
+def _mat(X) -> np.ndarray:
+    return np.asfortranarray(X, dtype=np.float64)
+
+
+def mean(x):
+    x = _col(x)
+    return lib().orc_mean(_dp(x), x.size)
+
+
+def variance_pop(x):
+    x = _col(x)
+    return lib().orc_variance_pop(_dp(x), x.size)
+
+
+def std_pop(x):
+    x = _col(x)
+    return lib().orc_std_pop(_dp(x), x.size)
+
+
+def covariance_pop(x, y):
+    x, y = _col(x), _col(y)
+    return lib().orc_covariance_pop(_dp(x), _dp(y), x.size)
+
+
+def log_cosh(u: float) -> float:
+    return lib().orc_log_cosh(float(u))
+
+
+def gaussian_entropy() -> float:
+    return lib().orc_gaussian_entropy()
+
+
+def standardize(x) -> np.ndarray:
+    x = _col(x)
+    out = np.empty_like(x)
+    st = _Status()
+    _check(lib().orc_standardize(_dp(x), ctypes.c_int64(x.size), _dp(out), ctypes.byref(st)), st)
+    return out
+
+
+def residual(xi, xj) -> np.ndarray:
+    xi, xj = _col(xi), _col(xj)
+    if xi.size != xj.size:
+        raise OracleError(5, -1, -1, "residual: length mismatch")
+    out = np.empty_like(xi)
+    st = _Status()
+    _check(lib().orc_residual(_dp(xi), _dp(xj), ctypes.c_int64(xi.size), _dp(out), ctypes.byref(st)), st)
+    return out
+
+
+def entropy_approx(u) -> float:
+    u = _col(u)
+    return lib().orc_entropy_approx(_dp(u), u.size)
+
+
+def entropy_of_normalized(r) -> float:
+    r = _col(r)
+    out = ctypes.c_double()
+    st = _Status()
+    _check(lib().orc_entropy_of_normalized(_dp(r), ctypes.c_int64(r.size), ctypes.byref(out), ctypes.byref(st)), st)
+    return out.value
+
+
+def diff_mutual_info(xi, xj, ri_j, rj_i) -> float:
+    a = [_col(v) for v in (xi, xj, ri_j, rj_i)]
+    if len({v.size for v in a}) != 1:
+        raise OracleError(5, -1, -1, "diff_mutual_info: length mismatch")
+    out = ctypes.c_double()
+    st = _Status()
+    _check(lib().orc_diff_mutual_info(*[_dp(v) for v in a], ctypes.c_int64(a[0].size), ctypes.byref(out),
+                                      ctypes.byref(st)), st)
+    return out.value
+
+
+def validate(X) -> None:
+    X = _mat(X)
+    st = _Status()
+    n, d = X.shape
+    _check(lib().orc_validate(_dp(X), ctypes.c_int64(n), ctypes.c_int32(d), ctypes.c_int64(max(n, 1)),
+                              ctypes.byref(st)), st)
+
+
+def search_causal_order(X, U, workers: int = 1, fast: bool = False):
+    X = _mat(X)
+    n, d = X.shape
+    U = np.ascontiguousarray(U, dtype=np.int32)
+    chosen = ctypes.c_int32(-1)
+    scores = np.empty(d, dtype=np.float64)
+    st = _Status()
+    _check(lib().orc_search_causal_order(_dp(X), ctypes.c_int64(n), ctypes.c_int32(d), ctypes.c_int64(max(n, 1)),
+                                         _ip(U), ctypes.c_int32(U.size), ctypes.c_int32(workers),
+                                         ctypes.c_int32(1 if fast else 0), ctypes.byref(chosen), _dp(scores),
+                                         ctypes.byref(st)), st)
+    return chosen.value, scores
+
+
+def regress_out(X, exog: int, remaining) -> np.ndarray:
+    X = _mat(X)
+    n, d = X.shape
+    rem = np.ascontiguousarray(remaining, dtype=np.int32)
+    out = np.empty((n, rem.size), dtype=np.float64, order="F")
+    st = _Status()
+    _check(lib().orc_regress_out(_dp(X), ctypes.c_int64(n), ctypes.c_int32(d), ctypes.c_int64(max(n, 1)),
+                                 ctypes.c_int32(exog), _ip(rem), ctypes.c_int32(rem.size), _dp(out),
+                                 ctypes.byref(st)), st)
+    return out
+
+
+def causal_order(X, parallel: bool = False, workers: int = 1, fast: bool = False, max_rounds: int = -1,
+                 return_scores: bool = False):
+    X = _mat(X)
+    n, d = X.shape
+    order = np.full(max(d, 1), -1, dtype=np.int32)
+    rounds = (d - 1) if max_rounds < 0 else min(max_rounds, max(d - 1, 0))
+    scores = np.zeros((max(rounds, 1), max(d, 1)), dtype=np.float64) if return_scores else None
+    st = _Status()
+    _check(lib().orc_causal_order(_dp(X), ctypes.c_int64(n), ctypes.c_int32(d), ctypes.c_int64(max(n, 1)),
+                                  ctypes.c_int32(1 if parallel else 0), ctypes.c_int32(workers),
+                                  ctypes.c_int32(1 if fast else 0), ctypes.c_int32(max_rounds), _ip(order),
+                                  _dp(scores) if return_scores else None, ctypes.byref(st)), st)
+    nout = d if max_rounds < 0 or rounds == d - 1 else rounds
+    out = [int(v) for v in order[:nout]]
+    return (out, scores[:rounds]) if return_scores else out
+
+
+def fit_weights(X, order):
+    X = _mat(X)
+    n, d = X.shape
+    o = np.ascontiguousarray(order, dtype=np.int32)
+    B = np.zeros((d, d), dtype=np.float64, order="F")
+    pinv = ctypes.c_int32(0)
+    st = _Status()
+    _check(lib().orc_fit_weights(_dp(X), ctypes.c_int64(n), ctypes.c_int32(d), ctypes.c_int64(n), _ip(o), _dp(B),
+                                 ctypes.byref(pinv), ctypes.byref(st)), st)
+    return B, bool(pinv.value)

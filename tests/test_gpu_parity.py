@@ -1,0 +1,264 @@
+"""GPU parity: the sm_100a engine against the CPU oracle and the committed goldens.
+
+Bar (BASELINE.json north_star): the causal order is identical (integer, bit-exact,
+lowest-index ties); candidate scores agree to 1e-9 relative; B agrees to 1e-6 relative;
+round-0 standardisation and regress_out are bit-identical to the reference's sums.
+Everything goes through the C-ABI (libplingam_b200.so) via the Python bindings.
+"""
+
+import hashlib
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from conftest import random_matrix, two_level_data
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def digest(X):
+    return hashlib.sha256(np.asfortranarray(X).tobytes(order="F")).hexdigest()
+
+
+def scores_close(a, b, rel=1e-9, abs_=1e-15):
+    a, b = np.asarray(a), np.asarray(b)
+    fin = np.isfinite(b)
+    assert np.array_equal(np.isfinite(a), fin)
+    return np.all(np.abs(a[fin] - b[fin]) <= rel * np.abs(b[fin]) + abs_)
+
+
+# ------------------------------------------------------------------ element math
+
+def test_math_probe_matches_libdevice_and_numpy(engine):
+    rng = np.random.default_rng(0)
+    u = np.concatenate([
+        np.linspace(-45.0, 45.0, 200001), rng.normal(size=100000), rng.laplace(size=100000) * 3,
+        np.array([0.0, -0.0, 1e-300, -1e-300, 5e-324, 1e-8, 0.5, 1.0, 2.0, 38.0, 40.0, 41.0, 100.0, 316.0,
+                  1000.0, -1000.0, 3e4, 4.6e4]),
+    ])
+    out = engine.math_probe(u)
+    lc, pdf, lc_ld, pdf_ld = out[:, 0], out[:, 1], out[:, 2], out[:, 3]
+    a = np.abs(u)
+    lc_np = a + (np.log1p(np.exp(-2.0 * a)) - math.log(2.0))
+    pdf_np = u * np.exp(-0.5 * (u * u))
+    err_lc = np.abs(lc - lc_np)
+    err_pdf = np.abs(pdf - pdf_np)
+    # table-driven FP64 path: a few ulp absolute (lc magnitude up to ~|u|)
+    assert np.all(err_lc <= 4e-16 * np.maximum(1.0, np.abs(lc_np)) + 2e-15), err_lc.max()
+    assert np.all(err_pdf <= 2e-15), err_pdf.max()
+    assert np.all(np.abs(lc_ld - lc_np) <= 4e-16 * np.maximum(1.0, np.abs(lc_np)) + 1e-15)
+    assert np.all(np.abs(pdf_ld - pdf_np) <= 1e-15)
+    assert lc[u == 0.0][0] == 0.0 and pdf[u == 0.0][0] == 0.0
+    # exact sign symmetry of the element functions (entropy sign-flip invariance)
+    pos = out[(u > 0)]
+    neg = engine.math_probe(-u[u > 0])
+    assert np.array_equal(pos[:, 0], neg[:, 0]) and np.array_equal(pos[:, 1], -neg[:, 1])
+
+
+# ------------------------------------------------------------------ kernels
+
+def test_round0_standardisation_bit_exact(engine, oracle):
+    rng = np.random.default_rng(3)
+    X = np.asfortranarray(rng.laplace(size=(4097, 7)) * rng.uniform(0.1, 100, 7) + rng.uniform(-5, 5, 7))
+    active, cols, prefix = engine.round_state(X, 0)
+    assert active == list(range(7)) and prefix == []
+    for j in range(7):
+        assert cols[:, j].tobytes() == oracle.standardize(X[:, j]).tobytes()
+
+
+def test_regress_out_bit_exact(plg, oracle):
+    rng = np.random.default_rng(19)
+    for _ in range(10):
+        d = 3 + int(rng.uniform() * 5)
+        X = random_matrix(rng, d, 400 + int(rng.uniform() * 600))
+        exog = int(rng.uniform() * d)
+        rem = [j for j in range(d) if j != exog]
+        assert plg.regress_out(X, exog, rem).tobytes() == oracle.regress_out(X, exog, rem).tobytes()
+
+
+# ------------------------------------------------------------------ one search round
+
+def test_search_singleton(plg):  # test_ordering.cpp:60-68
+    X = random_matrix(np.random.default_rng(1), 3, 50)
+    chosen, scores = plg.search_causal_order(X, [2])
+    assert chosen == 2 and scores[2] == 0.0 and math.isinf(scores[0])
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_search_parity_random(plg, oracle, seed):
+    rng = np.random.default_rng(5000 + seed)
+    d = 2 + int(rng.uniform() * 60)
+    m = 100 + int(rng.uniform() * 3000)
+    X = random_matrix(rng, d, m)
+    U = list(range(d))
+    c_ref, s_ref = oracle.search_causal_order(X, U, workers=8, fast=True)
+    c, s = plg.search_causal_order(X, U)
+    assert c == c_ref
+    assert scores_close(s, s_ref)
+    assert np.all(np.asarray(s) <= 0.0)
+
+
+def test_search_subset_and_unsorted_candidates(plg, oracle):
+    rng = np.random.default_rng(77)
+    X = random_matrix(rng, 40, 1500)
+    U = [37, 3, 11, 20, 0, 39, 5, 16, 28, 33]
+    c_ref, s_ref = oracle.search_causal_order(X, U, workers=8)
+    c, s = plg.search_causal_order(X, U)
+    assert c == c_ref and scores_close(s, s_ref)
+
+
+def test_search_two_level_validation_size(plg, oracle):  # test_ordering.cpp:169-179
+    for seed in range(99, 109):
+        X = two_level_data(plg, seed, 10, 10000)
+        c_ref, s_ref = oracle.search_causal_order(X, list(range(10)), workers=8)
+        c, s = plg.search_causal_order(X, list(range(10)))
+        assert c == c_ref and scores_close(s, s_ref)
+
+
+def test_search_scale_invariance(plg):  # test_ordering.cpp:181-193
+    rng = np.random.default_rng(13)
+    for _ in range(20):
+        d = 3 + int(rng.uniform() * 5)
+        X = random_matrix(rng, d, 300)
+        before = plg.search_causal_order(X, list(range(d)))[0]
+        X[:, int(rng.uniform() * d)] *= rng.uniform(0.1, 50.0)
+        assert plg.search_causal_order(X, list(range(d)))[0] == before
+
+
+# ------------------------------------------------------------------ full causal order
+
+def test_c1_golden_orders_and_weights(plg):
+    """BASELINE configs[0]: 50 AC1 seeds (acceptance.cpp:39-69), order + B vs the oracle."""
+    with open(os.path.join(GOLDEN, "c1_two_level.json")) as f:
+        fx = json.load(f)
+    for case in fx["cases"]:
+        dag = plg.gen_two_level_dag(10, seed=case["seed"])
+        X = plg.sample_lingam(dag, 10000, seed=case["seed"])
+        assert digest(X) == case["sha256"]
+        fit = plg.fit_direct_lingam(X)
+        assert fit.order == case["order"], case["seed"]
+        B_ref = np.asarray(case["B"])
+        assert np.all(np.abs(fit.weights - B_ref) <= 1e-6 * np.maximum(1.0, np.abs(B_ref)))
+        assert fit.used_pinv == case["used_pinv"]
+
+
+def test_c2_golden_order(plg):
+    """BASELINE configs[1]: sparse DAG d=100, n=10000, Laplace noise."""
+    with open(os.path.join(GOLDEN, "c2_order.json")) as f:
+        fx = json.load(f)
+    dag = plg.gen_sparse_dag(100, avg_parents=2.0, seed=1)
+    X = plg.sample_lingam(dag, 10000, seed=1, noise=(0.0, 1.0), kind="laplace")
+    assert digest(X) == fx["sha256"]
+    fit = plg.fit_direct_lingam(X)
+    assert fit.order == fx["order"]
+    B_ref = np.asarray(fx["B"])
+    assert np.all(np.abs(fit.weights - B_ref) <= 1e-6 * np.maximum(1.0, np.abs(B_ref)))
+    c, s = plg.search_causal_order(X, list(range(100)))
+    assert c == fx["order"][0] and scores_close(s, fx["round0_scores"])
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_causal_order_parity_random(plg, oracle, seed):  # test_ordering.cpp:342-352 shapes
+    rng = np.random.default_rng(8000 + seed)
+    d = 3 + int(rng.uniform() * 40)
+    X = random_matrix(rng, d, 500 + int(rng.uniform() * 2000))
+    assert plg.causal_order(X) == oracle.causal_order(X, parallel=True, workers=8, fast=True)
+
+
+def test_sampled_rounds_against_oracle(engine, oracle, plg):
+    """SURVEY.md §8d sampled-round protocol: the GPU's working state after r rounds, searched
+    by the oracle, must give the GPU's next choice; the scores agree to 1e-9."""
+    dag = plg.gen_sparse_dag(120, avg_parents=2.0, seed=9)
+    X = plg.sample_lingam(dag, 6000, seed=9, noise=(0.0, 1.0), kind="laplace")
+    full = engine.causal_order(X)
+    for r in (0, 1, 2, 10, 60, 117):
+        active, cols, prefix = engine.round_state(X, r)
+        assert prefix == full[:r]
+        c_ref, s_ref = oracle.search_causal_order(cols, list(range(len(active))), workers=8, fast=True)
+        assert active[c_ref] == full[r]
+        _, s_gpu = engine.search(cols, list(range(len(active))))
+        assert scores_close(s_gpu, s_ref, rel=1e-8)
+
+
+def test_causal_order_properties_mid_scale(engine, plg):
+    """Size-independent properties at d=600: permutation, determinism, chain respect."""
+    dag = plg.gen_sparse_dag(600, avg_parents=2.0, seed=3)
+    X = plg.sample_lingam(dag, 8000, seed=3, noise=(0.0, 1.0), kind="laplace")
+    o1 = engine.causal_order(X)
+    o2 = engine.causal_order(X)
+    assert o1 == o2 and sorted(o1) == list(range(600))
+    st = engine.stats()
+    assert st["rounds"] == 599 and st["pair_evals"] == 601 * 600 * 599 // 3
+    # device-resident entry gives the same order
+    import torch
+
+    dX = torch.from_numpy(np.ascontiguousarray(X.T)).cuda()  # rows of X.T = columns of X
+    assert engine.causal_order_device(dX.data_ptr(), 8000, 600, 8000) == o1
+
+
+# ------------------------------------------------------------------ error paths
+
+def test_error_paths(plg):
+    rng = np.random.default_rng(15)
+    X = random_matrix(rng, 3, 50)
+    for U, code in (([], "EmptyCandidates"), ([0, 3], "InvalidIndex"), ([0, 0], "InvalidIndex")):
+        with pytest.raises(plg.Error) as e:
+            plg.search_causal_order(X, U)
+        assert e.value.code == code
+    with pytest.raises(plg.Error) as e:
+        plg.search_causal_order_parallel(X, [0, 1], 0)
+    assert e.value.code == "OutOfRange"
+    Xc = X.copy(order="F")
+    Xc[:, 1] = 4.0
+    with pytest.raises(plg.Error) as e:
+        plg.search_causal_order(Xc, [0, 1, 2])
+    assert e.value.code == "ZeroVariance" and e.value.col == 1
+    with pytest.raises(plg.Error) as e:
+        plg.causal_order(Xc)
+    assert e.value.code == "ZeroVariance" and e.value.col == 1
+    Xn = X.copy(order="F")
+    Xn[7, 2] = np.nan
+    with pytest.raises(plg.Error) as e:
+        plg.causal_order(Xn)
+    assert e.value.code == "NonFinite" and (e.value.row, e.value.col) == (7, 2)
+    with pytest.raises(plg.Error) as e:
+        plg.causal_order(X, workers=0)
+    assert e.value.code == "OutOfRange"
+    assert plg.causal_order(np.array([[1.0], [2.0], [3.0]])) == [0]
+    with pytest.raises(plg.Error) as e:
+        plg.regress_out(X, 0, [0, 1])
+    assert e.value.code == "InvalidIndex"
+    with pytest.raises(plg.Error) as e:
+        plg.regress_out(X, 5, [0])
+    assert e.value.code == "InvalidIndex"
+
+
+def test_collinear_duplicate_raises(plg):  # test_ordering.cpp:271-281
+    X = random_matrix(np.random.default_rng(25), 3, 100)
+    X[:, 2] = X[:, 0]
+    with pytest.raises(plg.Error) as e:
+        plg.causal_order(X)
+    assert e.value.code == "ZeroVariance"
+
+
+def test_chain_weight(plg):  # test_direct_lingam.cpp:22-33
+    rng = np.random.default_rng(42)
+    x0 = rng.uniform(size=10000)
+    X = np.stack([x0, 0.8 * x0 + rng.uniform(size=10000)], axis=1)
+    fit = plg.fit_direct_lingam(X)
+    assert fit.order == [0, 1] and abs(fit.weights[1, 0] - 0.8) <= 0.05 and fit.weights[0, 1] == 0.0
+
+
+def test_pinv_fallback(plg, oracle):  # test_direct_lingam.cpp:96-113
+    rng = np.random.default_rng(77)
+    u, w = rng.uniform(-1, 1, 400), rng.uniform(-1, 1, 400)
+    X = np.stack([u, w, u + w, u - w], axis=1)
+    engine = plg.Engine(0)
+    B, pinv = engine.fit_weights(X, [0, 1, 2, 3])
+    B_ref, pinv_ref = oracle.fit_weights(X, [0, 1, 2, 3])
+    assert pinv and pinv_ref and np.all(np.isfinite(B))
+    assert np.allclose(B, B_ref, atol=1e-6)

@@ -1,0 +1,414 @@
+"""Pin the CPU oracle to the reference's own known answers and contracts.
+
+The reference cannot be compiled here (Eigen3 is absent), so the oracle
+(oracle/plingam_oracle.c) is checked against every golden value and property the
+reference's tests hold for the hot path:
+  proj/tests/test_kernels.cpp   (KATs, properties, statistics)
+  proj/tests/test_ordering.cpp  (naive composition, singleton, sign, parallel identity,
+                                 scale invariance, error paths, regress_out, orders)
+  proj/tests/test_direct_lingam.cpp (weights)
+CPU only.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import random_matrix, two_level_data
+
+
+# ---------------------------------------------------------------- kernels (test_kernels.cpp)
+
+def test_standardize_kat(oracle):  # test_kernels.cpp:12-21
+    s = oracle.standardize([1.0, 2.0, 3.0])
+    assert s[0] == pytest.approx(-1.224744871391589, rel=1e-9)
+    assert abs(s[1]) <= 1e-12
+    assert s[2] == pytest.approx(1.224744871391589, rel=1e-9)
+    assert abs(oracle.mean(s)) <= 1e-12
+    assert oracle.std_pop(s) == pytest.approx(1.0, rel=1e-12)
+
+
+def test_standardize_idempotent(oracle):  # :23-31
+    rng = np.random.default_rng(11)
+    x = rng.uniform(-3.0, 7.0, 500)
+    once = oracle.standardize(x)
+    twice = oracle.standardize(once)
+    assert np.all(np.abs(twice - once) <= 1e-12 * np.maximum(1.0, np.abs(once)))
+
+
+def test_standardize_errors(oracle):  # :33-37
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.standardize([5.0, 5.0, 5.0])
+    assert e.value.code == "ZeroVariance" and str(e.value) == "standardize: constant input"
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.standardize([1.0])
+    assert e.value.code == "TooShort"
+
+
+def test_self_residual_is_zero(oracle):  # :39-44
+    x = np.random.default_rng(3).uniform(size=100)
+    assert np.all(oracle.residual(x, x) == 0.0)
+
+
+def test_residual_kat(oracle):  # :46-54
+    r = oracle.residual([1.0, 2.0, 3.0], [1.0, 0.0, -1.0])
+    assert r == pytest.approx([2.0, 2.0, 2.0], rel=1e-12)
+
+
+def test_residual_orthogonal_regressor_untouched(oracle):  # :56-61
+    xi = np.array([1.0, 1.0, -1.0, -1.0])
+    xj = np.array([1.0, -1.0, 1.0, -1.0])
+    assert oracle.residual(xi, xj).tobytes() == xi.tobytes()
+
+
+def test_residual_errors(oracle):  # :63-74
+    with pytest.raises(oracle.OracleError):
+        oracle.residual([1.0, 2.0, 3.0], [1.0, 2.0])
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.residual([1.0, 2.0, 3.0], [2.0, 2.0, 2.0])
+    assert e.value.code == "ZeroVariance"
+
+
+def test_residual_orthogonality_and_linearity(oracle):  # :76-107
+    rng = np.random.default_rng(17)
+    for _ in range(100):
+        n = 10 + int(rng.uniform() * 300)
+        scale = 10 ** rng.uniform(-2, 2)
+        xi = rng.normal(rng.uniform(-5, 5), scale, n)
+        xj = rng.uniform(-scale, scale, n)
+        r = oracle.residual(xi, xj)
+        assert abs(oracle.covariance_pop(r, xj)) <= 1e-10 * oracle.std_pop(xi) * oracle.std_pop(xj)
+    for _ in range(100):
+        n = 20 + int(rng.uniform() * 200)
+        xi, xk, xj = rng.normal(size=n), rng.uniform(-2, 2, n), rng.normal(1.0, 2.0, n)
+        a, b = rng.uniform(-3, 3, 2)
+        lhs = oracle.residual(a * xi + b * xk, xj)
+        rhs = a * oracle.residual(xi, xj) + b * oracle.residual(xk, xj)
+        assert np.all(np.abs(lhs - rhs) <= 1e-10)
+
+
+def test_log_cosh(oracle):  # :109-116
+    assert math.isfinite(oracle.log_cosh(1000.0))
+    assert oracle.log_cosh(1000.0) == pytest.approx(1000.0 - math.log(2.0), rel=1e-12)
+    for u in (0.0, 0.1, 1.0, 5.0, 20.0):
+        assert oracle.log_cosh(u) == pytest.approx(math.log(math.cosh(u)), rel=1e-12, abs=1e-300)
+        assert oracle.log_cosh(-u) == oracle.log_cosh(u)
+
+
+def test_entropy_sign_flip_exact(oracle):  # :118-126
+    rng = np.random.default_rng(31)
+    for _ in range(50):
+        u = oracle.standardize(rng.uniform(size=200))
+        assert oracle.entropy_approx(u) == oracle.entropy_approx(-u)
+
+
+def test_entropy_uniform_vs_gaussian(oracle):  # :128-135
+    rng = np.random.default_rng(41)
+    uni = oracle.standardize(rng.uniform(size=100000))
+    assert oracle.entropy_approx(uni) < oracle.gaussian_entropy()
+    gau = oracle.standardize(rng.normal(size=100000))
+    assert oracle.entropy_approx(gau) == pytest.approx(oracle.gaussian_entropy(), rel=0.01)
+    assert oracle.gaussian_entropy() == pytest.approx(1.4189385332046727, rel=1e-15)
+
+
+def test_mi_antisymmetry_exact(oracle):  # :137-149
+    rng = np.random.default_rng(53)
+    for _ in range(50):
+        n = 50 + int(rng.uniform() * 200)
+        xi = oracle.standardize(rng.uniform(size=n))
+        xj = oracle.standardize(rng.normal(size=n))
+        ri, rj = oracle.residual(xi, xj), oracle.residual(xj, xi)
+        assert oracle.diff_mutual_info(xi, xj, ri, rj) == -oracle.diff_mutual_info(xj, xi, rj, ri)
+
+
+def test_mi_causal_pair(oracle):  # :151-168
+    correct = 0
+    for seed in range(100):
+        rng = np.random.default_rng(1000 + seed)
+        x0 = rng.uniform(size=10000)
+        x1 = 0.8 * x0 + rng.uniform(size=10000)
+        xi, xj = oracle.standardize(x0), oracle.standardize(x1)
+        if oracle.diff_mutual_info(xi, xj, oracle.residual(xi, xj), oracle.residual(xj, xi)) > 0.0:
+            correct += 1
+    assert correct >= 99
+
+
+def test_mi_independent_pair(oracle):  # :170-181
+    small = 0
+    for seed in range(100):
+        rng = np.random.default_rng(2000 + seed)
+        xi = oracle.standardize(rng.uniform(size=10000))
+        xj = oracle.standardize(rng.uniform(size=10000))
+        if abs(oracle.diff_mutual_info(xi, xj, oracle.residual(xi, xj), oracle.residual(xj, xi))) < 0.01:
+            small += 1
+    assert small >= 95
+
+
+def test_fused_entropy_equals_two_step(oracle):  # :183-192
+    rng = np.random.default_rng(61)
+    for _ in range(50):
+        r = rng.normal(0.0, rng.uniform(0.1, 10.0), 300)
+        sd = oracle.std_pop(r)
+        assert oracle.entropy_of_normalized(r) == oracle.entropy_approx(r / sd)
+
+
+def test_entropy_matches_numpy_formula(oracle):
+    """kernels.cpp:16-40 restated independently in numpy (same element order)."""
+    rng = np.random.default_rng(5)
+    u = oracle.standardize(rng.laplace(size=777))
+    a = np.abs(u)
+    lc = a + (np.log1p(np.exp(-2.0 * a)) - math.log(2.0))
+    pdf = u * np.exp(-0.5 * (u * u))
+    s1 = s2 = 0.0
+    for v, w in zip(lc, pdf):  # left-to-right sums
+        s1 += v
+        s2 += w
+    t1, t2 = s1 / u.size - 0.37457, s2 / u.size
+    h = 0.5 * (1 + math.log(2 * math.pi)) - 79.047 * t1 * t1 - 7.4129 * t2 * t2
+    assert oracle.entropy_approx(u) == pytest.approx(h, rel=1e-15, abs=1e-15)
+
+
+# --------------------------------------------------------------- ordering (test_ordering.cpp)
+
+def naive_scores(oracle, X, u):  # test_ordering.cpp:27-46
+    d = X.shape[1]
+    scores = np.full(d, -np.inf)
+    for i in u:
+        xi = oracle.standardize(X[:, i])
+        acc = 0.0
+        for j in u:
+            if j == i:
+                continue
+            xj = oracle.standardize(X[:, j])
+            mi = oracle.diff_mutual_info(xi, xj, oracle.residual(xi, xj), oracle.residual(xj, xi))
+            c = min(0.0, mi)
+            acc += c * c
+        scores[i] = -acc
+    return scores
+
+
+def test_singleton(oracle):  # :60-68
+    X = random_matrix(np.random.default_rng(1), 3, 50)
+    chosen, scores = oracle.search_causal_order(X, [2])
+    assert chosen == 2 and scores[2] == 0.0 and np.isinf(scores[0])
+
+
+def test_scores_match_naive_composition_bitwise(oracle):  # :70-84
+    rng = np.random.default_rng(2)
+    for _ in range(10):
+        d = 3 + int(rng.uniform() * 5)
+        X = random_matrix(rng, d, 200)
+        _, scores = oracle.search_causal_order(X, list(range(d)))
+        assert scores.tobytes() == naive_scores(oracle, X, list(range(d))).tobytes()
+
+
+def test_chain_exogenous_wins(oracle):  # :86-100
+    correct = 0
+    for seed in range(100):
+        rng = np.random.default_rng(3000 + seed)
+        x0 = rng.uniform(size=10000)
+        X = np.asfortranarray(np.stack([x0, 0.8 * x0 + rng.uniform(size=10000)], axis=1))
+        correct += oracle.search_causal_order(X, [0, 1])[0] == 0
+    assert correct >= 99
+
+
+def test_level0_chosen_first(oracle, plg):  # :102-120
+    correct = 0
+    for seed in range(100):
+        dag = plg.gen_two_level_dag(10, seed=4000 + seed)
+        X = plg.sample_lingam(dag, 10000, seed=4000 + seed)
+        chosen, _ = oracle.search_causal_order(X, list(range(10)), workers=8)
+        correct += chosen in dag.order[:5]
+    assert correct >= 95
+
+
+def test_scores_nonpositive(oracle):  # :122-146
+    rng = np.random.default_rng(7)
+    for _ in range(20):
+        d = 2 + int(rng.uniform() * 6)
+        X = random_matrix(rng, d, 150)
+        _, scores = oracle.search_causal_order(X, list(range(d)))
+        assert np.all(scores <= 0.0)
+
+
+def test_parallel_and_fast_bit_identical(oracle):  # :148-179
+    rng = np.random.default_rng(5000)
+    for seed in range(20):
+        d = 2 + int(rng.uniform() * 19)
+        m = 100 + int(rng.uniform() * 1901)
+        X = random_matrix(rng, d, m)
+        c0, s0 = oracle.search_causal_order(X, list(range(d)))
+        for w in (1, 2, 7, 32):
+            for fast in (False, True):
+                c, s = oracle.search_causal_order(X, list(range(d)), workers=w, fast=fast)
+                assert c == c0 and s.tobytes() == s0.tobytes()
+
+
+def test_scale_invariance(oracle):  # :181-193
+    rng = np.random.default_rng(13)
+    for _ in range(20):
+        d = 3 + int(rng.uniform() * 5)
+        X = random_matrix(rng, d, 300)
+        before = oracle.search_causal_order(X, list(range(d)))[0]
+        col = int(rng.uniform() * d)
+        X[:, col] *= rng.uniform(0.1, 50.0)
+        assert oracle.search_causal_order(X, list(range(d)))[0] == before
+
+
+def test_search_errors(oracle):  # :195-212
+    X = random_matrix(np.random.default_rng(15), 3, 50)
+    for U, code in (([], "EmptyCandidates"), ([0, 3], "InvalidIndex"), ([0, 0], "InvalidIndex")):
+        with pytest.raises(oracle.OracleError) as e:
+            oracle.search_causal_order(X, U)
+        assert e.value.code == code
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.search_causal_order(X, [0, 1], workers=0)
+    assert e.value.code == "OutOfRange"
+    Xc = X.copy(order="F")
+    Xc[:, 1] = 4.0
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.search_causal_order(Xc, [0, 1, 2])
+    assert e.value.code == "ZeroVariance" and e.value.col == 1
+
+
+def test_regress_out_kat(oracle):  # :214-226
+    X = np.asfortranarray([[1, 1, 0.5], [1, -1, 1.5], [-1, 1, -0.5], [-1, -1, 2.5]], dtype=float)
+    R = oracle.regress_out(X, 0, [1, 2])
+    assert R.shape == (4, 2)
+    assert R[:, 0].tobytes() == X[:, 1].tobytes()
+    assert abs(oracle.covariance_pop(R[:, 1], X[:, 0])) <= 1e-10 * oracle.std_pop(X[:, 2]) * oracle.std_pop(X[:, 0])
+
+
+def test_regress_out_orthogonal(oracle):  # :228-240
+    rng = np.random.default_rng(19)
+    for _ in range(30):
+        d = 3 + int(rng.uniform() * 5)
+        X = random_matrix(rng, d, 400)
+        R = oracle.regress_out(X, 0, list(range(1, d)))
+        for p in range(d - 1):
+            bound = 1e-10 * oracle.std_pop(X[:, p + 1]) * oracle.std_pop(X[:, 0])
+            assert abs(oracle.covariance_pop(R[:, p], X[:, 0])) <= bound
+
+
+def test_regress_out_errors(oracle):  # :254-269
+    X = random_matrix(np.random.default_rng(22), 3, 50)
+    with pytest.raises(oracle.OracleError):
+        oracle.regress_out(X, 0, [0, 1])
+    with pytest.raises(oracle.OracleError):
+        oracle.regress_out(X, 5, [0])
+    Xc = X.copy(order="F")
+    Xc[:, 0] = 1.0
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.regress_out(Xc, 0, [1, 2])
+    assert e.value.code == "ZeroVariance" and e.value.col == 0
+
+
+def test_collinear_duplicate_fails_next_round(oracle):  # :271-281
+    X = random_matrix(np.random.default_rng(25), 3, 100)
+    X[:, 2] = X[:, 0]
+    R = oracle.regress_out(X, 0, [1, 2])
+    nxt = X.copy(order="F")
+    nxt[:, 1], nxt[:, 2] = R[:, 0], R[:, 1]
+    with pytest.raises(oracle.OracleError):
+        oracle.search_causal_order(nxt, [1, 2])
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.causal_order(X)
+    assert e.value.code == "ZeroVariance"
+
+
+def test_causal_order_d1(oracle):  # :283-287
+    assert oracle.causal_order(np.array([[1.0], [2.0], [3.0]])) == [0]
+
+
+def test_causal_order_chain(oracle):  # :289-302
+    correct = 0
+    for seed in range(100):
+        rng = np.random.default_rng(6000 + seed)
+        x0 = rng.uniform(size=10000)
+        X = np.stack([x0, 0.8 * x0 + rng.uniform(size=10000)], axis=1)
+        correct += oracle.causal_order(X) == [0, 1]
+    assert correct >= 99
+
+
+def test_causal_order_two_level(oracle, plg):  # :304-327
+    correct = 0
+    for seed in range(100):
+        dag = plg.gen_two_level_dag(10, seed=7000 + seed)
+        X = plg.sample_lingam(dag, 10000, seed=7000 + seed)
+        order = oracle.causal_order(X, parallel=True, workers=8, fast=True)
+        pos = {v: p for p, v in enumerate(order)}
+        W = dag.weights
+        ok = all(pos[j] < pos[i] for i in range(10) for j in range(10) if W[i, j] != 0.0)
+        correct += ok
+    assert correct >= 90
+
+
+def test_causal_order_permutation_gaussian(oracle):  # :329-340
+    rng = np.random.default_rng(29)
+    for _ in range(10):
+        d = 2 + int(rng.uniform() * 6)
+        order = oracle.causal_order(rng.normal(size=(300, d)))
+        assert sorted(order) == list(range(d))
+
+
+def test_causal_order_parallel_fast_identical(oracle):  # :342-352
+    rng = np.random.default_rng(8000)
+    for _ in range(10):
+        d = 3 + int(rng.uniform() * 10)
+        X = random_matrix(rng, d, 500)
+        seq = oracle.causal_order(X)
+        for w in (2, 5, 16):
+            assert oracle.causal_order(X, parallel=True, workers=w) == seq
+            assert oracle.causal_order(X, parallel=True, workers=w, fast=True) == seq
+
+
+def test_validate_errors(oracle):  # types.cpp:21-47, SPEC validate examples
+    oracle.validate(np.array([[1, 1], [2, 0], [3, -1]], dtype=float))
+    X = np.array([[1.0, 2.0], [2.0, 2.0], [3.0, 2.0]])
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.validate(X)
+    assert e.value.code == "ZeroVariance" and e.value.col == 1
+    X = np.array([[1.0, 2.0], [np.nan, 3.0], [3.0, 1.0]])
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.validate(X)
+    assert e.value.code == "NonFinite" and (e.value.row, e.value.col) == (1, 0)
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.validate(np.ones((1, 3)))
+    assert e.value.code == "TooFewSamples"
+
+
+# --------------------------------------------------------- weights (test_direct_lingam.cpp)
+
+def test_weights_chain(oracle):  # test_direct_lingam.cpp:22-33
+    rng = np.random.default_rng(42)
+    x0 = rng.uniform(size=10000)
+    X = np.stack([x0, 0.8 * x0 + rng.uniform(size=10000)], axis=1)
+    order = oracle.causal_order(X)
+    assert order == [0, 1]
+    B, pinv = oracle.fit_weights(X, order)
+    assert abs(B[1, 0] - 0.8) <= 0.05 and B[0, 1] == 0.0 and not pinv
+
+
+def test_weights_match_lstsq(oracle, plg):
+    X = two_level_data(plg, 4242, 8, 2000)
+    order = oracle.causal_order(X)
+    B, pinv = oracle.fit_weights(X, order)
+    Xc = X - X.mean(axis=0)
+    for p in range(1, 8):
+        t, pred = order[p], order[:p]
+        beta = np.linalg.lstsq(Xc[:, pred], Xc[:, t], rcond=None)[0]
+        assert np.allclose(B[t, pred], beta, rtol=1e-9, atol=1e-12)
+    assert not pinv
+
+
+def test_weights_pinv_fallback(oracle):  # test_direct_lingam.cpp:96-113
+    rng = np.random.default_rng(77)
+    u, w = rng.uniform(-1, 1, 400), rng.uniform(-1, 1, 400)
+    X = np.stack([u, w, u + w, u - w], axis=1)
+    order = [0, 1, 2, 3]
+    B, pinv = oracle.fit_weights(X, order)
+    assert pinv and np.all(np.isfinite(B))
+    Xc = X - X.mean(axis=0)
+    ref = np.linalg.pinv(Xc[:, :3]) @ Xc[:, 3]
+    assert np.allclose(B[3, :3], ref, atol=1e-8)
