@@ -166,14 +166,14 @@ namespace {
 
 int make_tables(plg_ctx* ctx, plg_status* st) {
   std::vector<double> e(plg::kExpN);
-  std::vector<double2> l(plg::kLogN);
+  std::vector<double2> l(plg::kLogMasterN);
   for (int j = 0; j < plg::kExpN; ++j) e[j] = static_cast<double>(exp2l(static_cast<long double>(j) / plg::kExpN));
   const long double ln2 = logl(2.0L);
-  for (int j = 0; j < plg::kLogN; ++j) {
-    const double c = (j == plg::kLogN - 1)
+  for (int j = 0; j < plg::kLogMasterN; ++j) {
+    const double c = (j == plg::kLogMasterN - 1)
                          ? 0.5
                          : static_cast<double>(1.0L / (1.0L + (static_cast<long double>(j) + 0.5L) /
-                                                                  (plg::kLogN - 1)));
+                                                                  (plg::kLogMasterN - 1)));
     l[j] = make_double2(c, static_cast<double>(-logl(static_cast<long double>(c)) - ln2));
   }
   PLG_CUDA(cudaMalloc(&ctx->g_exp, e.size() * sizeof(double)));

@@ -65,8 +65,6 @@ constexpr size_t kPairSmem =
 __global__ void __launch_bounds__(kPairThreads, 1)
     pair_kernel(const PairLaunch a) {
   extern __shared__ __align__(128) unsigned char smem[];
-  double* s_exp = reinterpret_cast<double*>(smem);
-  double2* s_log = reinterpret_cast<double2*>(smem + kExpN * kExpRep * 8);
   double* s_data = reinterpret_cast<double*>(smem + kTableBytes);
   uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + kTableBytes + kDataDoubles * sizeof(double));
   int* s_col = reinterpret_cast<int*>(s_bar + 8);
@@ -91,7 +89,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
     mbar_init(&s_bar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  load_tables(s_exp, s_log, a.g_exp, a.g_log);
+  load_tables(smem, a.g_exp, a.g_log);
   __syncthreads();
   if (s_abort) return;
 
@@ -157,8 +155,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
     }
   }
   double lc1[4] = {0, 0, 0, 0}, pd1[4] = {0, 0, 0, 0}, lc2[4] = {0, 0, 0, 0}, pd2[4] = {0, 0, 0, 0};
-  const double* exp_row = s_exp + (lane & (kExpRep - 1));
-  const double2* log_row = s_log + (lane & (kLogRep - 1));
+  const TabPtr tp = table_ptrs(smem, lane);
   const int jrow = diag ? 0 : kBT;
 
   __syncthreads();  // zero-fill visible before the first chunk is consumed
@@ -185,8 +182,8 @@ __global__ void __launch_bounds__(kPairThreads, 1)
         const double y = xj[q & 1];
         const double u1 = fma(y, -bs1[q], x * s1[q]);  // (x_i - b_ij x_j) / sd_ij
         const double u2 = fma(x, -bs2[q], y * s2[q]);  // (x_j - b_ji x_i) / sd_ji
-        ede_accumulate(u1, lc1[q], pd1[q], exp_row, log_row);
-        ede_accumulate(u2, lc2[q], pd2[q], exp_row, log_row);
+        ede_accumulate(u1, lc1[q], pd1[q], tp);
+        ede_accumulate(u2, lc2[q], pd2[q], tp);
       }
     }
     __syncthreads();
@@ -243,15 +240,12 @@ __global__ void __launch_bounds__(kColentThreads)
                   const int* act, int u, double* H, const double* g_exp, const double2* g_log,
                   const int* nz, const int* col_var, int round, unsigned long long* err) {
   extern __shared__ __align__(128) unsigned char smem[];
-  double* s_exp = reinterpret_cast<double*>(smem);
-  double2* s_log = reinterpret_cast<double2*>(smem + kExpN * kExpRep * 8);
   __shared__ double s_red[2][kColentThreads / 32];
   if (*err != kNoError) return;
-  load_tables(s_exp, s_log, g_exp, g_log);
+  load_tables(smem, g_exp, g_log);
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const double* exp_row = s_exp + (lane & (kExpRep - 1));
-  const double2* log_row = s_log + (lane & (kLogRep - 1));
+  const TabPtr tp = table_ptrs(smem, lane);
   for (int p = blockIdx.x; p < u; p += gridDim.x) {
     const int col = act[p];
     const double ccc = C[static_cast<int64_t>(col) * ldc + col];
@@ -260,7 +254,7 @@ __global__ void __launch_bounds__(kColentThreads)
     const double inv_sd = 1.0 / sqrt(ccc);
     const double* w = W + static_cast<int64_t>(col) * ldw;
     double lc = 0.0, pd = 0.0;
-    for (int64_t t = threadIdx.x; t < n; t += kColentThreads) ede_accumulate(w[t] * inv_sd, lc, pd, exp_row, log_row);
+    for (int64_t t = threadIdx.x; t < n; t += kColentThreads) ede_accumulate(w[t] * inv_sd, lc, pd, tp);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       lc += __shfl_xor_sync(0xffffffffu, lc, o);
@@ -286,16 +280,15 @@ __global__ void __launch_bounds__(kColentThreads)
 __global__ void math_probe_kernel(const double* u, int64_t n, double* out, const double* g_exp,
                                   const double2* g_log) {
   extern __shared__ __align__(128) unsigned char smem[];
-  double* s_exp = reinterpret_cast<double*>(smem);
-  double2* s_log = reinterpret_cast<double2*>(smem + kExpN * kExpRep * 8);
-  load_tables(s_exp, s_log, g_exp, g_log);
+  load_tables(smem, g_exp, g_log);
   __syncthreads();
   const int lane = threadIdx.x & 31;
+  const TabPtr tp = table_ptrs(smem, lane);
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const double v = u[i];
     double lc = 0.0, pd = 0.0;
-    ede_accumulate(v, lc, pd, s_exp + (lane & (kExpRep - 1)), s_log + (lane & (kLogRep - 1)));
+    ede_accumulate(v, lc, pd, tp);
     const double a = fabs(v);
     out[4 * i + 0] = lc;
     out[4 * i + 1] = pd;
