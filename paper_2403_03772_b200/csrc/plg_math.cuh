@@ -5,11 +5,12 @@
 //     lc  = |u| + (log1p(exp(-2|u|)) - ln2)      (log cosh u)
 //     pdf = u * exp(-u^2 / 2)
 // libdevice exp + log1p + exp cost ~70 FP64-pipe instructions per EDE. Here both
-// exponentials use a 128-entry 2^(j/128) table (|reduced arg| <= ln2/256, degree-5
-// Taylor) and log1p a reciprocal/log table (|r| <= 1/257, degree-5 Taylor): 31 FP64
-// instructions per EDE and 14 integer ones (index and exponent arithmetic), checked in
-// SASS. Absolute error per element <= ~2e-15 in lc and pdf (tests/test_gpu_parity.py
-// checks against libdevice and numpy); the causal order needs ~1e-9.
+// exponentials use a 128-entry 2^(j/128) table (|reduced arg| <= ln2/256) and log1p a
+// 128-entry reciprocal/log table (|r| <= 1/257), each finished by a degree-4 near-minimax
+// polynomial (tools/fit_polys.py): 28 FP64 instructions per EDE plus ~14 integer ones
+// (index and exponent arithmetic), checked in SASS. Absolute error per element is a few
+// ulp of lc and pdf (tests/test_gpu_parity.py checks against libdevice and numpy); the
+// causal order needs ~1e-9.
 //
 // Shared-memory tables, replicated per lane group so random per-lane indices never
 // bank-conflict:
@@ -47,14 +48,18 @@ constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52: round-to-int in th
 // Coefficients that are not short doubles live in the constant bank: ptxas then feeds
 // them to DFMA as c[] operands instead of re-materialising register pairs every
 // iteration (measured: -20 issue slots per 8 EDE in the pair kernel's inner loop).
-static __constant__ double kC[13] = {
+static __constant__ double kC[16] = {
     -256.0 / kLn2,  // 0  exp(-2a):  k = rint(-2a * 128 / ln2)
     kLn2 / 256.0,   // 1            r = a + k ln2/256, exp(-2a) = 2^(k/128) e^(-2r)
     -64.0 / kLn2,   // 2  exp(-q/2): k = rint(-q/2 * 128 / ln2)
     kLn2 / 64.0,    // 3            r = q + k ln2/64,  exp(-q/2) = 2^(k/128) e^(-r/2)
-    -4.0 / 15.0, 2.0 / 3.0, -4.0 / 3.0,        // 4-6  (-2)^i / i!, i = 5, 4, 3
-    -1.0 / 3840.0, 1.0 / 384.0, -1.0 / 48.0,   // 7-9  (-1/2)^i / i!, i = 5, 4, 3
-    0.2, -0.25, 1.0 / 3.0,                     // 10-12 log1p: r^5/5, -r^4/4, r^3/3
+    // near-minimax degree-4 fits (tools/fit_polys.py, mpmath), highest degree first:
+    0.6666668744024424, -1.3333339565406885, 1.999999999999903, -1.9999999999997087,
+    //   4-7  exp(-2r),   |r| <= 1.01 ln2/512: max rel err 8.0e-17
+    0.0026041674781345408, -0.02083334307094826, 0.12499999999999394, -0.49999999999992717,
+    //   8-11 exp(-r/2),  |r| <= 1.01 ln2/128: max rel err 8.0e-17
+    0.20000270365230982, -0.25000315425970154, 0.3333333333230998, -0.4999999999880609,
+    //  12-15 log1p(r)/r, |r| <= 1/257: max rel err 9.3e-15 (abs err of log1p <= 3.6e-17)
 };
 // 2^(k/128) scaling is clamped at 2^-100: below it the term is < 1e-30 absolute (the true
 // value is smaller still) and the exponent field stays normal for any finite input.
@@ -102,10 +107,9 @@ __device__ __forceinline__ double exp_m2a(double a, const TabPtr& tp) {
   const int k = __double2loint(t);
   const double kd = t - kMagic;
   const double r = fma(kd, kC[1], a);  // exp(-2a) = 2^(k/128) * exp(-2r), |2r| <= ln2/128
-  double p = fma(r, kC[4], kC[5]);  // sum (-2r)^i / i!
+  double p = fma(r, kC[4], kC[5]);
   p = fma(p, r, kC[6]);
-  p = fma(p, r, 2.0);
-  p = fma(p, r, -2.0);
+  p = fma(p, r, kC[7]);
   p = fma(p, r, 1.0);
   return scale_pow2(p * exp_row(tp, k), k);
 }
@@ -116,10 +120,9 @@ __device__ __forceinline__ double exp_mhalf(double q, const TabPtr& tp) {
   const int k = __double2loint(t);
   const double kd = t - kMagic;
   const double r = fma(kd, kC[3], q);  // exp(-q/2) = 2^(k/128) * exp(-r/2), |r/2| <= ln2/256
-  double p = fma(r, kC[7], kC[8]);  // sum (-r/2)^i / i!
-  p = fma(p, r, kC[9]);
-  p = fma(p, r, 1.0 / 8.0);
-  p = fma(p, r, -0.5);
+  double p = fma(r, kC[8], kC[9]);
+  p = fma(p, r, kC[10]);
+  p = fma(p, r, kC[11]);
   p = fma(p, r, 1.0);
   return scale_pow2(p * exp_row(tp, k), k);
 }
@@ -131,9 +134,9 @@ __device__ __forceinline__ double logcosh_tail(double a, double v, const TabPtr&
   const unsigned row = (static_cast<unsigned>(__double2hiint(y)) >> (20 - kLogBits)) & (kLogRows - 1);
   const double2 cl = *reinterpret_cast<const double2*>(tp.log + row * kLogRowBytes);
   const double r = fma(y, cl.x, -1.0);
-  double p = fma(r, kC[10], kC[11]);  // log1p(r) = r (1 - r/2 + r^2/3 - r^3/4 + r^4/5)
-  p = fma(p, r, kC[12]);
-  p = fma(p, r, -0.5);
+  double p = fma(r, kC[12], kC[13]);  // log1p(r) = r p(r)
+  p = fma(p, r, kC[14]);
+  p = fma(p, r, kC[15]);
   p = fma(p, r, 1.0);
   return fma(r, p, a + cl.y);
 }
