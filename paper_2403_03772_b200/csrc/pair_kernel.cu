@@ -8,12 +8,16 @@
 // work is one residual, two exponentials and one log1p per direction.
 //
 // Work decomposition: a CTA owns one 32x32 tile of (i-block, j-block) positions and one
-// sample segment. 256 threads, each 2x2 pairs x 2 directions = 8 EDE per sample, with
-// per-thread left-to-right sums (the reduction order depends only on (u, n), never on
-// the tile schedule or the GPU count). Column chunks of 64 samples are staged in shared
-// memory by cp.async.bulk (one bulk copy per column chunk, mbarrier complete_tx,
-// double-buffered).
+// sample segment. Each compute thread owns NI x 2 pairs x 2 directions (NI = 2: 256
+// compute threads, 8 EDE per sample; NI = 1: 512 threads, 4 EDE) with per-thread
+// left-to-right sums (the reduction order depends only on (u, n), never on the tile
+// schedule or the GPU count). A dedicated producer warp stages 64-sample column chunks
+// in shared memory with cp.async.bulk (one bulk copy per column chunk, mbarrier
+// complete_tx) into a 3-stage ring; consumer warps release stages through per-stage
+// "empty" mbarriers, so no CTA-wide barrier sits in the main loop.
 #include <cuda_runtime.h>
+
+#include <cstdlib>
 
 #include "plg_kernels.h"
 #include "plg_math.cuh"
@@ -37,6 +41,10 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t done = 0;
   do {
@@ -58,16 +66,28 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
-constexpr int kDataDoubles = kStages * 2 * kBT * kCHS;
-constexpr size_t kPairSmem =
-    static_cast<size_t>(kTableBytes) + kDataDoubles * sizeof(double) + 64 + 2 * kBT * sizeof(int);
+constexpr int kStages = 3;
+constexpr int kStageDoubles = 2 * kBT * kCHS;
+constexpr size_t kPairSmem = static_cast<size_t>(kTableBytes) + kStages * kStageDoubles * sizeof(double) +
+                             2 * kStages * sizeof(uint64_t) + 2 * kBT * sizeof(int);
 
-__global__ void __launch_bounds__(kPairThreads, 1)
-    pair_kernel(const PairLaunch a) {
+template <int NI>
+struct PairCfg {
+  static constexpr int kCompute = 1024 / (NI * 2);   // compute threads
+  static constexpr int kThreads = kCompute + 32;     // + one producer warp
+  static constexpr int kWarps = kCompute / 32;
+  static constexpr int kIStride = kBT / NI;          // i positions ti + kIStride * a
+  static constexpr int kMinBlocks = 1;
+};
+
+template <int NI>
+__global__ void __launch_bounds__(PairCfg<NI>::kThreads, 1) pair_kernel(const PairLaunch a) {
+  using Cfg = PairCfg<NI>;
   extern __shared__ __align__(128) unsigned char smem[];
   double* s_data = reinterpret_cast<double*>(smem + kTableBytes);
-  uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + kTableBytes + kDataDoubles * sizeof(double));
-  int* s_col = reinterpret_cast<int*>(s_bar + 8);
+  uint64_t* s_full = reinterpret_cast<uint64_t*>(s_data + kStages * kStageDoubles);
+  uint64_t* s_empty = s_full + kStages;
+  int* s_col = reinterpret_cast<int*>(s_empty + kStages);
   __shared__ int s_abort;
 
   const int tid = threadIdx.x;
@@ -85,8 +105,10 @@ __global__ void __launch_bounds__(kPairThreads, 1)
     s_col[tid] = (p < a.u) ? a.act[p] : -1;
   }
   if (tid == 0) {
-    mbar_init(&s_bar[0], 1);
-    mbar_init(&s_bar[1], 1);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&s_full[s], 1);
+      mbar_init(&s_empty[s], Cfg::kWarps);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   load_tables(smem, a.g_exp, a.g_log);
@@ -95,40 +117,45 @@ __global__ void __launch_bounds__(kPairThreads, 1)
 
   const int ncols = diag ? kBT : 2 * kBT;
   // Rows of columns past the active set are zero so they contribute exact zeros.
-  for (int idx = tid; idx < kStages * ncols * kCHS; idx += kPairThreads) {
+  for (int idx = tid; idx < kStages * ncols * kCHS; idx += Cfg::kThreads) {
     const int st = idx / (ncols * kCHS);
     const int row = (idx / kCHS) % ncols;
-    if (s_col[row] < 0) s_data[st * 2 * kBT * kCHS + row * kCHS + idx % kCHS] = 0.0;
+    if (s_col[row] < 0) s_data[st * kStageDoubles + row * kCHS + idx % kCHS] = 0.0;
   }
-
   const int64_t t_seg0 = static_cast<int64_t>(seg) * a.seg_len;
-  const int64_t t_seg1 = min(a.n, t_seg0 + a.seg_len);
+  const int64_t t_seg1 = lmin(a.n, t_seg0 + a.seg_len);
   const int nch = static_cast<int>((t_seg1 - t_seg0 + kCH - 1) / kCH);
+  __syncthreads();  // zero-fill visible before the first chunk is consumed
 
-  auto issue = [&](int c) {  // warp 0: stage chunk c
-    const int st = c & 1;
-    const int64_t t0 = t_seg0 + static_cast<int64_t>(c) * kCH;
-    const int len = static_cast<int>(lmin(kCH, t_seg1 - t0));
-    const uint32_t bytes = static_cast<uint32_t>(((len + 1) & ~1) * sizeof(double));
+  if (warp == Cfg::kWarps) {  // ---- producer warp: the bulk-copy ring ----
     int nvalid = 0;
     for (int r = 0; r < ncols; ++r) nvalid += (s_col[r] >= 0);
-    if (lane == 0) mbar_expect_tx(&s_bar[st], bytes * nvalid);
-    __syncwarp();
-    for (int r = lane; r < ncols; r += 32) {
-      const int col = s_col[r];
-      if (col >= 0)
-        bulk_g2s(s_data + st * 2 * kBT * kCHS + r * kCHS, a.W + static_cast<int64_t>(col) * a.ldw + t0,
-                 bytes, &s_bar[st]);
+    for (int c = 0; c < nch; ++c) {
+      const int st = c % kStages;
+      if (c >= kStages) mbar_wait(&s_empty[st], ((c / kStages) - 1) & 1);
+      const int64_t t0 = t_seg0 + static_cast<int64_t>(c) * kCH;
+      const int len = static_cast<int>(lmin(kCH, t_seg1 - t0));
+      const uint32_t bytes = static_cast<uint32_t>(((len + 1) & ~1) * sizeof(double));
+      if (lane == 0) mbar_expect_tx(&s_full[st], bytes * nvalid);
+      __syncwarp();
+      for (int r = lane; r < ncols; r += 32) {
+        const int col = s_col[r];
+        if (col >= 0)
+          bulk_g2s(s_data + st * kStageDoubles + r * kCHS, a.W + static_cast<int64_t>(col) * a.ldw + t0, bytes,
+                   &s_full[st]);
+      }
     }
-  };
+    return;
+  }
 
-  // Per-thread pairs: i positions {ti, ti+16}, j positions {tj, tj+16} within the tile.
+  // ---- compute warps: pairs (ti + kIStride*x, tj + 16*y), x < NI, y < 2 ----
+  constexpr int NQ = NI * 2;
   const int ti = (warp >> 1) * 4 + (lane >> 3);
   const int tj = (warp & 1) * 8 + (lane & 7);
-  double s1[4], bs1[4], s2[4], bs2[4];
+  double s1[NQ], bs1[NQ], s2[NQ], bs2[NQ];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int pi = ti + 16 * (q >> 1);
+  for (int q = 0; q < NQ; ++q) {
+    const int pi = ti + Cfg::kIStride * (q >> 1);
     const int pj = tj + 16 * (q & 1);
     const int ci = s_col[pi];
     const int cj = s_col[diag ? pj : kBT + pj];
@@ -154,30 +181,30 @@ __global__ void __launch_bounds__(kPairThreads, 1)
       }
     }
   }
-  double lc1[4] = {0, 0, 0, 0}, pd1[4] = {0, 0, 0, 0}, lc2[4] = {0, 0, 0, 0}, pd2[4] = {0, 0, 0, 0};
+  double lc1[NQ], pd1[NQ], lc2[NQ], pd2[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) lc1[q] = pd1[q] = lc2[q] = pd2[q] = 0.0;
   const TabPtr tp = table_ptrs(smem, lane);
   const int jrow = diag ? 0 : kBT;
 
-  __syncthreads();  // zero-fill visible before the first chunk is consumed
-  if (warp == 0) {
-    issue(0);
-    if (nch > 1) issue(1);
-  }
   for (int c = 0; c < nch; ++c) {
-    const int st = c & 1;
-    mbar_wait(&s_bar[st], (c >> 1) & 1);
-    const double* base = s_data + st * 2 * kBT * kCHS;
-    const double* xi0p = base + ti * kCHS;
-    const double* xi1p = base + (ti + 16) * kCHS;
+    const int st = c % kStages;
+    mbar_wait(&s_full[st], (c / kStages) & 1);
+    const double* base = s_data + st * kStageDoubles;
+    const double* xip[NI];
+#pragma unroll
+    for (int x = 0; x < NI; ++x) xip[x] = base + (ti + Cfg::kIStride * x) * kCHS;
     const double* xj0p = base + (jrow + tj) * kCHS;
     const double* xj1p = base + (jrow + tj + 16) * kCHS;
     const int len = static_cast<int>(lmin(kCH, t_seg1 - (t_seg0 + static_cast<int64_t>(c) * kCH)));
 #pragma unroll 1
     for (int t = 0; t < len; ++t) {
-      const double xi[2] = {xi0p[t], xi1p[t]};
+      double xi[NI];
+#pragma unroll
+      for (int x = 0; x < NI; ++x) xi[x] = xip[x][t];
       const double xj[2] = {xj0p[t], xj1p[t]};
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < NQ; ++q) {
         const double x = xi[q >> 1];
         const double y = xj[q & 1];
         const double u1 = fma(y, -bs1[q], x * s1[q]);  // (x_i - b_ij x_j) / sd_ij
@@ -186,13 +213,13 @@ __global__ void __launch_bounds__(kPairThreads, 1)
         ede_accumulate(u2, lc2[q], pd2[q], tp);
       }
     }
-    __syncthreads();
-    if (warp == 0 && c + 2 < nch) issue(c + 2);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&s_empty[st]);
   }
 
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int slot = (ti + 16 * (q >> 1)) * kBT + tj + 16 * (q & 1);
+  for (int q = 0; q < NQ; ++q) {
+    const int slot = (ti + Cfg::kIStride * (q >> 1)) * kBT + tj + 16 * (q & 1);
     double2* dst = reinterpret_cast<double2*>(
         a.part + ((static_cast<int64_t>(tl) * a.nseg + seg) * kTilePairs + slot) * 4);
     dst[0] = make_double2(lc1[q], pd1[q]);
@@ -297,16 +324,29 @@ __global__ void math_probe_kernel(const double* u, int64_t n, double* out, const
   }
 }
 
-}  // namespace
-
-void launch_pair(const PairLaunch& a, cudaStream_t s) {
+template <int NI>
+void launch_pair_ni(const PairLaunch& a, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(pair_kernel<NI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(kPairSmem));
     attr = true;
   }
-  pair_kernel<<<a.ntiles * a.nseg, kPairThreads, kPairSmem, s>>>(a);
+  pair_kernel<NI><<<a.ntiles * a.nseg, PairCfg<NI>::kThreads, kPairSmem, s>>>(a);
+}
+
+}  // namespace
+
+void launch_pair(const PairLaunch& a, cudaStream_t s) {
+  // PLG_PAIR_NI (1 or 2) selects the thread geometry; tuning knob, default 2.
+  static const int ni = [] {
+    const char* v = std::getenv("PLG_PAIR_NI");
+    return (v && v[0] == '1') ? 1 : 2;
+  }();
+  if (ni == 1)
+    launch_pair_ni<1>(a, s);
+  else
+    launch_pair_ni<2>(a, s);
 }
 
 void launch_finalize(const PairLaunch& a, cudaStream_t s) {

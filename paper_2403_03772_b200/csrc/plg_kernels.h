@@ -8,10 +8,8 @@ namespace plg {
 
 constexpr int kBT = 32;           // active positions per tile side
 constexpr int kTilePairs = kBT * kBT;
-constexpr int kPairThreads = 256;
 constexpr int kCH = 64;           // samples per shared-memory stage
 constexpr int kCHS = kCH + 2;     // padded column stride in shared memory (doubles)
-constexpr int kStages = 2;
 constexpr int kSegMin = 256;      // smallest sample segment per CTA
 
 // Error key: first error in the reference's raising order (ordering.cpp build_cache
