@@ -143,7 +143,7 @@ struct plg_ctx {
   double* g_exp = nullptr;
   double2* g_log = nullptr;
 
-  DevBuf<double> Xd, W, C, part, epack, H, k, scores, msd;
+  DevBuf<double> Xd, W, C, part, epack, H, k, scores, msd, gscr;
   DevBuf<int> act0, act1, colvar, order, stat, idx, nz;
   DevBuf<plg::RoundState> rs;
   DevBuf<unsigned long long> err;
@@ -275,6 +275,7 @@ int reserve_run(plg_ctx* c, int64_t n, int ncols, int64_t ldw, plg_status* st) {
   }
   PLG_CUDA(c->W.reserve(static_cast<size_t>(ncols) * ldw));
   PLG_CUDA(c->C.reserve(static_cast<size_t>(ncols) * ncols));
+  PLG_CUDA(c->gscr.reserve(static_cast<size_t>(plg::gram_scratch_doubles(ncols, n))));
   PLG_CUDA(c->part.reserve(part_max));
   PLG_CUDA(c->epack.reserve(epack_max));
   PLG_CUDA(c->H.reserve(ncols));
@@ -363,7 +364,7 @@ int causal_order_impl(plg_ctx* c, const double* dX, int64_t ldx, int64_t n, int 
   if (int rc = upload_iota(c, c->act0.p, d, nullptr, st)) return rc;
   if (int rc = upload_iota(c, c->colvar.p, d, nullptr, st)) return rc;
   PLG_CUDA(cudaMemsetAsync(c->err.p, 0xff, sizeof(unsigned long long), c->stream));
-  plg::launch_gram(c->W.p, ldw, n, d, c->C.p, d, c->stream);
+  plg::launch_gram(c->W.p, ldw, n, d, c->C.p, d, c->gscr.p, c->stream);
   ++c->launches;
   const int rounds = (max_rounds < 0) ? d - 1 : std::min(max_rounds, d - 1);
   for (int r = 0; r < rounds; ++r) {
@@ -503,6 +504,7 @@ void plg_ctx_destroy(plg_ctx* c) {
   c->order.release();
   c->stat.release();
   c->msd.release();
+  c->gscr.release();
   c->idx.release();
   c->nz.release();
   c->rs.release();
@@ -559,7 +561,7 @@ int plg_search(plg_ctx* c, const double* X, int64_t n, int32_t d, int64_t ld, co
   if (int rc = standardize_validate(c, c->Xd.p, n, n, u, c->colvar.p, us.data(), ldw, false, st)) return rc;
   if (int rc = upload_iota(c, c->act0.p, u, nullptr, st)) return rc;
   PLG_CUDA(cudaMemsetAsync(c->err.p, 0xff, sizeof(unsigned long long), c->stream));
-  plg::launch_gram(c->W.p, ldw, n, u, c->C.p, u, c->stream);
+  plg::launch_gram(c->W.p, ldw, n, u, c->C.p, u, c->gscr.p, c->stream);
   ++c->launches;
   if (int rc = search_round(c, n, ldw, u, u, c->act0.p, 0, 3, st)) return rc;
   PLG_CUDA(c->scores.reserve(d));
@@ -766,7 +768,7 @@ extern "C" int plg_fit_weights(plg_ctx* c, const double* X, int64_t n, int32_t d
   const int64_t ldw = round_up(n, 16);
   if (int rc = reserve_run(c, n, d, ldw, st)) return rc;
   if (int rc = standardize_validate(c, c->Xd.p, n, n, d, nullptr, nullptr, ldw, true, st)) return rc;
-  plg::launch_gram(c->W.p, ldw, n, d, c->C.p, d, c->stream);
+  plg::launch_gram(c->W.p, ldw, n, d, c->C.p, d, c->gscr.p, c->stream);
   std::vector<double> C(static_cast<size_t>(d) * d), msd(2 * static_cast<size_t>(d));
   PLG_CUDA(cudaMemcpyAsync(C.data(), c->C.p, C.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   PLG_CUDA(cudaMemcpyAsync(msd.data(), c->msd.p, msd.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));

@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <cstring>
 
 #include "plg_kernels.h"
 #include "plg_math.cuh"
@@ -71,18 +72,25 @@ constexpr int kStageDoubles = 2 * kBT * kCHS;
 constexpr size_t kPairSmem = static_cast<size_t>(kTableBytes) + kStages * kStageDoubles * sizeof(double) +
                              2 * kStages * sizeof(uint64_t) + 2 * kBT * sizeof(int);
 
-template <int NI>
+// Thread geometry: each compute thread owns NI i-positions x NJ j-positions of the 32x32
+// tile (NQ = NI * NJ pairs, 2 NQ EDE per sample). kDedicated adds a producer warp; else the
+// last compute warp also refills the ring.
+template <int NI, int NJ, bool kDedicated>
 struct PairCfg {
-  static constexpr int kCompute = 1024 / (NI * 2);   // compute threads
-  static constexpr int kThreads = kCompute + 32;     // + one producer warp
+  static constexpr int NQ = NI * NJ;
+  static constexpr int kCompute = kTilePairs / NQ;  // compute threads
   static constexpr int kWarps = kCompute / 32;
-  static constexpr int kIStride = kBT / NI;          // i positions ti + kIStride * a
-  static constexpr int kMinBlocks = 1;
+  static constexpr int kThreads = kCompute + (kDedicated ? 32 : 0);
+  static constexpr int kIStride = kBT / NI;  // i positions ti + kIStride * x
+  static constexpr int kJStride = kBT / NJ;  // j positions tj + kJStride * y
+  static constexpr int kJGroups = kJStride / 8;  // warps along j (8 j-lanes per warp)
+  static_assert(kWarps * 32 == kCompute && kJStride % 8 == 0, "geometry");
 };
 
-template <int NI>
-__global__ void __launch_bounds__(PairCfg<NI>::kThreads, 1) pair_kernel(const PairLaunch a) {
-  using Cfg = PairCfg<NI>;
+template <int NI, int NJ, bool kDedicated>
+__global__ void __launch_bounds__(PairCfg<NI, NJ, kDedicated>::kThreads, 1) pair_kernel(const PairLaunch a) {
+  using Cfg = PairCfg<NI, NJ, kDedicated>;
+  constexpr int NQ = Cfg::NQ;
   extern __shared__ __align__(128) unsigned char smem[];
   double* s_data = reinterpret_cast<double*>(smem + kTableBytes);
   uint64_t* s_full = reinterpret_cast<uint64_t*>(s_data + kStages * kStageDoubles);
@@ -125,38 +133,43 @@ __global__ void __launch_bounds__(PairCfg<NI>::kThreads, 1) pair_kernel(const Pa
   const int64_t t_seg0 = static_cast<int64_t>(seg) * a.seg_len;
   const int64_t t_seg1 = lmin(a.n, t_seg0 + a.seg_len);
   const int nch = static_cast<int>((t_seg1 - t_seg0 + kCH - 1) / kCH);
+  int nvalid = 0;
+  for (int r = 0; r < ncols; ++r) nvalid += (s_col[r] >= 0);
   __syncthreads();  // zero-fill visible before the first chunk is consumed
 
-  if (warp == Cfg::kWarps) {  // ---- producer warp: the bulk-copy ring ----
-    int nvalid = 0;
-    for (int r = 0; r < ncols; ++r) nvalid += (s_col[r] >= 0);
+  auto issue = [&](int c) {  // one warp: stage chunk c into ring slot c % kStages
+    const int st = c % kStages;
+    const int64_t t0 = t_seg0 + static_cast<int64_t>(c) * kCH;
+    const int len = static_cast<int>(lmin(kCH, t_seg1 - t0));
+    const uint32_t bytes = static_cast<uint32_t>(((len + 1) & ~1) * sizeof(double));
+    if (lane == 0) mbar_expect_tx(&s_full[st], bytes * nvalid);
+    __syncwarp();
+    for (int r = lane; r < ncols; r += 32) {
+      const int col = s_col[r];
+      if (col >= 0)
+        bulk_g2s(s_data + st * kStageDoubles + r * kCHS, a.W + static_cast<int64_t>(col) * a.ldw + t0, bytes,
+                 &s_full[st]);
+    }
+  };
+  const int producer = kDedicated ? Cfg::kWarps : Cfg::kWarps - 1;
+  if (kDedicated && warp == producer) {  // ---- dedicated producer warp ----
     for (int c = 0; c < nch; ++c) {
-      const int st = c % kStages;
-      if (c >= kStages) mbar_wait(&s_empty[st], ((c / kStages) - 1) & 1);
-      const int64_t t0 = t_seg0 + static_cast<int64_t>(c) * kCH;
-      const int len = static_cast<int>(lmin(kCH, t_seg1 - t0));
-      const uint32_t bytes = static_cast<uint32_t>(((len + 1) & ~1) * sizeof(double));
-      if (lane == 0) mbar_expect_tx(&s_full[st], bytes * nvalid);
-      __syncwarp();
-      for (int r = lane; r < ncols; r += 32) {
-        const int col = s_col[r];
-        if (col >= 0)
-          bulk_g2s(s_data + st * kStageDoubles + r * kCHS, a.W + static_cast<int64_t>(col) * a.ldw + t0, bytes,
-                   &s_full[st]);
-      }
+      if (c >= kStages) mbar_wait(&s_empty[c % kStages], ((c / kStages) - 1) & 1);
+      issue(c);
     }
     return;
   }
+  if (!kDedicated && warp == producer)
+    for (int c = 0; c < kStages && c < nch; ++c) issue(c);
 
-  // ---- compute warps: pairs (ti + kIStride*x, tj + 16*y), x < NI, y < 2 ----
-  constexpr int NQ = NI * 2;
-  const int ti = (warp >> 1) * 4 + (lane >> 3);
-  const int tj = (warp & 1) * 8 + (lane & 7);
+  // ---- compute warps: pairs (ti + kIStride*x, tj + kJStride*y) ----
+  const int ti = (warp / Cfg::kJGroups) * 4 + (lane >> 3);
+  const int tj = (warp % Cfg::kJGroups) * 8 + (lane & 7);
   double s1[NQ], bs1[NQ], s2[NQ], bs2[NQ];
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
-    const int pi = ti + Cfg::kIStride * (q >> 1);
-    const int pj = tj + 16 * (q & 1);
+    const int pi = ti + Cfg::kIStride * (q / NJ);
+    const int pj = tj + Cfg::kJStride * (q % NJ);
     const int ci = s_col[pi];
     const int cj = s_col[diag ? pj : kBT + pj];
     const bool valid = (ci >= 0) && (cj >= 0) && (!diag || pi < pj);
@@ -189,24 +202,31 @@ __global__ void __launch_bounds__(PairCfg<NI>::kThreads, 1) pair_kernel(const Pa
 
   for (int c = 0; c < nch; ++c) {
     const int st = c % kStages;
+    if (!kDedicated && warp == producer && c >= 1 && c - 1 + kStages < nch) {
+      // refill the slot chunk c-1 used once every warp has released it
+      mbar_wait(&s_empty[(c - 1) % kStages], ((c - 1) / kStages) & 1);
+      issue(c - 1 + kStages);
+    }
     mbar_wait(&s_full[st], (c / kStages) & 1);
     const double* base = s_data + st * kStageDoubles;
     const double* xip[NI];
+    const double* xjp[NJ];
 #pragma unroll
     for (int x = 0; x < NI; ++x) xip[x] = base + (ti + Cfg::kIStride * x) * kCHS;
-    const double* xj0p = base + (jrow + tj) * kCHS;
-    const double* xj1p = base + (jrow + tj + 16) * kCHS;
+#pragma unroll
+    for (int y = 0; y < NJ; ++y) xjp[y] = base + (jrow + tj + Cfg::kJStride * y) * kCHS;
     const int len = static_cast<int>(lmin(kCH, t_seg1 - (t_seg0 + static_cast<int64_t>(c) * kCH)));
 #pragma unroll 1
     for (int t = 0; t < len; ++t) {
-      double xi[NI];
+      double xi[NI], xj[NJ];
 #pragma unroll
       for (int x = 0; x < NI; ++x) xi[x] = xip[x][t];
-      const double xj[2] = {xj0p[t], xj1p[t]};
+#pragma unroll
+      for (int y = 0; y < NJ; ++y) xj[y] = xjp[y][t];
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
-        const double x = xi[q >> 1];
-        const double y = xj[q & 1];
+        const double x = xi[q / NJ];
+        const double y = xj[q % NJ];
         const double u1 = fma(y, -bs1[q], x * s1[q]);  // (x_i - b_ij x_j) / sd_ij
         const double u2 = fma(x, -bs2[q], y * s2[q]);  // (x_j - b_ji x_i) / sd_ji
         ede_accumulate(u1, lc1[q], pd1[q], tp);
@@ -219,7 +239,7 @@ __global__ void __launch_bounds__(PairCfg<NI>::kThreads, 1) pair_kernel(const Pa
 
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
-    const int slot = (ti + Cfg::kIStride * (q >> 1)) * kBT + tj + 16 * (q & 1);
+    const int slot = (ti + Cfg::kIStride * (q / NJ)) * kBT + tj + Cfg::kJStride * (q % NJ);
     double2* dst = reinterpret_cast<double2*>(
         a.part + ((static_cast<int64_t>(tl) * a.nseg + seg) * kTilePairs + slot) * 4);
     dst[0] = make_double2(lc1[q], pd1[q]);
@@ -324,29 +344,37 @@ __global__ void math_probe_kernel(const double* u, int64_t n, double* out, const
   }
 }
 
-template <int NI>
-void launch_pair_ni(const PairLaunch& a, cudaStream_t s) {
+template <int NI, int NJ, bool kDedicated>
+void launch_pair_cfg(const PairLaunch& a, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(pair_kernel<NI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(pair_kernel<NI, NJ, kDedicated>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(kPairSmem));
     attr = true;
   }
-  pair_kernel<NI><<<a.ntiles * a.nseg, PairCfg<NI>::kThreads, kPairSmem, s>>>(a);
+  pair_kernel<NI, NJ, kDedicated><<<a.ntiles * a.nseg, PairCfg<NI, NJ, kDedicated>::kThreads, kPairSmem, s>>>(a);
 }
 
 }  // namespace
 
 void launch_pair(const PairLaunch& a, cudaStream_t s) {
-  // PLG_PAIR_NI (1 or 2) selects the thread geometry; tuning knob, default 2.
-  static const int ni = [] {
-    const char* v = std::getenv("PLG_PAIR_NI");
-    return (v && v[0] == '1') ? 1 : 2;
+  // PLG_PAIR_GEOM selects the thread geometry (tuning knob): "22d" = 2x2 pairs per thread +
+  // producer warp, "12d" = 1x2 + producer warp, "12" = 1x2 in-warp producer, "11" = 1x1.
+  static const int geom = [] {
+    const char* v = std::getenv("PLG_PAIR_GEOM");
+    if (!v) return 2;
+    if (!strcmp(v, "22d")) return 0;
+    if (!strcmp(v, "12d")) return 1;
+    if (!strcmp(v, "12")) return 2;
+    if (!strcmp(v, "11")) return 3;
+    return 2;
   }();
-  if (ni == 1)
-    launch_pair_ni<1>(a, s);
-  else
-    launch_pair_ni<2>(a, s);
+  switch (geom) {
+    case 0: launch_pair_cfg<2, 2, true>(a, s); break;
+    case 1: launch_pair_cfg<1, 2, true>(a, s); break;
+    case 3: launch_pair_cfg<1, 1, false>(a, s); break;
+    default: launch_pair_cfg<1, 2, false>(a, s); break;
+  }
 }
 
 void launch_finalize(const PairLaunch& a, cudaStream_t s) {

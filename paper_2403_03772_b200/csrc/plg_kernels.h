@@ -79,9 +79,33 @@ void launch_standardize(const double* X, int64_t ldx, int64_t n, const int* col_
                         double* W, int64_t ldw, int* stat, double* msd, int check_finite,
                         cudaStream_t s);
 
-// C = W^T W / n (FP64, symmetric, deterministic order).
+// C = W^T W / n (FP64, symmetric, deterministic order). Few 64x64 output tiles (small d)
+// split the sample axis into chunks reduced in ascending order through `scratch`
+// (gram_scratch_doubles(ncol, n) doubles); the split is a pure function of (ncol, n).
+struct GramPlan {
+  int ntb;       // 64-wide column blocks
+  int ntiles;    // upper-triangle output tiles
+  int nchunk;    // sample chunks
+  int64_t chunk; // samples per chunk (multiple of 16)
+};
+inline GramPlan gram_plan(int ncol, int64_t n) {
+  GramPlan g;
+  g.ntb = (ncol + 63) / 64;
+  g.ntiles = g.ntb * (g.ntb + 1) / 2;
+  int64_t nchunk = (2 * 148 + g.ntiles - 1) / g.ntiles;
+  const int64_t cap = n / 512 > 1 ? n / 512 : 1;
+  if (nchunk > cap) nchunk = cap;
+  if (nchunk < 1) nchunk = 1;
+  g.chunk = ((n + nchunk - 1) / nchunk + 15) / 16 * 16;
+  g.nchunk = static_cast<int>((n + g.chunk - 1) / g.chunk);
+  return g;
+}
+inline int64_t gram_scratch_doubles(int ncol, int64_t n) {
+  const GramPlan g = gram_plan(ncol, n);
+  return g.nchunk > 1 ? static_cast<int64_t>(g.nchunk) * g.ntiles * 64 * 64 : 0;
+}
 void launch_gram(const double* W, int64_t ldw, int64_t n, int ncol, double* C, int64_t ldc,
-                 cudaStream_t s);
+                 double* scratch, cudaStream_t s);
 
 // k[p] = sum_{q != p} min(0, M_pq)^2 with M_pq = (H_q + E(p|q)) - (H_p + E(q|p)).
 void launch_kreduce(const double* epack, const double* H, int u, int nb, double* k,

@@ -76,20 +76,23 @@ __global__ void __launch_bounds__(32 * kStdWarps)
 // C = W^T W / n, 64x64 output tiles on the upper triangle, mirrored (bit-symmetric).
 constexpr int kGT = 64, kGK = 16;
 __global__ void __launch_bounds__(256) gram_kernel(const double* W, int64_t ldw, int64_t n, int ncol,
-                                                   double* C, int64_t ldc, int ntb) {
+                                                   double* C, int64_t ldc, int ntb, int64_t chunk,
+                                                   double* scratch) {
   __shared__ double As[kGK][kGT + 2];
   __shared__ double Bs[kGK][kGT + 2];
   int bi, bj;
   tile_decode(blockIdx.x, ntb, bi, bj);
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   double acc[4][4] = {};
-  for (int64_t t0 = 0; t0 < n; t0 += kGK) {
+  const int64_t tb = blockIdx.y * chunk;
+  const int64_t te = lmin(n, tb + chunk);
+  for (int64_t t0 = tb; t0 < te; t0 += kGK) {
     for (int e = threadIdx.x; e < kGK * kGT; e += 256) {
       const int tt = e % kGK, cc = e / kGK;
       const int ca = bi * kGT + cc, cb = bj * kGT + cc;
       const int64_t t = t0 + tt;
-      As[tt][cc] = (ca < ncol && t < n) ? W[static_cast<int64_t>(ca) * ldw + t] : 0.0;
-      Bs[tt][cc] = (cb < ncol && t < n) ? W[static_cast<int64_t>(cb) * ldw + t] : 0.0;
+      As[tt][cc] = (ca < ncol && t < te) ? W[static_cast<int64_t>(ca) * ldw + t] : 0.0;
+      Bs[tt][cc] = (cb < ncol && t < te) ? W[static_cast<int64_t>(cb) * ldw + t] : 0.0;
     }
     __syncthreads();
 #pragma unroll
@@ -107,6 +110,14 @@ __global__ void __launch_bounds__(256) gram_kernel(const double* W, int64_t ldw,
     }
     __syncthreads();
   }
+  if (gridDim.y > 1) {  // partial tile of this sample chunk
+    double* dst = scratch + (static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x) * kGT * kGT;
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int s = 0; s < 4; ++s) dst[(ty * 4 + r) * kGT + tx * 4 + s] = acc[r][s];
+    return;
+  }
   const double dn = static_cast<double>(n);
 #pragma unroll
   for (int r = 0; r < 4; ++r)
@@ -119,6 +130,24 @@ __global__ void __launch_bounds__(256) gram_kernel(const double* W, int64_t ldw,
         C[static_cast<int64_t>(j) * ldc + i] = v;
       }
     }
+}
+
+// Sum the chunk partials in ascending chunk order and mirror (bit-symmetric C).
+__global__ void gram_reduce_kernel(const double* scratch, int ntiles, int nchunk, int ntb, int64_t n,
+                                   int ncol, double* C, int64_t ldc) {
+  int bi, bj;
+  tile_decode(blockIdx.x, ntb, bi, bj);
+  const double dn = static_cast<double>(n);
+  for (int e = threadIdx.x; e < kGT * kGT; e += blockDim.x) {
+    const int r = e / kGT, s = e % kGT;
+    const int i = bi * kGT + r, j = bj * kGT + s;
+    if (i >= ncol || j >= ncol) continue;
+    double v = 0.0;
+    for (int c = 0; c < nchunk; ++c) v += scratch[(static_cast<int64_t>(c) * ntiles + blockIdx.x) * kGT * kGT + e];
+    v /= dn;
+    C[static_cast<int64_t>(i) * ldc + j] = v;
+    C[static_cast<int64_t>(j) * ldc + i] = v;
+  }
 }
 
 __device__ __forceinline__ int tile_index(int bi, int bj, int nb) {
@@ -296,9 +325,10 @@ void launch_standardize(const double* X, int64_t ldx, int64_t n, const int* col_
 }
 
 void launch_gram(const double* W, int64_t ldw, int64_t n, int ncol, double* C, int64_t ldc,
-                 cudaStream_t s) {
-  const int ntb = (ncol + kGT - 1) / kGT;
-  gram_kernel<<<ntb * (ntb + 1) / 2, 256, 0, s>>>(W, ldw, n, ncol, C, ldc, ntb);
+                 double* scratch, cudaStream_t s) {
+  const GramPlan g = gram_plan(ncol, n);
+  gram_kernel<<<dim3(g.ntiles, g.nchunk), 256, 0, s>>>(W, ldw, n, ncol, C, ldc, g.ntb, g.chunk, scratch);
+  if (g.nchunk > 1) gram_reduce_kernel<<<g.ntiles, 256, 0, s>>>(scratch, g.ntiles, g.nchunk, g.ntb, n, ncol, C, ldc);
 }
 
 void launch_kreduce(const double* epack, const double* H, int u, int nb, double* k,
