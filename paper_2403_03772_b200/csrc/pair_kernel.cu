@@ -194,9 +194,9 @@ __global__ void __launch_bounds__(PairCfg<NI, NJ, kDedicated>::kThreads, 1) pair
       }
     }
   }
-  double lc1[NQ], pd1[NQ], lc2[NQ], pd2[NQ];
+  double lc[2 * NQ], pd[2 * NQ];  // [q] direction i|j, [NQ + q] direction j|i
 #pragma unroll
-  for (int q = 0; q < NQ; ++q) lc1[q] = pd1[q] = lc2[q] = pd2[q] = 0.0;
+  for (int q = 0; q < 2 * NQ; ++q) lc[q] = pd[q] = 0.0;
   const TabPtr tp = table_ptrs(smem, lane);
   const int jrow = diag ? 0 : kBT;
 
@@ -229,8 +229,8 @@ __global__ void __launch_bounds__(PairCfg<NI, NJ, kDedicated>::kThreads, 1) pair
         const double y = xj[q % NJ];
         const double u1 = fma(y, -bs1[q], x * s1[q]);  // (x_i - b_ij x_j) / sd_ij
         const double u2 = fma(x, -bs2[q], y * s2[q]);  // (x_j - b_ji x_i) / sd_ji
-        ede_accumulate(u1, lc1[q], pd1[q], tp);
-        ede_accumulate(u2, lc2[q], pd2[q], tp);
+        ede_accumulate(u1, lc[q], pd[q], tp);
+        ede_accumulate(u2, lc[NQ + q], pd[NQ + q], tp);
       }
     }
     __syncwarp();
@@ -242,8 +242,8 @@ __global__ void __launch_bounds__(PairCfg<NI, NJ, kDedicated>::kThreads, 1) pair
     const int slot = (ti + Cfg::kIStride * (q / NJ)) * kBT + tj + Cfg::kJStride * (q % NJ);
     double2* dst = reinterpret_cast<double2*>(
         a.part + ((static_cast<int64_t>(tl) * a.nseg + seg) * kTilePairs + slot) * 4);
-    dst[0] = make_double2(lc1[q], pd1[q]);
-    dst[1] = make_double2(lc2[q], pd2[q]);
+    dst[0] = make_double2(lc[q], pd[q]);
+    dst[1] = make_double2(lc[NQ + q], pd[NQ + q]);
   }
 }
 

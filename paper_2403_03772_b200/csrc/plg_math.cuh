@@ -7,10 +7,15 @@
 // libdevice exp + log1p + exp cost ~70 FP64-pipe instructions per EDE. Here both
 // exponentials use a 128-entry 2^(j/128) table (|reduced arg| <= ln2/256) and log1p a
 // 128-entry reciprocal/log table (|r| <= 1/257), each finished by a degree-4 near-minimax
-// polynomial (tools/fit_polys.py): 28 FP64 instructions per EDE plus ~14 integer ones
-// (index and exponent arithmetic), checked in SASS. Absolute error per element is a few
-// ulp of lc and pdf (tests/test_gpu_parity.py checks against libdevice and numpy); the
-// causal order needs ~1e-9.
+// polynomial (tools/fit_polys.py): 29 FP64 instructions per EDE plus ~20 integer/LDS ones
+// (index and exponent arithmetic, table reads), checked in SASS. Absolute error per
+// element is a few ulp of lc and pdf (tests/test_gpu_parity.py checks against libdevice
+// and numpy); the causal order needs ~1e-9.
+//
+// Throughput is bound by register-file reads rather than by the FP64 pipe itself: a DFMA
+// reading 3 distinct register pairs takes 3 issue cycles instead of 2, and integer
+// instructions share the read ports (measured, tools/probe/fp64_mix.cu; model and SASS
+// census in tools/rf_model.py, which predicts the measured 69% FP64-pipe utilisation).
 //
 // Shared-memory tables, replicated per lane group so random per-lane indices never
 // bank-conflict:
@@ -45,9 +50,9 @@ constexpr double kLn2 = 0.69314718055994530942;
 
 constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52: round-to-int in the low word
 
-// Coefficients that are not short doubles live in the constant bank: ptxas then feeds
-// them to DFMA as c[] operands instead of re-materialising register pairs every
-// iteration (measured: -20 issue slots per 8 EDE in the pair kernel's inner loop).
+// Coefficients that are not short doubles live in the constant bank: ptxas loads them
+// once (uniform registers for DFMA's addend slot) instead of re-materialising register
+// pairs every iteration (measured: -20 issue slots per 8 EDE in the pair kernel's loop).
 static __constant__ double kC[16] = {
     -256.0 / kLn2,  // 0  exp(-2a):  k = rint(-2a * 128 / ln2)
     kLn2 / 256.0,   // 1            r = a + k ln2/256, exp(-2a) = 2^(k/128) e^(-2r)
