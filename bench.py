@@ -276,6 +276,9 @@ def run_ours(args, world, rank, local):
                      "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
                      "frac": achieved / FP64_PEAK_TFLOPS if achieved else None,
                      "traffic": load_ncu_traffic(),
+                     "traffic_note": "dram read+write bytes of one u=2000 pair-kernel launch (ncu --set full, "
+                                     "profiles/r1_pair_kernel_ncu.md); its algorithmic bytes are one pass over W "
+                                     "(160 MB) — compute-bound, L2 serves the tile re-reads",
                      "basis": f"{FP64_OPS_PER_EDE} FP64-pipe instructions per EDE (SASS) x 2 flops, "
                               f"EDE = n * pair-evals; peak = measured DFMA rate (no FP64 figure in "
                               f"MEASURED_PEAKS.json)",
