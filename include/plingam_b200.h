@@ -105,6 +105,20 @@ int plg_regress_out(plg_ctx* ctx, const double* X, int64_t n, int32_t d, int64_t
 int plg_fit_weights(plg_ctx* ctx, const double* X, int64_t n, int32_t d, int64_t ld,
                     const int32_t* order, double* B_out, int32_t* used_pinv, plg_status* st);
 
+/* The element functions of plingam::kernels (include/plingam/kernels.hpp:25-70), exposed
+ * by the reference's Python module (bindings/pymodule.cpp:79-96):
+ *   standardize (kernels.cpp:92-104; bit-identical: left-to-right sums),
+ *   residual (kernels.cpp:106-121; bit-identical), entropy_approx (:123-132),
+ *   entropy_of_normalized (:134-148), diff_mutual_info (:150-159; exactly antisymmetric).
+ * Entropies use the engine's table-driven FP64 element math (a few ulp from libm). */
+int plg_standardize(plg_ctx* ctx, const double* x, int64_t n, double* out, plg_status* st);
+int plg_residual(plg_ctx* ctx, const double* xi, int64_t ni, const double* xj, int64_t nj, double* out,
+                 plg_status* st);
+int plg_entropy_approx(plg_ctx* ctx, const double* u, int64_t n, double* out, plg_status* st);
+int plg_entropy_of_normalized(plg_ctx* ctx, const double* r, int64_t n, double* out, plg_status* st);
+int plg_diff_mutual_info(plg_ctx* ctx, const double* xi_std, const double* xj_std, const double* ri_j,
+                         const double* rj_i, int64_t n, double* out, plg_status* st);
+
 /* Round schedule (host-only, no device needed): the rank's contiguous share of the pair
  * tiles and the round's sample segmentation. The segmentation depends only on (u, n), so
  * every pair entropy has the same bits for any world size. */

@@ -18,6 +18,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <initializer_list>
 #include <limits>
 #include <string>
 #include <vector>
@@ -32,7 +33,10 @@ using plg::kBT;
 using plg::kTilePairs;
 
 constexpr double kZeroVarTol = 1e-12;  // partial variance relative to the standardised 1.0
-constexpr int kTargetCtas = 4 * 148 * 8;  // sized so 8 ranks still get several waves
+// Pair-kernel CTAs per round over all ranks: ~16 waves even when 8 ranks split the tiles,
+// so the last partial wave costs little; the segmentation is chosen from this constant and
+// (u, n) only, never from the rank count.
+constexpr int kTargetCtas = 16 * 148 * 8;
 
 int set_status(plg_status* st, int32_t code, int64_t row, int64_t col, const char* fmt, ...) {
   if (st) {
@@ -623,6 +627,122 @@ int plg_regress_out(plg_ctx* c, const double* X, int64_t n, int32_t d, int64_t l
                            c->stream));
   PLG_CUDA(cudaStreamSynchronize(c->stream));
   PLG_CUDA(cudaGetLastError());
+  return ok(st);
+}
+
+// ---- element kernels of the reference's plingam::kernels namespace (kernels.hpp:25-70) ----
+
+namespace {
+
+// Mean/sd of one device column with the reference's left-to-right sums; returns sd.
+int device_moments(plg_ctx* c, const double* d_x, int64_t n, double* mean, double* sd, plg_status* st) {
+  PLG_CUDA(c->W.reserve(static_cast<size_t>(round_up(n, 16))));
+  PLG_CUDA(c->stat.reserve(2));
+  PLG_CUDA(c->msd.reserve(2));
+  plg::launch_standardize(d_x, n, n, nullptr, 1, c->W.p, round_up(n, 16), c->stat.p, c->msd.p, 0, c->stream);
+  double msd[2];
+  PLG_CUDA(cudaMemcpyAsync(msd, c->msd.p, sizeof(msd), cudaMemcpyDeviceToHost, c->stream));
+  PLG_CUDA(cudaStreamSynchronize(c->stream));
+  *mean = msd[0];
+  *sd = msd[1];
+  return 0;
+}
+
+int device_entropy(plg_ctx* c, const double* d_u, int64_t n, double scale, double* out, plg_status* st) {
+  PLG_CUDA(c->H.reserve(1));
+  plg::launch_entropy_vec(d_u, n, scale, c->H.p, c->g_exp, c->g_log, c->stream);
+  PLG_CUDA(cudaMemcpyAsync(out, c->H.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  PLG_CUDA(cudaStreamSynchronize(c->stream));
+  PLG_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int upload_vectors(plg_ctx* c, std::initializer_list<const double*> vs, int64_t n, plg_status* st) {
+  PLG_CUDA(c->Xd.reserve(static_cast<size_t>(n) * vs.size()));
+  size_t i = 0;
+  for (const double* v : vs)
+    PLG_CUDA(cudaMemcpyAsync(c->Xd.p + i++ * n, v, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  return 0;
+}
+
+// entropy_of_normalized (kernels.cpp:134-148) of device vector d_r.
+int device_eon(plg_ctx* c, const double* d_r, int64_t n, double* out, plg_status* st) {
+  double m, sd;
+  if (int rc = device_moments(c, d_r, n, &m, &sd, st)) return rc;
+  if (sd == 0.0)
+    return set_status(st, PLG_ZeroVariance, -1, -1, "entropy_of_normalized: zero residual (exactly collinear pair)");
+  return device_entropy(c, d_r, n, 1.0 / sd, out, st);
+}
+
+}  // namespace
+
+int plg_standardize(plg_ctx* c, const double* x, int64_t n, double* out, plg_status* st) {
+  if (!c) return set_status(st, PLG_OutOfRange, -1, -1, "null context");
+  if (n < 2) return set_status(st, PLG_TooShort, -1, -1, "standardize: need at least 2 samples");
+  if (int rc = begin_call(c, st)) return rc;
+  if (int rc = upload_vectors(c, {x}, n, st)) return rc;
+  double m, sd;
+  if (int rc = device_moments(c, c->Xd.p, n, &m, &sd, st)) return rc;
+  if (sd == 0.0) return set_status(st, PLG_ZeroVariance, -1, -1, "standardize: constant input");
+  PLG_CUDA(cudaMemcpyAsync(out, c->W.p, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  PLG_CUDA(cudaStreamSynchronize(c->stream));
+  return ok(st);
+}
+
+int plg_residual(plg_ctx* c, const double* xi, int64_t ni, const double* xj, int64_t nj, double* out,
+                 plg_status* st) {
+  if (!c) return set_status(st, PLG_OutOfRange, -1, -1, "null context");
+  if (ni != nj) return set_status(st, PLG_LengthMismatch, -1, -1, "residual: length mismatch");
+  if (ni < 2) return set_status(st, PLG_TooShort, -1, -1, "residual: need at least 2 samples");
+  if (int rc = begin_call(c, st)) return rc;
+  if (int rc = upload_vectors(c, {xi, xj}, ni, st)) return rc;
+  PLG_CUDA(c->idx.reserve(1));
+  PLG_CUDA(c->stat.reserve(1));
+  PLG_CUDA(c->W.reserve(static_cast<size_t>(ni)));
+  PLG_CUDA(cudaMemsetAsync(c->idx.p, 0, sizeof(int), c->stream));
+  PLG_CUDA(cudaMemsetAsync(c->stat.p, 0, sizeof(int), c->stream));
+  plg::launch_regress_out(c->Xd.p, ni, ni, 1, c->idx.p, 1, c->W.p, ni, c->stat.p, c->stream);
+  int zero_var = 0;
+  PLG_CUDA(cudaMemcpyAsync(&zero_var, c->stat.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  PLG_CUDA(cudaStreamSynchronize(c->stream));
+  if (zero_var) return set_status(st, PLG_ZeroVariance, -1, -1, "residual: regressor has zero variance");
+  PLG_CUDA(cudaMemcpyAsync(out, c->W.p, ni * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  PLG_CUDA(cudaStreamSynchronize(c->stream));
+  return ok(st);
+}
+
+int plg_entropy_approx(plg_ctx* c, const double* u, int64_t n, double* out, plg_status* st) {
+  if (!c) return set_status(st, PLG_OutOfRange, -1, -1, "null context");
+  if (n < 1) return set_status(st, PLG_TooShort, -1, -1, "entropy_approx: empty input");
+  if (int rc = begin_call(c, st)) return rc;
+  if (int rc = upload_vectors(c, {u}, n, st)) return rc;
+  if (int rc = device_entropy(c, c->Xd.p, n, 1.0, out, st)) return rc;
+  return ok(st);
+}
+
+int plg_entropy_of_normalized(plg_ctx* c, const double* r, int64_t n, double* out, plg_status* st) {
+  if (!c) return set_status(st, PLG_OutOfRange, -1, -1, "null context");
+  if (n < 1) return set_status(st, PLG_TooShort, -1, -1, "entropy_of_normalized: empty input");
+  if (int rc = begin_call(c, st)) return rc;
+  if (int rc = upload_vectors(c, {r}, n, st)) return rc;
+  if (int rc = device_eon(c, c->Xd.p, n, out, st)) return rc;
+  return ok(st);
+}
+
+int plg_diff_mutual_info(plg_ctx* c, const double* xi_std, const double* xj_std, const double* ri_j,
+                         const double* rj_i, int64_t n, double* out, plg_status* st) {
+  if (!c) return set_status(st, PLG_OutOfRange, -1, -1, "null context");
+  if (n < 1) return set_status(st, PLG_TooShort, -1, -1, "diff_mutual_info: empty input");
+  if (int rc = begin_call(c, st)) return rc;
+  if (int rc = upload_vectors(c, {xi_std, xj_std, ri_j, rj_i}, n, st)) return rc;
+  double hj, e1, hi, e2;  // kernels.cpp:156-158, in the reference's evaluation order
+  if (int rc = device_entropy(c, c->Xd.p + n, n, 1.0, &hj, st)) return rc;
+  if (int rc = device_eon(c, c->Xd.p + 2 * n, n, &e1, st)) return rc;
+  if (int rc = device_entropy(c, c->Xd.p, n, 1.0, &hi, st)) return rc;
+  if (int rc = device_eon(c, c->Xd.p + 3 * n, n, &e2, st)) return rc;
+  const double favor_i = hj + e1;
+  const double favor_j = hi + e2;
+  *out = favor_i - favor_j;
   return ok(st);
 }
 

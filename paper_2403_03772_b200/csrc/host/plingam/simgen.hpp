@@ -29,4 +29,14 @@ Dag gen_sparse_dag(int d, double avg_parents, std::uint64_t seed, double wmin = 
 // n x d column-major samples.
 std::vector<double> sample_lingam(const Dag& dag, std::int64_t n, std::uint64_t seed, const NoiseSpec& noise);
 
+// x(t) = B0 x(t) + sum_tau lagged[tau-1] x(t - tau) + eps(t), burn_in rows discarded
+// (simgen.cpp:83-130); the instantaneous system is solved by substitution in B0's causal
+// order. lagged[tau]: d x d column-major. Throws UnstableSystem past |x| > 1e9.
+// Returns T x d column-major.
+std::vector<double> sample_svar(const Dag& b0, const std::vector<std::vector<double>>& lagged, int T,
+                                int burn_in, std::uint64_t seed, const NoiseSpec& noise);
+
+// d-vector of U(lo, hi) draws from the seeded generator (e.g. a random lag diagonal).
+std::vector<double> uniform_vector(int d, std::uint64_t seed, double lo, double hi);
+
 }  // namespace plingam::sim

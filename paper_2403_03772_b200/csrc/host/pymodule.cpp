@@ -12,6 +12,7 @@
 #include "../../../include/plingam_b200.h"
 #include "plingam/plingam.hpp"
 #include "plingam/simgen.hpp"
+#include "plingam/var.hpp"
 
 namespace py = pybind11;
 using namespace plingam;
@@ -154,6 +155,109 @@ PYBIND11_MODULE(_core, m) {
       },
       py::arg("dag"), py::arg("threshold") = 0.05);
 
+  // ---- element kernels (pymodule.cpp:79-96) ----
+  using CArray = py::array_t<double, py::array::c_style | py::array::forcecast>;
+  m.def(
+      "standardize",
+      [](const CArray& x) {
+        py::array_t<double> out(x.size());
+        plg_status st{};
+        int rc;
+        {
+          py::gil_scoped_release rel;
+          rc = plg_standardize(gpu::context(), x.data(), x.size(), out.mutable_data(), &st);
+        }
+        gpu::check(rc, &st);
+        return out;
+      },
+      py::arg("x"));
+  m.def(
+      "residual",
+      [](const CArray& xi, const CArray& xj) {
+        py::array_t<double> out(xi.size());
+        plg_status st{};
+        int rc;
+        {
+          py::gil_scoped_release rel;
+          rc = plg_residual(gpu::context(), xi.data(), xi.size(), xj.data(), xj.size(), out.mutable_data(), &st);
+        }
+        gpu::check(rc, &st);
+        return out;
+      },
+      py::arg("xi"), py::arg("xj"));
+  m.def(
+      "entropy_approx",
+      [](const CArray& u) {
+        double out = 0.0;
+        plg_status st{};
+        int rc;
+        {
+          py::gil_scoped_release rel;
+          rc = plg_entropy_approx(gpu::context(), u.data(), u.size(), &out, &st);
+        }
+        gpu::check(rc, &st);
+        return out;
+      },
+      py::arg("u"));
+  m.def(
+      "diff_mutual_info",
+      [](const CArray& xi, const CArray& xj, const CArray& ri, const CArray& rj) {
+        if (xi.size() != xj.size() || xi.size() != ri.size() || xi.size() != rj.size())
+          throw Error(ErrorCode::LengthMismatch, "diff_mutual_info: length mismatch");
+        double out = 0.0;
+        plg_status st{};
+        int rc;
+        {
+          py::gil_scoped_release rel;
+          rc = plg_diff_mutual_info(gpu::context(), xi.data(), xj.data(), ri.data(), rj.data(), xi.size(), &out, &st);
+        }
+        gpu::check(rc, &st);
+        return out;
+      },
+      py::arg("xi_std"), py::arg("xj_std"), py::arg("ri_j"), py::arg("rj_i"));
+
+  // ---- VarLiNGAM (pymodule.cpp:57-61, 136-154) ----
+  py::class_<VarModel>(m, "VarModel")
+      .def_readonly("b0", &VarModel::b0)
+      .def_property_readonly("b_lagged",
+                             [](const VarModel& v) {
+                               std::vector<py::array_t<double>> out;
+                               for (const auto& b : v.b_lagged) out.push_back(colmajor_array(b, v.b0.d, v.b0.d));
+                               return out;
+                             })
+      .def_property_readonly("m_raw",
+                             [](const VarModel& v) {
+                               std::vector<py::array_t<double>> out;
+                               for (const auto& b : v.m_raw) out.push_back(colmajor_array(b, v.b0.d, v.b0.d));
+                               return out;
+                             })
+      .def_readonly("lag", &VarModel::lag);
+  m.def(
+      "estimate_var",
+      [](const FArray& X, int lag) {
+        DataMatrix ts = to_data(X);
+        VarEstimate est;
+        {
+          py::gil_scoped_release rel;
+          est = estimate_var(ts, lag);
+        }
+        std::vector<py::array_t<double>> ms;
+        for (const auto& M : est.m_raw) ms.push_back(colmajor_array(M, ts.dims(), ts.dims()));
+        return py::make_tuple(ms, colmajor_array(est.residuals.values, est.residuals.rows, est.residuals.cols));
+      },
+      py::arg("X"), py::arg("lag") = 1);
+  m.def(
+      "fit_var_lingam",
+      [](const FArray& X, int lag, bool parallel, int workers) {
+        DataMatrix ts = to_data(X);
+        DirectLingamConfig cfg;
+        cfg.parallel = parallel;
+        cfg.workers = workers;
+        py::gil_scoped_release rel;
+        return fit_varlingam(ts, lag, cfg);
+      },
+      py::arg("X"), py::arg("lag") = 1, py::arg("parallel") = false, py::arg("workers") = 1);
+
   // ---- device selection / multi-GPU ranks ----
   m.def("set_device", &gpu::set_device, py::arg("device"));
   m.def("reset", &gpu::reset);
@@ -194,6 +298,33 @@ PYBIND11_MODULE(_core, m) {
       },
       py::arg("dag"), py::arg("samples"), py::arg("seed") = 0,
       py::arg("noise") = std::pair<double, double>{0.0, 1.0}, py::arg("kind") = "uniform");
+  m.def(
+      "sample_svar",
+      [](const sim::Dag& b0, const std::vector<FArray>& lagged, int T, int burn_in, std::uint64_t seed,
+         std::pair<double, double> noise, const std::string& kind) {
+        sim::NoiseSpec spec;
+        spec.lo = noise.first;
+        spec.hi = noise.second;
+        if (kind == "uniform") spec.kind = sim::NoiseKind::Uniform;
+        else if (kind == "laplace") spec.kind = sim::NoiseKind::Laplace;
+        else if (kind == "t3") spec.kind = sim::NoiseKind::StudentT3;
+        else throw Error(ErrorCode::OutOfRange, "sample_svar: unknown noise kind " + kind);
+        std::vector<std::vector<double>> L;
+        for (const auto& M : lagged) {
+          if (M.ndim() != 2 || M.shape(0) != b0.d || M.shape(1) != b0.d)
+            throw Error(ErrorCode::DimensionMismatch, "sample_svar: lagged matrix shape mismatch");
+          L.emplace_back(M.data(), M.data() + M.size());
+        }
+        std::vector<double> X;
+        {
+          py::gil_scoped_release rel;
+          X = sim::sample_svar(b0, L, T, burn_in, seed, spec);
+        }
+        return colmajor_array(X, T, b0.d);
+      },
+      py::arg("b0"), py::arg("lagged"), py::arg("T"), py::arg("burn_in") = 100, py::arg("seed") = 0,
+      py::arg("noise") = std::pair<double, double>{0.0, 1.0}, py::arg("kind") = "uniform");
+  m.def("uniform_vector", &sim::uniform_vector, py::arg("d"), py::arg("seed"), py::arg("lo"), py::arg("hi"));
 
   // ---- low-level engine handle (bench, sampled-round parity, math probe) ----
   py::class_<Engine>(m, "Engine")

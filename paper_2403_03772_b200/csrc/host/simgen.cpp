@@ -128,4 +128,55 @@ std::vector<double> sample_lingam(const Dag& dag, std::int64_t n, std::uint64_t 
   return X;
 }
 
+std::vector<double> sample_svar(const Dag& b0, const std::vector<std::vector<double>>& lagged, int T,
+                                int burn_in, std::uint64_t seed, const NoiseSpec& noise) {
+  const int d = b0.d;
+  for (const auto& m : lagged)
+    if (m.size() != static_cast<std::size_t>(d) * d)
+      throw Error(ErrorCode::DimensionMismatch, "sample_svar: lagged matrix shape mismatch");
+  if (T < 1 || burn_in < 0) throw Error(ErrorCode::OutOfRange, "sample_svar: need T >= 1 and burn_in >= 0");
+  std::vector<std::vector<std::pair<int, double>>> parents(static_cast<std::size_t>(d));
+  for (int v = 0; v < d; ++v)
+    for (int j = 0; j < d; ++j) {
+      const double w = b0.weights[static_cast<std::size_t>(v) + static_cast<std::size_t>(d) * j];
+      if (w != 0.0) parents[static_cast<std::size_t>(v)].emplace_back(j, w);
+    }
+  const int k = static_cast<int>(lagged.size());
+  Rng rng(seed);
+  std::vector<std::vector<double>> history(static_cast<std::size_t>(k), std::vector<double>(d, 0.0));
+  std::vector<double> out(static_cast<std::size_t>(T) * d), rhs(d), x(d);
+  for (int t = 0; t < burn_in + T; ++t) {
+    for (int j = 0; j < d; ++j) rhs[j] = draw_noise(rng, noise);
+    for (int tau = 0; tau < k; ++tau) {
+      const auto& M = lagged[static_cast<std::size_t>(tau)];
+      const auto& h = history[static_cast<std::size_t>(tau)];
+      for (int j = 0; j < d; ++j) {
+        const double hj = h[j];
+        if (hj == 0.0) continue;
+        for (int i = 0; i < d; ++i) rhs[i] += M[static_cast<std::size_t>(j) * d + i] * hj;
+      }
+    }
+    for (int v : b0.order) {  // (I - B0) x = rhs by substitution in causal order
+      double s = rhs[v];
+      for (const auto& [j, w] : parents[static_cast<std::size_t>(v)]) s += w * x[j];
+      x[v] = s;
+    }
+    for (int j = 0; j < d; ++j)
+      if (!std::isfinite(x[j]) || std::fabs(x[j]) > 1e9)
+        throw Error(ErrorCode::UnstableSystem, "sample_svar: series exceeded overflow guard");
+    for (int tau = k - 1; tau > 0; --tau) history[static_cast<std::size_t>(tau)] = history[static_cast<std::size_t>(tau - 1)];
+    if (k > 0) history[0] = x;
+    if (t >= burn_in)
+      for (int j = 0; j < d; ++j) out[static_cast<std::size_t>(t - burn_in) + static_cast<std::size_t>(T) * j] = x[j];
+  }
+  return out;
+}
+
+std::vector<double> uniform_vector(int d, std::uint64_t seed, double lo, double hi) {
+  Rng rng(seed);
+  std::vector<double> v(static_cast<std::size_t>(d));
+  for (auto& x : v) x = rng.uniform(lo, hi);
+  return v;
+}
+
 }  // namespace plingam::sim

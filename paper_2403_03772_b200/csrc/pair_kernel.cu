@@ -324,6 +324,38 @@ __global__ void __launch_bounds__(kColentThreads)
   }
 }
 
+// entropy_approx(u * scale) of one vector (kernels.cpp:123-148), fixed-shape reduction.
+__global__ void __launch_bounds__(kColentThreads)
+    entropy_vec_kernel(const double* u, int64_t n, double scale, double* out, const double* g_exp,
+                       const double2* g_log) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ double s_red[2][kColentThreads / 32];
+  load_tables(smem, g_exp, g_log);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const TabPtr tp = table_ptrs(smem, lane);
+  double lc = 0.0, pd = 0.0;
+  for (int64_t t = threadIdx.x; t < n; t += kColentThreads) ede_accumulate(u[t] * scale, lc, pd, tp);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lc += __shfl_xor_sync(0xffffffffu, lc, o);
+    pd += __shfl_xor_sync(0xffffffffu, pd, o);
+  }
+  if (lane == 0) {
+    s_red[0][warp] = lc;
+    s_red[1][warp] = pd;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double l = 0.0, q = 0.0;
+    for (int w2 = 0; w2 < kColentThreads / 32; ++w2) {
+      l += s_red[0][w2];
+      q += s_red[1][w2];
+    }
+    *out = entropy_from_sums(l, q, 1.0 / static_cast<double>(n));
+  }
+}
+
 __global__ void math_probe_kernel(const double* u, int64_t n, double* out, const double* g_exp,
                                   const double2* g_log) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -393,6 +425,16 @@ void launch_colent(const double* W, int64_t ldw, int64_t n, const double* C, int
   const int grid = u < 4 * 148 ? u : 4 * 148;
   colent_kernel<<<grid, kColentThreads, kTableBytes, s>>>(W, ldw, n, C, ldc, act, u, H, g_exp,
                                                           g_log, nz, col_var, round, err);
+}
+
+void launch_entropy_vec(const double* u, int64_t n, double scale, double* out, const double* g_exp,
+                        const double2* g_log, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(entropy_vec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTableBytes);
+    attr = true;
+  }
+  entropy_vec_kernel<<<1, kColentThreads, kTableBytes, s>>>(u, n, scale, out, g_exp, g_log);
 }
 
 void launch_math_probe(const double* u, int64_t n, double* out, const double* g_exp,

@@ -130,6 +130,10 @@ void launch_residualize(double* W, int64_t ldw, int64_t n, const double* C, int6
 void launch_regress_out(const double* X, int64_t ldx, int64_t n, int exog, const int* remaining,
                         int r, double* out, int64_t ldo, int* zero_var_flag, cudaStream_t s);
 
+// entropy_approx(u * scale) of one vector (kernels.cpp:123-148).
+void launch_entropy_vec(const double* u, int64_t n, double scale, double* out, const double* g_exp,
+                        const double2* g_log, cudaStream_t s);
+
 // Test hook: evaluate lc/pdf element functions on a vector (custom and libdevice).
 void launch_math_probe(const double* u, int64_t n, double* out, const double* g_exp,
                        const double2* g_log, cudaStream_t s);

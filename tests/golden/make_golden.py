@@ -39,17 +39,40 @@ def config_input(name: str) -> np.ndarray:
     if name == "c3":  # Perturb-seq-shaped d=1000, n=10000, heavy-tailed noise, seed 1
         dag = plg.gen_sparse_dag(1000, avg_parents=2.0, seed=1)
         return plg.sample_lingam(dag, 10000, seed=1, noise=(0.0, 1.0), kind="t3")
+    if name == "c4":  # VarLiNGAM lag 1: d=500, T=2500 SVAR, Laplace noise; the path sees the residuals
+        return c4_residuals()
     if name == "c5":  # large synthetic d=2000, n=10000, Laplace noise, seed 1
         dag = plg.gen_sparse_dag(2000, avg_parents=2.0, seed=1)
         return plg.sample_lingam(dag, 10000, seed=1, noise=(0.0, 1.0), kind="laplace")
     raise ValueError(name)
 
 
+def c4_series():
+    """SVAR d=500, T=2500, burn-in 500: sparse acyclic B0 (|w| in [0.1, 0.5]) and a diagonal
+    lag-1 matrix with entries U(0.2, 0.5), so M1 = (I - B0)^-1 B1 has spectral radius <= 0.5."""
+    d = 500
+    b0 = plg.gen_sparse_dag(d, avg_parents=2.0, seed=1, wmin=0.1, wmax=0.5)
+    b1 = np.diag(plg.uniform_vector(d, 1, 0.2, 0.5))
+    return b0, plg.sample_svar(b0, [np.asfortranarray(b1)], T=2500, burn_in=500, seed=1, noise=(0.0, 1.0),
+                               kind="laplace")
+
+
+def c4_residuals():
+    _, X = c4_series()
+    return plg.estimate_var(X, 1)[1]
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--c3", action="store_true", help="also the d=1000 golden (hours on 8 cores)")
+    ap.add_argument("configs", nargs="*", default=["c1", "c2"], help="c1 c2 c4 (c3: hours on 8 cores)")
     args = ap.parse_args()
+    if "c1" in args.configs:
+        make_c1()
+    for name in [c for c in args.configs if c != "c1"]:
+        make_config(name)
 
+
+def make_c1():
     # C1: acceptance AC1 seeds (acceptance.cpp:39-69), two-level DAG d=10, m=10000, U(0,1) noise
     c1 = []
     for s in range(50):
@@ -64,8 +87,9 @@ def main():
                    "generator": "gen_two_level_dag + sample_lingam", "cases": c1}, f)
     print("c1 done", flush=True)
 
-    names = ["c2"] + (["c3"] if args.c3 else [])
-    for name in names:
+
+def make_config(name):
+    if True:
         X = config_input(name)
         t0 = time.time()
         order, scores = oracle_lib.causal_order(X, parallel=True, workers=WORKERS, fast=True, return_scores=True)
@@ -79,7 +103,12 @@ def main():
         with open(os.path.join(HERE, f"{name}_order.json"), "w") as f:
             json.dump({"config": name, "n": int(X.shape[0]), "d": int(X.shape[1]), "sha256": digest(X),
                        "order": order, "round0_scores": scores[0].tolist(), "round_gaps": gaps,
-                       "B": B.tolist() if X.shape[1] <= 100 else None, "used_pinv": pinv,
+                       "B": B.tolist() if X.shape[1] <= 100 else None,
+                       # larger d: 40 target rows spread over the order (full B is d^2 doubles)
+                       "B_rows": {int(order[p]): B[order[p]].tolist()
+                                  for p in np.linspace(1, X.shape[1] - 1, 40).astype(int)}
+                       if X.shape[1] > 100 else None,
+                       "used_pinv": pinv,
                        "oracle_seconds": el, "oracle_workers": WORKERS}, f)
         print(name, "done", el, flush=True)
 
