@@ -87,7 +87,7 @@ struct PairCfg {
   static_assert(kWarps * 32 == kCompute && kJStride % 8 == 0, "geometry");
 };
 
-template <int NI, int NJ, bool kDedicated>
+template <int NI, int NJ, bool kDedicated, bool kClampA>
 __global__ void __launch_bounds__(PairCfg<NI, NJ, kDedicated>::kThreads, 1) pair_kernel(const PairLaunch a) {
   using Cfg = PairCfg<NI, NJ, kDedicated>;
   constexpr int NQ = Cfg::NQ;
@@ -187,16 +187,14 @@ __global__ void __launch_bounds__(PairCfg<NI, NJ, kDedicated>::kThreads, 1) pair
         // is identically zero and entropy_of_normalized throws (kernels.cpp:136-139)
         atomicMin(a.err, err_key(a.round, kErrPairCollinear, -1));
       } else {
-        s1[q] = 1.0 / sqrt(v1);
+        s1[q] = kUScale / sqrt(v1);  // u' = K u (plg_math.cuh)
         bs1[q] = b1 * s1[q];
-        s2[q] = 1.0 / sqrt(v2);
+        s2[q] = kUScale / sqrt(v2);
         bs2[q] = b2 * s2[q];
       }
     }
   }
-  double lc[2 * NQ], pd[2 * NQ];  // [q] direction i|j, [NQ + q] direction j|i
-#pragma unroll
-  for (int q = 0; q < 2 * NQ; ++q) lc[q] = pd[q] = 0.0;
+  EdeAcc acc[2 * NQ];  // [q] direction i|j, [NQ + q] direction j|i
   const TabPtr tp = table_ptrs(smem, lane);
   const int jrow = diag ? 0 : kBT;
 
@@ -229,8 +227,8 @@ __global__ void __launch_bounds__(PairCfg<NI, NJ, kDedicated>::kThreads, 1) pair
         const double y = xj[q % NJ];
         const double u1 = fma(y, -bs1[q], x * s1[q]);  // (x_i - b_ij x_j) / sd_ij
         const double u2 = fma(x, -bs2[q], y * s2[q]);  // (x_j - b_ji x_i) / sd_ji
-        ede_accumulate(u1, lc[q], pd[q], tp);
-        ede_accumulate(u2, lc[NQ + q], pd[NQ + q], tp);
+        ede_accumulate<kClampA>(u1, acc[q], tp);
+        ede_accumulate<kClampA>(u2, acc[NQ + q], tp);
       }
     }
     __syncwarp();
@@ -242,8 +240,8 @@ __global__ void __launch_bounds__(PairCfg<NI, NJ, kDedicated>::kThreads, 1) pair
     const int slot = (ti + Cfg::kIStride * (q / NJ)) * kBT + tj + Cfg::kJStride * (q % NJ);
     double2* dst = reinterpret_cast<double2*>(
         a.part + ((static_cast<int64_t>(tl) * a.nseg + seg) * kTilePairs + slot) * 4);
-    dst[0] = make_double2(lc[q], pd[q]);
-    dst[1] = make_double2(lc[NQ + q], pd[NQ + q]);
+    dst[0] = make_double2(acc_lc(acc[q]), acc_pdf(acc[q]));
+    dst[1] = make_double2(acc_lc(acc[NQ + q]), acc_pdf(acc[NQ + q]));
   }
 }
 
@@ -300,8 +298,10 @@ __global__ void __launch_bounds__(kColentThreads)
       atomicMin(err, err_key(round, kErrColZeroVar, col_var[col]));  // ordering.cpp:56-62
     const double inv_sd = 1.0 / sqrt(ccc);
     const double* w = W + static_cast<int64_t>(col) * ldw;
-    double lc = 0.0, pd = 0.0;
-    for (int64_t t = threadIdx.x; t < n; t += kColentThreads) ede_accumulate(w[t] * inv_sd, lc, pd, tp);
+    EdeAcc acc;
+    const double su = inv_sd * kUScale;
+    for (int64_t t = threadIdx.x; t < n; t += kColentThreads) ede_accumulate<true>(w[t] * su, acc, tp);
+    double lc = acc_lc(acc), pd = acc_pdf(acc);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       lc += __shfl_xor_sync(0xffffffffu, lc, o);
@@ -334,8 +334,10 @@ __global__ void __launch_bounds__(kColentThreads)
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const TabPtr tp = table_ptrs(smem, lane);
-  double lc = 0.0, pd = 0.0;
-  for (int64_t t = threadIdx.x; t < n; t += kColentThreads) ede_accumulate(u[t] * scale, lc, pd, tp);
+  EdeAcc acc;
+  const double su = scale * kUScale;
+  for (int64_t t = threadIdx.x; t < n; t += kColentThreads) ede_accumulate<true>(u[t] * su, acc, tp);
+  double lc = acc_lc(acc), pd = acc_pdf(acc);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     lc += __shfl_xor_sync(0xffffffffu, lc, o);
@@ -366,8 +368,9 @@ __global__ void math_probe_kernel(const double* u, int64_t n, double* out, const
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const double v = u[i];
-    double lc = 0.0, pd = 0.0;
-    ede_accumulate(v, lc, pd, tp);
+    EdeAcc acc;
+    ede_accumulate<true>(v * kUScale, acc, tp);
+    const double lc = acc_lc(acc), pd = acc_pdf(acc);
     const double a = fabs(v);
     out[4 * i + 0] = lc;
     out[4 * i + 1] = pd;
@@ -376,36 +379,36 @@ __global__ void math_probe_kernel(const double* u, int64_t n, double* out, const
   }
 }
 
-template <int NI, int NJ, bool kDedicated>
+template <int NI, int NJ, bool kDedicated, bool kClampA>
 void launch_pair_cfg(const PairLaunch& a, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(pair_kernel<NI, NJ, kDedicated>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(pair_kernel<NI, NJ, kDedicated, kClampA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(kPairSmem));
     attr = true;
   }
-  pair_kernel<NI, NJ, kDedicated><<<a.ntiles * a.nseg, PairCfg<NI, NJ, kDedicated>::kThreads, kPairSmem, s>>>(a);
+  pair_kernel<NI, NJ, kDedicated, kClampA>
+      <<<a.ntiles * a.nseg, PairCfg<NI, NJ, kDedicated>::kThreads, kPairSmem, s>>>(a);
 }
 
 }  // namespace
 
 void launch_pair(const PairLaunch& a, cudaStream_t s) {
-  // PLG_PAIR_GEOM selects the thread geometry (tuning knob): "22d" = 2x2 pairs per thread +
-  // producer warp, "12d" = 1x2 + producer warp, "12" = 1x2 in-warp producer, "11" = 1x1.
-  static const int geom = [] {
+  // |u| <= sqrt(n) for a normalised residual; exp(-2|u|)'s scaling needs its clamp only past
+  // |u| ~ 350 (plg_math.cuh).
+  const bool clamp = a.n > 90000;
+  // PLG_PAIR_GEOM selects the thread geometry (tuning knob): "12" (default) = 1x2 pairs per
+  // thread, 512 threads, in-warp producer; "22d" = 2x2 pairs, 256 threads + producer warp.
+  static const bool g22 = [] {
     const char* v = std::getenv("PLG_PAIR_GEOM");
-    if (!v) return 2;
-    if (!strcmp(v, "22d")) return 0;
-    if (!strcmp(v, "12d")) return 1;
-    if (!strcmp(v, "12")) return 2;
-    if (!strcmp(v, "11")) return 3;
-    return 2;
+    return v && !strcmp(v, "22d");
   }();
-  switch (geom) {
-    case 0: launch_pair_cfg<2, 2, true>(a, s); break;
-    case 1: launch_pair_cfg<1, 2, true>(a, s); break;
-    case 3: launch_pair_cfg<1, 1, false>(a, s); break;
-    default: launch_pair_cfg<1, 2, false>(a, s); break;
+  if (g22) {
+    if (clamp) launch_pair_cfg<2, 2, true, true>(a, s);
+    else launch_pair_cfg<2, 2, true, false>(a, s);
+  } else {
+    if (clamp) launch_pair_cfg<1, 2, false, true>(a, s);
+    else launch_pair_cfg<1, 2, false, false>(a, s);
   }
 }
 

@@ -7,15 +7,19 @@
 // libdevice exp + log1p + exp cost ~70 FP64-pipe instructions per EDE. Here both
 // exponentials use a 128-entry 2^(j/128) table (|reduced arg| <= ln2/256) and log1p a
 // 128-entry reciprocal/log table (|r| <= 1/257), each finished by a degree-4 near-minimax
-// polynomial (tools/fit_polys.py): 29 FP64 instructions per EDE plus ~20 integer/LDS ones
-// (index and exponent arithmetic, table reads), checked in SASS. Absolute error per
-// element is a few ulp of lc and pdf (tests/test_gpu_parity.py checks against libdevice
-// and numpy); the causal order needs ~1e-9.
+// polynomial (tools/fit_polys.py). Absolute error per element is a few ulp of lc and pdf
+// (tests/test_gpu_parity.py checks against libdevice and numpy); the causal order needs
+// ~1e-9.
 //
 // Throughput is bound by register-file reads rather than by the FP64 pipe itself: a DFMA
 // reading 3 distinct register pairs takes 3 issue cycles instead of 2, and integer
 // instructions share the read ports (measured, tools/probe/fp64_mix.cu; model and SASS
-// census in tools/rf_model.py, which predicts the measured 69% FP64-pipe utilisation).
+// census in tools/rf_model.py). The formulation below is shaped by that:
+//   * the caller supplies u scaled by K = 256/ln2, so exp(-2|u|) reduces with one
+//     immediate-operand DADD (k = rint(-|u'|), r' = |u'| + k) instead of two DFMAs with a
+//     register constant; sum |u| is kept apart and rescaled once at the end;
+//   * each polynomial's leading coefficient is a short double, so its first Horner step
+//     is DMUL-by-immediate + DADD (1 register pair each) instead of a 3-pair DFMA.
 //
 // Shared-memory tables, replicated per lane group so random per-lane indices never
 // bank-conflict:
@@ -49,25 +53,29 @@ constexpr double kGaussianEntropy = 1.4189385332046727418;  // 0.5 * (1 + log(2 
 constexpr double kLn2 = 0.69314718055994530942;
 
 constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52: round-to-int in the low word
+constexpr double kUScale = 369.32993046757461;  // K = 256 / ln2: callers pass u' = K u
+constexpr double kInvUScale = 0.0027076061740622863;  // ln2 / 256
 
-// Coefficients that are not short doubles live in the constant bank: ptxas loads them
-// once (uniform registers for DFMA's addend slot) instead of re-materialising register
-// pairs every iteration (measured: -20 issue slots per 8 EDE in the pair kernel's loop).
-static __constant__ double kC[16] = {
-    -256.0 / kLn2,  // 0  exp(-2a):  k = rint(-2a * 128 / ln2)
-    kLn2 / 256.0,   // 1            r = a + k ln2/256, exp(-2a) = 2^(k/128) e^(-2r)
-    -64.0 / kLn2,   // 2  exp(-q/2): k = rint(-q/2 * 128 / ln2)
-    kLn2 / 64.0,    // 3            r = q + k ln2/64,  exp(-q/2) = 2^(k/128) e^(-r/2)
-    // near-minimax degree-4 fits (tools/fit_polys.py, mpmath), highest degree first:
-    0.6666668744024424, -1.3333339565406885, 1.999999999999903, -1.9999999999997087,
-    //   4-7  exp(-2r),   |r| <= 1.01 ln2/512: max rel err 8.0e-17
-    0.0026041674781345408, -0.02083334307094826, 0.12499999999999394, -0.49999999999992717,
-    //   8-11 exp(-r/2),  |r| <= 1.01 ln2/128: max rel err 8.0e-17
-    0.20000270365230982, -0.25000315425970154, 0.3333333333230998, -0.4999999999880609,
-    //  12-15 log1p(r)/r, |r| <= 1/257: max rel err 9.3e-15 (abs err of log1p <= 3.6e-17)
+// Coefficients that are not short doubles live in the constant bank (uniform registers
+// for the addend slot). Near-minimax degree-4 fits (tools/fit_polys.py, mpmath) whose
+// leading coefficient is a short double used as an immediate (kLead*), highest degree
+// first:
+static __constant__ double kC[12] = {
+    -0.00067690154351557160,  // 0  exp(-q/2), q' = u'^2: k = rint(q' * -ln2/1024)
+    1477.3197218702985,       // 1                        r' = q' + k * 1024/ln2
+    -2.6466431340771855e-08, 1.4662262387638428e-05, -0.005415212348124257,
+    //  2-4  exp(-x ln2/128),    |x| <= 0.505:          max rel err 1.6e-16
+    -8.20865303897247e-18, 6.718185572625523e-12, -3.6655655969098924e-06,
+    //  5-7  exp(-x / (2 K^2)),  |x| <= 1.01 * 512/ln2: max rel err 1.6e-16
+    -0.2500025234041795, 0.33333333332155823, -0.4999999999952244,
+    //  8-10 log1p(r)/r,         |r| <= 1/257:          max rel err 1.9e-14 (abs of log1p <= 7e-17)
+    0.0,
 };
-// 2^(k/128) scaling is clamped at 2^-100: below it the term is < 1e-30 absolute (the true
-// value is smaller still) and the exponent field stays normal for any finite input.
+constexpr double kLead1 = 3.583033869603014e-11;   // exp1 x^4 (short double)
+constexpr double kLead2 = 7.522337778472381e-24;   // exp2 x^4 (short double)
+constexpr double kLeadL = 0.20000267028808594;     // log1p x^4 (short double)
+// 2^(k/128) scaling is clamped at 2^-100 where the input can leave the normal range: below
+// it the term is < 1e-30 absolute (the true value is smaller still).
 constexpr int kMinScaledK = -100 * kExpN;
 
 // Fill the shared-memory tables (every thread of the block, then __syncthreads()).
@@ -96,9 +104,11 @@ __device__ __forceinline__ TabPtr table_ptrs(const unsigned char* s_tab, int lan
   return {s_tab + (lane & (kExpRep - 1)) * 8, s_tab + kExpTableBytes + (lane & (kLogRep - 1)) * 16};
 }
 
-// v * 2^(k >> 7) with k clamped: add (k & ~127) << 13 to the high word (one IMAD).
+// v * 2^(k >> 7): add (k & ~127) << 13 to the high word (one IMAD), optionally clamped.
+template <bool kClamp>
 __device__ __forceinline__ double scale_pow2(double v, int k) {
-  const int kh = max(k & ~(kExpN - 1), kMinScaledK);
+  int kh = k & ~(kExpN - 1);
+  if (kClamp) kh = max(kh, kMinScaledK);
   return __hiloint2double(__double2hiint(v) + kh * (1 << (20 - kExpBits)), __double2loint(v));
 }
 
@@ -106,56 +116,55 @@ __device__ __forceinline__ double exp_row(const TabPtr& tp, int k) {
   return *reinterpret_cast<const double*>(tp.exp + (k & (kExpN - 1)) * kExpRowBytes);
 }
 
-// exp(-2a) for a >= 0.
-__device__ __forceinline__ double exp_m2a(double a, const TabPtr& tp) {
-  const double t = fma(a, kC[0], kMagic);
-  const int k = __double2loint(t);
-  const double kd = t - kMagic;
-  const double r = fma(kd, kC[1], a);  // exp(-2a) = 2^(k/128) * exp(-2r), |2r| <= ln2/128
-  double p = fma(r, kC[4], kC[5]);
-  p = fma(p, r, kC[6]);
-  p = fma(p, r, kC[7]);
-  p = fma(p, r, 1.0);
-  return scale_pow2(p * exp_row(tp, k), k);
-}
-
-// exp(-q/2) for q >= 0.
-__device__ __forceinline__ double exp_mhalf(double q, const TabPtr& tp) {
-  const double t = fma(q, kC[2], kMagic);
-  const int k = __double2loint(t);
-  const double kd = t - kMagic;
-  const double r = fma(kd, kC[3], q);  // exp(-q/2) = 2^(k/128) * exp(-r/2), |r/2| <= ln2/256
-  double p = fma(r, kC[8], kC[9]);
-  p = fma(p, r, kC[10]);
-  p = fma(p, r, kC[11]);
-  p = fma(p, r, 1.0);
-  return scale_pow2(p * exp_row(tp, k), k);
-}
-
-// a + log1p(v) - ln2 for v in (0, 1]: y = 1 + v in (1, 2]; r = y c - 1 (one rounding);
-// log y = -log c + log1p(r). The rounding of 1 + v perturbs the result by <= 1.1e-16.
-__device__ __forceinline__ double logcosh_tail(double a, double v, const TabPtr& tp) {
-  const double y = 1.0 + v;
-  const unsigned row = (static_cast<unsigned>(__double2hiint(y)) >> (20 - kLogBits)) & (kLogRows - 1);
-  const double2 cl = *reinterpret_cast<const double2*>(tp.log + row * kLogRowBytes);
-  const double r = fma(y, cl.x, -1.0);
-  double p = fma(r, kC[12], kC[13]);  // log1p(r) = r p(r)
-  p = fma(p, r, kC[14]);
-  p = fma(p, r, kC[15]);
-  p = fma(p, r, 1.0);
-  return fma(r, p, a + cl.y);
+// Horner p(x) = 1 + x (c1 + x (c2 + x (c3 + lead x))) with the leading step as
+// DMUL-by-immediate + DADD (no contraction).
+__device__ __forceinline__ double poly4(double x, double lead, double c3, double c2, double c1) {
+  double p = __dadd_rn(__dmul_rn(x, lead), c3);
+  p = fma(p, x, c2);
+  p = fma(p, x, c1);
+  return fma(p, x, 1.0);
 }
 
 __device__ __forceinline__ double abs_int(double u) {  // |u| on the integer pipe
   return __hiloint2double(__double2hiint(u) & 0x7fffffff, __double2loint(u));
 }
 
-// Accumulate one EDE of sample u into (s_lc, s_pdf).
-__device__ __forceinline__ void ede_accumulate(double u, double& s_lc, double& s_pdf, const TabPtr& tp) {
-  s_pdf = fma(u, exp_mhalf(u * u, tp), s_pdf);
-  const double a = abs_int(u);
-  s_lc += logcosh_tail(a, exp_m2a(a, tp), tp);
+// Running sums of one residual direction: sum lc = tail + a / K, sum pdf = pdf / K.
+struct EdeAcc {
+  double tail = 0.0;
+  double a = 0.0;
+  double pdf = 0.0;
+};
+
+// Accumulate one EDE. us = K u (K = 256/ln2). kClampA must be true when |u| can exceed
+// ~350 (n > ~1.2e5 samples); |u| <= sqrt(n) for a normalised residual.
+template <bool kClampA>
+__device__ __forceinline__ void ede_accumulate(double us, EdeAcc& acc, const TabPtr& tp) {
+  // pdf = u exp(-u^2/2) in q' = us^2 units (clamped: q' reaches the subnormal range)
+  const double q = us * us;
+  const double t2 = fma(q, kC[0], kMagic);
+  const int k2 = __double2loint(t2);
+  const double r2 = fma(t2 - kMagic, kC[1], q);
+  const double e2 = scale_pow2<true>(poly4(r2, kLead2, kC[5], kC[6], kC[7]) * exp_row(tp, k2), k2);
+  acc.pdf = fma(us, e2, acc.pdf);
+  // exp(-2|u|): k = rint(-|us|), r' = |us| + k, exp(-2|u|) = 2^(k/128) exp(-r' ln2/128)
+  const double a = abs_int(us);
+  const double t1 = kMagic - a;
+  const int k1 = __double2loint(t1);
+  const double r1 = a + (t1 - kMagic);
+  const double v = scale_pow2<kClampA>(poly4(r1, kLead1, kC[2], kC[3], kC[4]) * exp_row(tp, k1), k1);
+  // log1p(v) - ln2: y = 1 + v in (1, 2]; r = y c - 1 (one rounding); log y = -log c + log1p(r).
+  // The rounding of 1 + v perturbs the result by <= 1.1e-16.
+  const double y = 1.0 + v;
+  const unsigned row = (static_cast<unsigned>(__double2hiint(y)) >> (20 - kLogBits)) & (kLogRows - 1);
+  const double2 cl = *reinterpret_cast<const double2*>(tp.log + row * kLogRowBytes);
+  const double r = fma(y, cl.x, -1.0);
+  acc.tail += fma(r, poly4(r, kLeadL, kC[8], kC[9], kC[10]), cl.y);
+  acc.a += a;
 }
+
+__device__ __forceinline__ double acc_lc(const EdeAcc& acc) { return fma(acc.a, kInvUScale, acc.tail); }
+__device__ __forceinline__ double acc_pdf(const EdeAcc& acc) { return acc.pdf * kInvUScale; }
 
 // Entropy from the two sums (kernels.cpp:36-40): H = (kG - (k1 t1) t1) - (k2 t2) t2.
 __device__ __forceinline__ double entropy_from_sums(double s_lc, double s_pdf, double inv_n) {

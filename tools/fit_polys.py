@@ -41,3 +41,33 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def short(x):
+    """Round to a double whose low 32 bits are zero (a DMUL/DADD 32-bit immediate)."""
+    import struct
+
+    bits = struct.unpack("<Q", struct.pack("<d", float(x)))[0]
+    lo = bits & 0xFFFFFFFF
+    bits = (bits >> 32) << 32
+    if lo >= 0x80000000:
+        bits += 1 << 32
+    return struct.unpack("<d", struct.pack("<Q", bits))[0]
+
+
+def fit_short_lead(f, lo, hi, deg):
+    """Near-minimax fit whose leading coefficient is a short double (immediate operand):
+    fit deg first, round the leading coefficient, refit the rest to f - c x^deg."""
+    coeffs, _ = fit(f, lo, hi, deg)
+    c = short(coeffs[0])
+    rest, _ = fit(lambda x: f(x) - mp.mpf(c) * x ** deg, lo, hi, deg - 1)
+    full = [c] + rest
+    worst = mp.mpf(0)
+    N = 4000
+    for i in range(N + 1):
+        x = lo + (hi - lo) * i / N
+        p = mp.mpf(0)
+        for cc in full:
+            p = p * x + mp.mpf(cc)
+        worst = max(worst, abs(p - f(x)) / abs(f(x)))
+    return full, float(worst)
