@@ -75,6 +75,8 @@ struct NcclApi {
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -88,8 +90,11 @@ NcclApi& nccl() {
       api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
       api.AllGather = reinterpret_cast<decltype(api.AllGather)>(dlsym(h, "ncclAllGather"));
       api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+      api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(dlsym(h, "ncclGroupStart"));
+      api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(dlsym(h, "ncclGroupEnd"));
       api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
-      api.loaded = api.GetUniqueId && api.CommInitRank && api.AllGather && api.CommDestroy;
+      api.loaded = api.GetUniqueId && api.CommInitRank && api.AllGather && api.CommDestroy && api.GroupStart &&
+                   api.GroupEnd;
     }
   }
   return api;
@@ -150,7 +155,7 @@ struct plg_ctx {
   DevBuf<double> Xd, W, C, part, epack, H, k, scores, msd, gscr;
   DevBuf<int> act0, act1, colvar, order, stat, idx, nz;
   DevBuf<plg::RoundState> rs;
-  DevBuf<unsigned long long> err;
+  DevBuf<unsigned long long> err, errs;
   std::vector<cudaEvent_t> ev;  // pool: [0]=start [1]=end [2]=h2d end, then 2 per round
   plg_stats last{};
   int64_t launches = 0;
@@ -193,6 +198,7 @@ int ctx_init(plg_ctx* ctx, int device, plg_status* st) {
   PLG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
   if (int rc = make_tables(ctx, st)) return rc;
   PLG_CUDA(ctx->err.reserve(1));
+  PLG_CUDA(ctx->errs.reserve(64));
   PLG_CUDA(ctx->rs.reserve(1));
   return ok(st);
 }
@@ -258,13 +264,21 @@ int search_round(plg_ctx* c, int64_t n, int64_t ldw, int ldc, int u, const int* 
   }
   if (c->timing) cudaEventRecord(c->ev[ev_base + 1], c->stream);
   if (c->world > 1) {
+    // One grouped exchange per round: the entropy tiles (in place, rank slots of tpr tiles)
+    // and every rank's error key.
     const size_t cnt = static_cast<size_t>(rp.tpr) * 2 * kTilePairs;
-    ncclResult_t r = nccl().AllGather(c->epack.p + static_cast<size_t>(c->rank) * cnt, c->epack.p, cnt,
-                                      ncclDouble, c->comm, c->stream);
-    if (r != ncclSuccess)
-      return set_status(st, PLG_NcclError, -1, -1, "ncclAllGather: %s", nccl().GetErrorString(r));
+    NcclApi& api = nccl();
+    api.GroupStart();
+    ncclResult_t r = api.AllGather(c->epack.p + static_cast<size_t>(c->rank) * cnt, c->epack.p, cnt, ncclDouble,
+                                   c->comm, c->stream);
+    ncclResult_t r2 = api.AllGather(c->err.p, c->errs.p, 1, ncclUint64, c->comm, c->stream);
+    ncclResult_t r3 = api.GroupEnd();
+    if (r != ncclSuccess || r2 != ncclSuccess || r3 != ncclSuccess)
+      return set_status(st, PLG_NcclError, -1, -1, "ncclAllGather: %s",
+                        api.GetErrorString(r != ncclSuccess ? r : (r2 != ncclSuccess ? r2 : r3)));
   }
-  plg::launch_kreduce(c->epack.p, c->H.p, u, rp.nb, c->k.p, c->err.p, c->stream);
+  plg::launch_kreduce(c->epack.p, c->H.p, u, rp.nb, c->k.p, c->err.p, c->world > 1 ? c->errs.p : c->err.p,
+                      c->world, c->stream);
   ++c->launches;
   return 0;
 }
@@ -461,8 +475,8 @@ int plg_nccl_unique_id(void* out_128_bytes, plg_status* st) {
 int plg_ctx_create_dist(int32_t device, int32_t rank, int32_t world, const void* nccl_uid_128,
                         plg_ctx** out, plg_status* st) {
   if (!out) return set_status(st, PLG_OutOfRange, -1, -1, "null output pointer");
-  if (world < 1 || rank < 0 || rank >= world)
-    return set_status(st, PLG_OutOfRange, -1, -1, "invalid rank %d / world %d", rank, world);
+  if (world < 1 || world > 64 || rank < 0 || rank >= world)
+    return set_status(st, PLG_OutOfRange, -1, -1, "invalid rank %d / world %d (1..64 ranks)", rank, world);
   plg_ctx* c = new plg_ctx();
   int rc = ctx_init(c, device, st);
   if (!rc && world > 1) {
@@ -513,6 +527,7 @@ void plg_ctx_destroy(plg_ctx* c) {
   c->nz.release();
   c->rs.release();
   c->err.release();
+  c->errs.release();
   if (c->g_exp) cudaFree(c->g_exp);
   if (c->g_log) cudaFree(c->g_log);
   if (c->stream) cudaStreamDestroy(c->stream);

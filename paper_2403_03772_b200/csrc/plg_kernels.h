@@ -108,8 +108,9 @@ void launch_gram(const double* W, int64_t ldw, int64_t n, int ncol, double* C, i
                  double* scratch, cudaStream_t s);
 
 // k[p] = sum_{q != p} min(0, M_pq)^2 with M_pq = (H_q + E(p|q)) - (H_p + E(q|p)).
+// errs[0..world): error keys gathered from every rank (world = 1: errs = err).
 void launch_kreduce(const double* epack, const double* H, int u, int nb, double* k,
-                    const unsigned long long* err, cudaStream_t s);
+                    unsigned long long* err, const unsigned long long* errs, int world, cudaStream_t s);
 
 // argmin over k (lowest position on ties), order/score bookkeeping, active-list compaction.
 void launch_commit(const double* k, const int* act_cur, int* act_nxt, int u, const int* col_var,

@@ -154,10 +154,17 @@ __device__ __forceinline__ int tile_index(int bi, int bj, int nb) {
   return bi * nb - (bi * (bi - 1)) / 2 + (bj - bi);
 }
 
-// Warp per candidate position p; lanes stride q, fixed xor-tree reduction.
+// Warp per candidate position p; lanes stride q, fixed xor-tree reduction. errs[0..world)
+// are the ranks' error keys gathered with the entropy tiles (a pair error is seen only by
+// the rank that owns the tile): every rank adopts the smallest, so all report the same.
 __global__ void kreduce_kernel(const double* epack, const double* H, int u, int nb, double* k,
-                               const unsigned long long* err) {
-  if (*err != kNoError) return;
+                               unsigned long long* err, const unsigned long long* errs, int world) {
+  unsigned long long key = *err;
+  for (int r = 0; r < world; ++r) key = min(key, errs[r]);
+  if (key != kNoError) {
+    if (threadIdx.x == 0) atomicMin(err, key);
+    return;
+  }
   const int p = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (p >= u) return;
@@ -332,8 +339,8 @@ void launch_gram(const double* W, int64_t ldw, int64_t n, int ncol, double* C, i
 }
 
 void launch_kreduce(const double* epack, const double* H, int u, int nb, double* k,
-                    const unsigned long long* err, cudaStream_t s) {
-  kreduce_kernel<<<(u + 7) / 8, 256, 0, s>>>(epack, H, u, nb, k, err);
+                    unsigned long long* err, const unsigned long long* errs, int world, cudaStream_t s) {
+  kreduce_kernel<<<(u + 7) / 8, 256, 0, s>>>(epack, H, u, nb, k, err, errs, world);
 }
 
 void launch_commit(const double* k, const int* act_cur, int* act_nxt, int u, const int* col_var,
