@@ -31,6 +31,7 @@ CONFIGS = {
     "c1": (10, 1000, "two-level DAG (gen_two_level_dag), U(0,1) noise, seed 42000"),
     "c2": (100, 10000, "sparse ER DAG (avg 2 parents, |w| in [0.5,1.5]), Laplace(0,1) noise, seed 1"),
     "c3": (1000, 10000, "sparse ER DAG (avg 2 parents), Student-t3 noise, seed 1 (Perturb-seq shaped)"),
+    "c4": (500, 2499, "VarLiNGAM lag 1: residuals of a d=500, T=2500 SVAR (sparse B0, diagonal B1, Laplace noise)"),
     "c5": (2000, 10000, "sparse ER DAG (avg 2 parents, |w| in [0.5,1.5]), Laplace(0,1) noise, seed 1"),
 }
 FP64_OPS_PER_EDE = 29     # FP64-pipe instructions per EDE in the pair kernel inner loop (cuobjdump SASS)
@@ -49,6 +50,11 @@ def make_input(name: str):
     if name == "c1":
         dag = plg.gen_two_level_dag(d, seed=42000)
         return plg.sample_lingam(dag, n, seed=42000)
+    if name == "c4":  # same generator as tests/golden/make_golden.py c4_series()
+        b0 = plg.gen_sparse_dag(d, avg_parents=2.0, seed=1, wmin=0.1, wmax=0.5)
+        b1 = np.asfortranarray(np.diag(plg.uniform_vector(d, 1, 0.2, 0.5)))
+        X = plg.sample_svar(b0, [b1], T=2500, burn_in=500, seed=1, noise=(0.0, 1.0), kind="laplace")
+        return plg.estimate_var(X, 1)[1]
     kind = "t3" if name == "c3" else "laplace"
     dag = plg.gen_sparse_dag(d, avg_parents=2.0, seed=1)
     return plg.sample_lingam(dag, n, seed=1, noise=(0.0, 1.0), kind=kind)

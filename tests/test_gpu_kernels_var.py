@@ -100,3 +100,37 @@ def test_c4_golden_order(plg):
     for t, row in fx["B_rows"].items():
         ref = np.asarray(row)
         assert np.all(np.abs(model.b0.weights[int(t)] - ref) <= 1e-6 * np.maximum(1.0, np.abs(ref)))
+
+
+def _sampled_rounds(engine, oracle, X, rounds):
+    """the GPU's working state after r rounds, searched by the oracle (all host
+    cores), must give the GPU's own next choice; scores agree to 1e-8 relative."""
+    full = engine.causal_order(X)
+    for r in rounds:
+        active, cols, prefix = engine.round_state(X, r)
+        assert prefix == full[:r]
+        c_ref, s_ref = oracle.search_causal_order(cols, list(range(len(active))), workers=os.cpu_count(), fast=True)
+        assert active[c_ref] == full[r], r
+        _, s_gpu = engine.search(cols, list(range(len(active))))
+        fin = np.isfinite(s_ref)
+        assert np.all(np.abs(np.asarray(s_gpu)[fin] - s_ref[fin]) <= 1e-8 * np.abs(s_ref[fin]) + 1e-15)
+    return full
+
+
+@pytest.mark.slow
+def test_c3_sampled_rounds(engine, oracle):
+    """BASELINE configs[2] (d=1000, n=10000, heavy-tailed noise): sampled-round parity."""
+    import bench
+
+    X = bench.make_input("c3")
+    full = _sampled_rounds(engine, oracle, X, (0, 500, 990))
+    assert sorted(full) == list(range(1000))
+
+
+@pytest.mark.slow
+def test_c5_sampled_rounds(engine, oracle):
+    """BASELINE configs[4] (d=2000, n=10000): late-round parity (u = 500 and 10)."""
+    import bench
+
+    X = bench.make_input("c5")
+    _sampled_rounds(engine, oracle, X, (1500, 1990))
