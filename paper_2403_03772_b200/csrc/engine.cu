@@ -904,48 +904,37 @@ extern "C" int plg_fit_weights(plg_ctx* c, const double* X, int64_t n, int32_t d
   if (int rc = reserve_run(c, n, d, ldw, st)) return rc;
   if (int rc = standardize_validate(c, c->Xd.p, n, n, d, nullptr, nullptr, ldw, true, st)) return rc;
   plg::launch_gram(c->W.p, ldw, n, d, c->C.p, d, c->gscr.p, c->stream);
-  std::vector<double> C(static_cast<size_t>(d) * d), msd(2 * static_cast<size_t>(d));
-  PLG_CUDA(cudaMemcpyAsync(C.data(), c->C.p, C.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-  PLG_CUDA(cudaMemcpyAsync(msd.data(), c->msd.p, msd.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  // Device: S = permuted correlation, S = L L^T (blocked FP64 Cholesky, chol_kernels.cu),
+  // then one backward substitution per target. Positions p <= deficient_from have a
+  // full-rank predecessor design.
+  const size_t dd = static_cast<size_t>(d) * d;
+  PLG_CUDA(c->part.reserve(2 * dd));  // scratch: S/L and the per-target beta rows
+  PLG_CUDA(c->scores.reserve(dd));    // B on device
+  PLG_CUDA(c->idx.reserve(d));
+  PLG_CUDA(c->stat.reserve(2));
+  PLG_CUDA(cudaMemcpyAsync(c->idx.p, order, d * sizeof(int32_t), cudaMemcpyHostToDevice, c->stream));
+  PLG_CUDA(cudaMemcpyAsync(c->stat.p, &d, sizeof(int32_t), cudaMemcpyHostToDevice, c->stream));
+  PLG_CUDA(cudaMemsetAsync(c->scores.p, 0, dd * sizeof(double), c->stream));
+  double* S = c->part.p;
+  plg::launch_permute(c->C.p, d, c->idx.p, d, S, c->stream);
+  plg::launch_cholesky(S, d, kZeroVarTol, c->stat.p, c->stream);
+  int deficient_from = d;
+  PLG_CUDA(cudaMemcpyAsync(&deficient_from, c->stat.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   PLG_CUDA(cudaStreamSynchronize(c->stream));
-  // L (row-major, lower) of the permuted correlation; S[p][q] = C[order[p]][order[q]]
-  std::vector<double> L(static_cast<size_t>(d) * d, 0.0);
-  int deficient_from = d;  // first position whose pivot vanishes
-  for (int j = 0; j < d; ++j) {
-    const double* Cj = &C[static_cast<size_t>(order[j]) * d];
-    double djj = Cj[order[j]];
-    for (int k = 0; k < j; ++k) djj -= L[static_cast<size_t>(j) * d + k] * L[static_cast<size_t>(j) * d + k];
-    if (!(djj > kZeroVarTol * Cj[order[j]])) {
-      deficient_from = j;
-      break;
-    }
-    const double ljj = std::sqrt(djj);
-    L[static_cast<size_t>(j) * d + j] = ljj;
-    for (int i = j + 1; i < d; ++i) {
-      double s = C[static_cast<size_t>(order[i]) * d + order[j]];
-      const double* Li = &L[static_cast<size_t>(i) * d];
-      const double* Lj = &L[static_cast<size_t>(j) * d];
-      for (int k = 0; k < j; ++k) s -= Li[k] * Lj[k];
-      L[static_cast<size_t>(i) * d + j] = s / ljj;
-    }
-  }
-  // Regressions of positions p <= deficient_from use the full-rank leading block:
-  // beta solves L_p^T beta = l_p (l_p = L[p, 0:p]), then rescale to original units.
-  for (int i = 0; i < d * d; ++i) B_out[i] = 0.0;
-  *used_pinv = 0;
-  std::vector<double> beta(d);
   const int full = std::min(d, deficient_from + 1);
-  for (int p = 1; p < full; ++p) {
-    const double* lp = &L[static_cast<size_t>(p) * d];
-    for (int i = p - 1; i >= 0; --i) {
-      double s = lp[i];
-      for (int k = i + 1; k < p; ++k) s -= L[static_cast<size_t>(k) * d + i] * beta[k];
-      beta[i] = s / L[static_cast<size_t>(i) * d + i];
-    }
-    const int t = order[p];
-    for (int q = 0; q < p; ++q) B_out[t + static_cast<int64_t>(d) * order[q]] = beta[q] * msd[2 * t + 1] / msd[2 * order[q] + 1];
+  plg::launch_regress_rows(S, d, c->idx.p, c->msd.p, full, c->part.p + dd, c->scores.p, d, c->stream);
+  PLG_CUDA(cudaMemcpyAsync(B_out, c->scores.p, dd * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  std::vector<double> C, msd(2 * static_cast<size_t>(d));
+  PLG_CUDA(cudaMemcpyAsync(msd.data(), c->msd.p, msd.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  if (full < d) {
+    C.resize(dd);
+    PLG_CUDA(cudaMemcpyAsync(C.data(), c->C.p, dd * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   }
-  // Rank-deficient predecessor designs: minimum-norm solution on the unscaled covariance.
+  PLG_CUDA(cudaStreamSynchronize(c->stream));
+  PLG_CUDA(cudaGetLastError());
+  *used_pinv = 0;
+  // Rank-deficient predecessor designs (rare): minimum-norm solution on the unscaled
+  // covariance, on the host.
   for (int p = full; p < d; ++p) {
     *used_pinv = 1;
     std::vector<double> A(static_cast<size_t>(p) * p), b(p), x(p);

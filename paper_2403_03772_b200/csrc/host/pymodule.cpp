@@ -87,38 +87,59 @@ PYBIND11_MODULE(_core, m) {
       .def("__repr__", [](const WeightedDag& d) { return "<WeightedDag dims=" + std::to_string(d.d) + ">"; });
 
   // ---- ordering (pymodule.cpp:103-118) ----
+  // The numpy buffer goes straight to the C-ABI (zero-copy when Fortran-ordered float64;
+  // forcecast converts anything else once), with the GIL released for the device call.
   m.def(
       "causal_order",
       [](const FArray& X, bool parallel, int workers) {
-        DataMatrix data = to_data(X);
-        py::gil_scoped_release rel;
-        return causal_order(data, parallel, workers).order;
+        (void)parallel;
+        if (X.ndim() != 2) throw Error(ErrorCode::DimensionMismatch, "X must be a 2-D array (samples x variables)");
+        if (workers < 1) {  // ordering.cpp:214-217: validate first, then the worker count
+          validate(to_data(X));
+          throw Error(ErrorCode::OutOfRange, "causal_order: workers must be >= 1");
+        }
+        const auto n = static_cast<std::int64_t>(X.shape(0));
+        const auto d = static_cast<int32_t>(X.shape(1));
+        std::vector<int> order(static_cast<std::size_t>(std::max(d, 1)));
+        plg_status st{};
+        int rc;
+        {
+          py::gil_scoped_release rel;
+          rc = plg_causal_order(gpu::context(), X.data(), n, d, std::max<std::int64_t>(n, 1), order.data(), &st);
+        }
+        gpu::check(rc, &st);
+        order.resize(static_cast<std::size_t>(std::max(d, 0)));
+        return order;
       },
       py::arg("X"), py::arg("parallel") = false, py::arg("workers") = 1,
       "Recursive causal ordering on the GPU engine (ordering.cpp:213-244).");
+  // pymodule.cpp:110-118: workers > 1 selects the parallel path, whose workers < 1 check
+  // (ordering.cpp:172-174) is therefore only reachable through search_causal_order_parallel.
+  auto search = [](const FArray& X, const std::vector<int>& U, int workers, bool check_workers) {
+    if (X.ndim() != 2) throw Error(ErrorCode::DimensionMismatch, "X must be a 2-D array (samples x variables)");
+    if (check_workers && workers < 1)
+      throw Error(ErrorCode::OutOfRange, "search_causal_order_parallel: workers must be >= 1");
+    const auto n = static_cast<std::int64_t>(X.shape(0));
+    const auto d = static_cast<int32_t>(X.shape(1));
+    std::vector<double> scores(static_cast<std::size_t>(d));
+    int chosen = -1;
+    plg_status st{};
+    int rc;
+    {
+      py::gil_scoped_release rel;
+      rc = plg_search(gpu::context(), X.data(), n, d, std::max<std::int64_t>(n, 1), U.data(),
+                      static_cast<int32_t>(U.size()), &chosen, scores.data(), &st);
+    }
+    gpu::check(rc, &st);
+    return py::make_tuple(chosen, scores);
+  };
   m.def(
       "search_causal_order",
-      [](const FArray& X, const std::vector<int>& U, int workers) {
-        DataMatrix data = to_data(X);
-        SearchResult res;
-        {
-          py::gil_scoped_release rel;
-          res = workers > 1 ? search_causal_order_parallel(data, U, workers) : search_causal_order(data, U);
-        }
-        return py::make_tuple(res.chosen, res.scores.scores);
-      },
+      [search](const FArray& X, const std::vector<int>& U, int workers) { return search(X, U, workers, false); },
       py::arg("X"), py::arg("U"), py::arg("workers") = 1);
   m.def(
       "search_causal_order_parallel",
-      [](const FArray& X, const std::vector<int>& U, int workers) {
-        DataMatrix data = to_data(X);
-        SearchResult res;
-        {
-          py::gil_scoped_release rel;
-          res = search_causal_order_parallel(data, U, workers);
-        }
-        return py::make_tuple(res.chosen, res.scores.scores);
-      },
+      [search](const FArray& X, const std::vector<int>& U, int workers) { return search(X, U, workers, true); },
       py::arg("X"), py::arg("U"), py::arg("workers"));
   m.def(
       "regress_out",
@@ -137,14 +158,33 @@ PYBIND11_MODULE(_core, m) {
   m.def(
       "fit_direct_lingam",
       [](const FArray& X, bool parallel, int workers, double edge_threshold) {
-        DataMatrix data = to_data(X);
+        // DirectLingam::fit (direct_lingam.cpp:33-76) on the numpy buffer, zero-copy
         DirectLingamConfig cfg;
         cfg.parallel = parallel;
         cfg.workers = workers;
         cfg.edge_threshold = edge_threshold;
-        DirectLingam model(cfg);
-        py::gil_scoped_release rel;
-        return model.fit(data);
+        DirectLingam model(cfg);  // config validation (direct_lingam.cpp:19-26)
+        if (X.ndim() != 2) throw Error(ErrorCode::DimensionMismatch, "X must be a 2-D array (samples x variables)");
+        const auto n = static_cast<std::int64_t>(X.shape(0));
+        const auto d = static_cast<int32_t>(X.shape(1));
+        WeightedDag dag;
+        dag.d = d;
+        dag.weights.assign(static_cast<std::size_t>(d) * d, 0.0);
+        dag.intercepts.assign(static_cast<std::size_t>(d), 0.0);
+        dag.order.order.assign(static_cast<std::size_t>(std::max(d, 1)), -1);
+        int32_t pinv = 0;
+        plg_status st{};
+        int rc;
+        {
+          py::gil_scoped_release rel;
+          rc = plg_causal_order(gpu::context(), X.data(), n, d, std::max<std::int64_t>(n, 1), dag.order.order.data(), &st);
+          if (rc == 0 && d > 1)
+            rc = plg_fit_weights(gpu::context(), X.data(), n, d, n, dag.order.order.data(), dag.weights.data(), &pinv, &st);
+        }
+        gpu::check(rc, &st);
+        dag.order.order.resize(static_cast<std::size_t>(std::max(d, 0)));
+        dag.used_pinv = pinv != 0;
+        return dag;
       },
       py::arg("X"), py::arg("parallel") = false, py::arg("workers") = 1, py::arg("edge_threshold") = 0.05);
   m.def(

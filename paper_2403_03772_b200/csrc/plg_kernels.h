@@ -131,6 +131,14 @@ void launch_residualize(double* W, int64_t ldw, int64_t n, const double* C, int6
 void launch_regress_out(const double* X, int64_t ldx, int64_t n, int exog, const int* remaining,
                         int r, double* out, int64_t ldo, int* zero_var_flag, cudaStream_t s);
 
+// Weight step (chol_kernels.cu): S = C[order][order]; in-place blocked Cholesky of the
+// correlation S (fail = first position whose pivot is <= tol, else untouched); beta rows of
+// every target p < limit written as B[order[p] + ldb * order[q]] in original units.
+void launch_permute(const double* C, int64_t ldc, const int* order, int n, double* S, cudaStream_t s);
+void launch_cholesky(double* S, int n, double tol, int* fail, cudaStream_t s);
+void launch_regress_rows(const double* L, int n, const int* order, const double* msd, int limit, double* beta,
+                         double* B, int64_t ldb, cudaStream_t s);
+
 // entropy_approx(u * scale) of one vector (kernels.cpp:123-148).
 void launch_entropy_vec(const double* u, int64_t n, double scale, double* out, const double* g_exp,
                         const double2* g_log, cudaStream_t s);

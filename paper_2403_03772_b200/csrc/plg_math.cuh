@@ -104,12 +104,12 @@ __device__ __forceinline__ TabPtr table_ptrs(const unsigned char* s_tab, int lan
   return {s_tab + (lane & (kExpRep - 1)) * 8, s_tab + kExpTableBytes + (lane & (kLogRep - 1)) * 16};
 }
 
-// v * 2^(k >> 7): add (k & ~127) << 13 to the high word (one IMAD), optionally clamped.
+// v * 2^(k >> 7): add (k >> 7) << 20 to the high word (shift + lea), optionally clamped.
 template <bool kClamp>
 __device__ __forceinline__ double scale_pow2(double v, int k) {
-  int kh = k & ~(kExpN - 1);
-  if (kClamp) kh = max(kh, kMinScaledK);
-  return __hiloint2double(__double2hiint(v) + kh * (1 << (20 - kExpBits)), __double2loint(v));
+  int e = k >> kExpBits;
+  if (kClamp) e = max(e, kMinScaledK >> kExpBits);
+  return __hiloint2double(__double2hiint(v) + (e << 20), __double2loint(v));
 }
 
 __device__ __forceinline__ double exp_row(const TabPtr& tp, int k) {
