@@ -96,12 +96,19 @@ struct CausalOrder {
   std::vector<int> positions() const;
 };
 
+struct FitPhases {
+  double ordering_seconds = 0.0;
+  double weights_seconds = 0.0;
+  double total_seconds = 0.0;
+};
+
 struct WeightedDag {
   std::vector<double> weights;  // d x d column-major: weights[i + d*j] = effect of j on i
   int d = 0;
   CausalOrder order;
   std::vector<double> intercepts;
   bool used_pinv = false;
+  FitPhases phases;  // filled by the fitting calls (the reference returns it separately)
   int dims() const { return d; }
   double operator()(int i, int j) const { return weights[static_cast<std::size_t>(i) + static_cast<std::size_t>(d) * j]; }
 };
@@ -130,12 +137,6 @@ struct DirectLingamConfig {
   bool parallel = false;
   int workers = 1;
   double edge_threshold = 0.05;
-};
-
-struct FitPhases {
-  double ordering_seconds = 0.0;
-  double weights_seconds = 0.0;
-  double total_seconds = 0.0;
 };
 
 class DirectLingam {

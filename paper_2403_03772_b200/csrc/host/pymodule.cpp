@@ -7,6 +7,8 @@
 #include <pybind11/pybind11.h>
 #include <pybind11/stl.h>
 
+#include <chrono>
+#include <cstdio>
 #include <limits>
 
 #include "../../../include/plingam_b200.h"
@@ -84,6 +86,14 @@ PYBIND11_MODULE(_core, m) {
       .def_property_readonly("weights", [](const WeightedDag& d) { return colmajor_array(d.weights, d.d, d.d); })
       .def_property_readonly("order", [](const WeightedDag& d) { return d.order.order; })
       .def_readonly("used_pinv", &WeightedDag::used_pinv)
+      .def_property_readonly("phases",
+                             [](const WeightedDag& d) {
+                               py::dict p;
+                               p["ordering_seconds"] = d.phases.ordering_seconds;
+                               p["weights_seconds"] = d.phases.weights_seconds;
+                               p["total_seconds"] = d.phases.total_seconds;
+                               return p;
+                             })
       .def("__repr__", [](const WeightedDag& d) { return "<WeightedDag dims=" + std::to_string(d.d) + ">"; });
 
   // ---- ordering (pymodule.cpp:103-118) ----
@@ -175,15 +185,24 @@ PYBIND11_MODULE(_core, m) {
         int32_t pinv = 0;
         plg_status st{};
         int rc;
+        FitPhases phases;  // direct_lingam.hpp:16-20 (wall clock, as the reference)
         {
           py::gil_scoped_release rel;
+          using Clock = std::chrono::steady_clock;
+          const auto t0 = Clock::now();
           rc = plg_causal_order(gpu::context(), X.data(), n, d, std::max<std::int64_t>(n, 1), dag.order.order.data(), &st);
+          const auto t1 = Clock::now();
           if (rc == 0 && d > 1)
             rc = plg_fit_weights(gpu::context(), X.data(), n, d, n, dag.order.order.data(), dag.weights.data(), &pinv, &st);
+          const auto t2 = Clock::now();
+          phases.ordering_seconds = std::chrono::duration<double>(t1 - t0).count();
+          phases.weights_seconds = std::chrono::duration<double>(t2 - t1).count();
+          phases.total_seconds = std::chrono::duration<double>(t2 - t0).count();
         }
         gpu::check(rc, &st);
         dag.order.order.resize(static_cast<std::size_t>(std::max(d, 0)));
         dag.used_pinv = pinv != 0;
+        dag.phases = phases;
         return dag;
       },
       py::arg("X"), py::arg("parallel") = false, py::arg("workers") = 1, py::arg("edge_threshold") = 0.05);
@@ -365,6 +384,25 @@ PYBIND11_MODULE(_core, m) {
       py::arg("b0"), py::arg("lagged"), py::arg("T"), py::arg("burn_in") = 100, py::arg("seed") = 0,
       py::arg("noise") = std::pair<double, double>{0.0, 1.0}, py::arg("kind") = "uniform");
   m.def("uniform_vector", &sim::uniform_vector, py::arg("d"), py::arg("seed"), py::arg("lo"), py::arg("hi"));
+  m.def(
+      "digest_file",
+      [](const std::string& path) {  // csv.cpp:151-167: FNV-1a 64 over the file bytes, hex
+        std::FILE* f = std::fopen(path.c_str(), "rb");
+        if (!f) throw Error(ErrorCode::IoError, "cannot open " + path);
+        std::uint64_t h = 0xcbf29ce484222325ULL;
+        std::vector<unsigned char> buf(1 << 20);
+        std::size_t got;
+        {
+          py::gil_scoped_release rel;
+          while ((got = std::fread(buf.data(), 1, buf.size(), f)) > 0)
+            for (std::size_t i = 0; i < got; ++i) h = (h ^ buf[i]) * 0x100000001b3ULL;
+        }
+        std::fclose(f);
+        char out[17];
+        std::snprintf(out, sizeof(out), "%016llx", static_cast<unsigned long long>(h));
+        return std::string(out);
+      },
+      py::arg("path"));
 
   // ---- low-level engine handle (bench, sampled-round parity, math probe) ----
   py::class_<Engine>(m, "Engine")
