@@ -34,7 +34,7 @@ CONFIGS = {
     "c4": (500, 2499, "VarLiNGAM lag 1: residuals of a d=500, T=2500 SVAR (sparse B0, diagonal B1, Laplace noise)"),
     "c5": (2000, 10000, "sparse ER DAG (avg 2 parents, |w| in [0.5,1.5]), Laplace(0,1) noise, seed 1"),
 }
-FP64_OPS_PER_EDE = 32     # FP64-pipe instructions per EDE in the pair kernel inner loop (cuobjdump SASS)
+FP64_OPS_PER_EDE = 31     # FP64-pipe instructions per EDE in the pair kernel inner loop (cuobjdump SASS)
 LIBDEVICE_OPS_PER_EDE = 70  # SURVEY.md §8d algorithmic basis (libdevice exp/log1p)
 FP64_PEAK_TFLOPS = 33.85  # measured DFMA microbenchmark on this pool's B200 (tools/probe/fp64_peak.cu)
 

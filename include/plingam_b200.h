@@ -130,6 +130,9 @@ typedef struct plg_round_plan {
   int32_t tile_count;
   int32_t nseg;
   int32_t seg_len;
+  int32_t replicated;     /* u <= 128: every rank evaluates every pair (tile_begin 0, tile_count
+                             ntiles) and the round has no exchange; the segmentation is then
+                             that of the compact small-round kernel */
 } plg_round_plan;
 int plg_plan_round(int32_t u, int64_t n, int32_t rank, int32_t world, plg_round_plan* out);
 /* tile index -> (bi, bj), bi <= bj, row-major over the upper triangle */

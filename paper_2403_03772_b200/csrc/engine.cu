@@ -176,7 +176,14 @@ namespace {
 int make_tables(plg_ctx* ctx, plg_status* st) {
   std::vector<double> e(plg::kExpN);
   std::vector<double2> l(plg::kLogMasterN);
-  for (int j = 0; j < plg::kExpN; ++j) e[j] = static_cast<double>(exp2l(static_cast<long double>(j) / plg::kExpN));
+  for (int j = 0; j < plg::kExpN; ++j) {
+    // 2^(j/128) with j << 13 taken off the high word (plg_math.cuh exp2_k)
+    uint64_t bits;
+    const double v = static_cast<double>(exp2l(static_cast<long double>(j) / plg::kExpN));
+    std::memcpy(&bits, &v, 8);
+    bits -= static_cast<uint64_t>(j) << (32 + 20 - plg::kExpBits);
+    std::memcpy(&e[j], &bits, 8);
+  }
   const long double ln2 = logl(2.0L);
   for (int j = 0; j < plg::kLogMasterN; ++j) {
     const double c = (j == plg::kLogMasterN - 1)
@@ -214,8 +221,21 @@ int report_error(unsigned long long key, const int* /*unused*/, plg_status* st) 
                     "entropy_of_normalized: zero residual (exactly collinear pair)");
 }
 
+// Segmentation of a small round (pair_small_kernel): ~kTargetCtas CTAs of 256 pairs, at
+// least kSmallSegMin samples each; segment starts 16-sample aligned. Pure function of (u, n).
+constexpr int64_t kSmallSegMin = 128;
+SegPlan small_seg_plan(int u, int64_t n) {
+  const int64_t npairs = static_cast<int64_t>(u) * (u - 1) / 2;
+  const int64_t chunks = (npairs + plg::kSmallThreads - 1) / plg::kSmallThreads;
+  int64_t nseg = std::max<int64_t>(1, kTargetCtas / chunks);
+  nseg = std::min(nseg, std::max<int64_t>(1, n / kSmallSegMin));
+  const int64_t seg_len = round_up((n + nseg - 1) / nseg, 16);
+  return {static_cast<int>((n + seg_len - 1) / seg_len), static_cast<int>(seg_len)};
+}
+
 struct RoundPlan {
   int nb, ntiles, tpr, tb, ntl;
+  bool replicated;  // small round: every rank evaluates every pair, no exchange
   SegPlan seg;
 };
 
@@ -223,11 +243,23 @@ RoundPlan plan_round(int u, int64_t n, int rank, int world) {
   RoundPlan p;
   p.nb = (u + kBT - 1) / kBT;
   p.ntiles = p.nb * (p.nb + 1) / 2;
+  p.replicated = u <= plg::kSmallU;
+  if (p.replicated) {
+    p.tpr = p.ntl = p.ntiles;
+    p.tb = 0;
+    p.seg = small_seg_plan(u, n);
+    return p;
+  }
   p.tpr = (p.ntiles + world - 1) / world;
   p.tb = std::min(p.ntiles, rank * p.tpr);
   p.ntl = std::min(p.ntiles, p.tb + p.tpr) - p.tb;
   p.seg = seg_plan(u, n);
   return p;
+}
+
+size_t part_doubles(const RoundPlan& rp, int u) {
+  if (rp.replicated) return static_cast<size_t>(u) * (u - 1) / 2 * rp.seg.nseg * 4;
+  return static_cast<size_t>(rp.ntl) * rp.seg.nseg * kTilePairs * 4;
 }
 
 // One search round over the active list act_cur (u >= 2): H, pairs, exchange, k.
@@ -257,13 +289,18 @@ int search_round(plg_ctx* c, int64_t n, int64_t ldw, int ldc, int u, const int* 
   a.err = c->err.p;
   a.round = round;
   if (c->timing) cudaEventRecord(c->ev[ev_base], c->stream);
-  if (rp.ntl > 0) {
+  if (rp.replicated) {
+    plg::launch_pair_small(a, c->stream);
+    plg::launch_finalize_small(a, c->stream);
+    c->launches += 2;
+  } else if (rp.ntl > 0) {
     plg::launch_pair(a, c->stream);
     plg::launch_finalize(a, c->stream);
     c->launches += 2;
   }
   if (c->timing) cudaEventRecord(c->ev[ev_base + 1], c->stream);
-  if (c->world > 1) {
+  const bool exchange = c->world > 1 && !rp.replicated;
+  if (exchange) {
     // One grouped exchange per round: the entropy tiles (in place, rank slots of tpr tiles)
     // and every rank's error key.
     const size_t cnt = static_cast<size_t>(rp.tpr) * 2 * kTilePairs;
@@ -277,8 +314,8 @@ int search_round(plg_ctx* c, int64_t n, int64_t ldw, int ldc, int u, const int* 
       return set_status(st, PLG_NcclError, -1, -1, "ncclAllGather: %s",
                         api.GetErrorString(r != ncclSuccess ? r : (r2 != ncclSuccess ? r2 : r3)));
   }
-  plg::launch_kreduce(c->epack.p, c->H.p, u, rp.nb, c->k.p, c->err.p, c->world > 1 ? c->errs.p : c->err.p,
-                      c->world, c->stream);
+  plg::launch_kreduce(c->epack.p, c->H.p, u, rp.nb, c->k.p, c->err.p, exchange ? c->errs.p : c->err.p,
+                      exchange ? c->world : 1, c->stream);
   ++c->launches;
   return 0;
 }
@@ -288,8 +325,8 @@ int reserve_run(plg_ctx* c, int64_t n, int ncols, int64_t ldw, plg_status* st) {
   size_t part_max = 0, epack_max = 0;
   for (int u = ncols; u >= 2; --u) {
     const RoundPlan rp = plan_round(u, n, c->rank, c->world);
-    part_max = std::max(part_max, static_cast<size_t>(rp.ntl) * rp.seg.nseg * kTilePairs * 4);
-    epack_max = std::max(epack_max, static_cast<size_t>(rp.tpr) * c->world * 2 * kTilePairs);
+    part_max = std::max(part_max, part_doubles(rp, u));
+    epack_max = std::max(epack_max, static_cast<size_t>(rp.tpr) * (rp.replicated ? 1 : c->world) * 2 * kTilePairs);
   }
   PLG_CUDA(c->W.reserve(static_cast<size_t>(ncols) * ldw));
   PLG_CUDA(c->C.reserve(static_cast<size_t>(ncols) * ncols));
@@ -771,6 +808,7 @@ int plg_plan_round(int32_t u, int64_t n, int32_t rank, int32_t world, plg_round_
   out->tile_count = rp.ntl;
   out->nseg = rp.seg.nseg;
   out->seg_len = rp.seg.seg_len;
+  out->replicated = rp.replicated ? 1 : 0;
   return 0;
 }
 

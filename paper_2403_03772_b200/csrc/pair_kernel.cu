@@ -67,6 +67,31 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// Per-pair scales of both directions from the maintained Gram: u'_1 = x s1 - y bs1 is the
+// scaled residual of i on j, u'_2 = y s2 - x bs2 that of j on i (u' = K u, plg_math.cuh).
+// Zeros (and the error key) for an exactly collinear pair.
+__device__ __forceinline__ void pair_params(const PairLaunch& a, int ci, int cj, double& s1, double& bs1,
+                                            double& s2, double& bs2) {
+  const double cii = a.C[static_cast<int64_t>(ci) * a.ldc + ci];
+  const double cjj = a.C[static_cast<int64_t>(cj) * a.ldc + cj];
+  const double cij = a.C[static_cast<int64_t>(ci) * a.ldc + cj];
+  const double b1 = cij / cjj;  // slope of i on j (ordering.cpp:89, cov / col_var[q])
+  const double v1 = cii - cij * b1;
+  const double b2 = cij / cii;  // slope of j on i (ordering.cpp:90)
+  const double v2 = cjj - cij * b2;
+  if (!(v1 > 0.0) || !(v2 > 0.0)) {
+    // exactly collinear pair (e.g. bit-identical standardised columns): the residual is
+    // identically zero and entropy_of_normalized throws (kernels.cpp:136-139)
+    atomicMin(a.err, err_key(a.round, kErrPairCollinear, -1));
+    s1 = bs1 = s2 = bs2 = 0.0;
+    return;
+  }
+  s1 = kUScale / sqrt(v1);
+  bs1 = b1 * s1;
+  s2 = kUScale / sqrt(v2);
+  bs2 = b2 * s2;
+}
+
 constexpr int kStages = 3;
 constexpr int kStageDoubles = 2 * kBT * kCHS;
 constexpr size_t kPairSmem = static_cast<size_t>(kTableBytes) + kStages * kStageDoubles * sizeof(double) +
@@ -174,25 +199,7 @@ __global__ void __launch_bounds__(PairCfg<NI, NJ, kDedicated>::kThreads, 1) pair
     const int cj = s_col[diag ? pj : kBT + pj];
     const bool valid = (ci >= 0) && (cj >= 0) && (!diag || pi < pj);
     s1[q] = bs1[q] = s2[q] = bs2[q] = 0.0;
-    if (valid) {
-      const double cii = a.C[static_cast<int64_t>(ci) * a.ldc + ci];
-      const double cjj = a.C[static_cast<int64_t>(cj) * a.ldc + cj];
-      const double cij = a.C[static_cast<int64_t>(ci) * a.ldc + cj];
-      const double b1 = cij / cjj;  // slope of i on j (ordering.cpp:89, cov / col_var[q])
-      const double v1 = cii - cij * b1;
-      const double b2 = cij / cii;  // slope of j on i (ordering.cpp:90)
-      const double v2 = cjj - cij * b2;
-      if (!(v1 > 0.0) || !(v2 > 0.0)) {
-        // exactly collinear pair (e.g. bit-identical standardised columns): the residual
-        // is identically zero and entropy_of_normalized throws (kernels.cpp:136-139)
-        atomicMin(a.err, err_key(a.round, kErrPairCollinear, -1));
-      } else {
-        s1[q] = kUScale / sqrt(v1);  // u' = K u (plg_math.cuh)
-        bs1[q] = b1 * s1[q];
-        s2[q] = kUScale / sqrt(v2);
-        bs2[q] = b2 * s2[q];
-      }
-    }
+    if (valid) pair_params(a, ci, cj, s1[q], bs1[q], s2[q], bs2[q]);
   }
   EdeAcc acc[2 * NQ];  // [q] direction i|j, [NQ + q] direction j|i
   const TabPtr tp = table_ptrs(smem, lane);
@@ -275,6 +282,86 @@ __global__ void finalize_kernel(const PairLaunch a) {
   double* tile = a.epack + static_cast<int64_t>(a.tile_begin + tl) * 2 * kTilePairs;
   tile[x * kBT + y] = e1;
   tile[kTilePairs + y * kBT + x] = e2;
+}
+
+// (p, q), p < q < u, of the p-major pair index.
+__device__ __forceinline__ void pair_decode(int pair, int u, int& p, int& q) {
+  int rem = pair;
+  p = 0;
+  while (rem >= u - 1 - p) {
+    rem -= u - 1 - p;
+    ++p;
+  }
+  q = p + 1 + rem;
+}
+
+template <bool kClampA>
+__global__ void __launch_bounds__(kSmallThreads) pair_small_kernel(const PairLaunch a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ int s_abort;
+  if (threadIdx.x == 0) s_abort = (*a.err != kNoError);
+  load_tables(smem, a.g_exp, a.g_log);
+  __syncthreads();
+  if (s_abort) return;
+  const int npairs = a.u * (a.u - 1) / 2;
+  const int pair = blockIdx.x * kSmallThreads + threadIdx.x;
+  if (pair >= npairs) return;
+  const int seg = blockIdx.y;
+  int p, q;
+  pair_decode(pair, a.u, p, q);
+  double s1, bs1, s2, bs2;
+  pair_params(a, a.act[p], a.act[q], s1, bs1, s2, bs2);
+  const double* wi = a.W + static_cast<int64_t>(a.act[p]) * a.ldw;
+  const double* wj = a.W + static_cast<int64_t>(a.act[q]) * a.ldw;
+  const TabPtr tp = table_ptrs(smem, threadIdx.x & 31);
+  EdeAcc acc1, acc2;
+  const int64_t t0 = static_cast<int64_t>(seg) * a.seg_len;  // multiple of 16: 16-byte aligned
+  const int64_t t1 = lmin(a.n, t0 + a.seg_len);
+  int64_t t = t0;
+#pragma unroll 1
+  for (; t + 1 < t1; t += 2) {
+    const double2 x = __ldg(reinterpret_cast<const double2*>(wi + t));
+    const double2 y = __ldg(reinterpret_cast<const double2*>(wj + t));
+    const double u1a = fma(y.x, -bs1, x.x * s1), u2a = fma(x.x, -bs2, y.x * s2);
+    const double u1b = fma(y.y, -bs1, x.y * s1), u2b = fma(x.y, -bs2, y.y * s2);
+    ede_accumulate<kClampA>(u1a, acc1, tp);
+    ede_accumulate<kClampA>(u2a, acc2, tp);
+    ede_accumulate<kClampA>(u1b, acc1, tp);
+    ede_accumulate<kClampA>(u2b, acc2, tp);
+  }
+  if (t < t1) {
+    const double x = wi[t], y = wj[t];
+    ede_accumulate<kClampA>(fma(y, -bs1, x * s1), acc1, tp);
+    ede_accumulate<kClampA>(fma(x, -bs2, y * s2), acc2, tp);
+  }
+  double2* dst = reinterpret_cast<double2*>(a.part + (static_cast<int64_t>(seg) * npairs + pair) * 4);
+  dst[0] = make_double2(acc_lc(acc1), acc_pdf(acc1));
+  dst[1] = make_double2(acc_lc(acc2), acc_pdf(acc2));
+}
+
+__global__ void finalize_small_kernel(const PairLaunch a) {
+  if (*a.err != kNoError) return;
+  const int npairs = a.u * (a.u - 1) / 2;
+  const int pair = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pair >= npairs) return;
+  int p, q;
+  pair_decode(pair, a.u, p, q);
+  double l1 = 0.0, p1 = 0.0, l2 = 0.0, p2 = 0.0;
+  const double* src = a.part + static_cast<int64_t>(pair) * 4;
+  for (int s = 0; s < a.nseg; ++s) {
+    const double2 v1 = reinterpret_cast<const double2*>(src)[0];
+    const double2 v2 = reinterpret_cast<const double2*>(src)[1];
+    l1 += v1.x;
+    p1 += v1.y;
+    l2 += v2.x;
+    p2 += v2.y;
+    src += static_cast<int64_t>(npairs) * 4;
+  }
+  const double inv_n = 1.0 / static_cast<double>(a.n);
+  const int bi = p / kBT, x = p % kBT, bj = q / kBT, y = q % kBT;
+  double* tile = a.epack + static_cast<int64_t>(bi * a.nb - (bi * (bi - 1)) / 2 + (bj - bi)) * 2 * kTilePairs;
+  tile[x * kBT + y] = entropy_from_sums(l1, p1, inv_n);
+  tile[kTilePairs + y * kBT + x] = entropy_from_sums(l2, p2, inv_n);
 }
 
 constexpr int kColentThreads = 256;
@@ -415,6 +502,30 @@ void launch_pair(const PairLaunch& a, cudaStream_t s) {
 
 void launch_finalize(const PairLaunch& a, cudaStream_t s) {
   finalize_kernel<<<dim3(a.ntiles, kTilePairs / 256), 256, 0, s>>>(a);
+}
+
+namespace {
+template <bool kClampA>
+void launch_pair_small_cfg(const PairLaunch& a, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(pair_small_kernel<kClampA>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTableBytes);
+    attr = true;
+  }
+  const int npairs = a.u * (a.u - 1) / 2;
+  pair_small_kernel<kClampA>
+      <<<dim3((npairs + kSmallThreads - 1) / kSmallThreads, a.nseg), kSmallThreads, kTableBytes, s>>>(a);
+}
+}  // namespace
+
+void launch_pair_small(const PairLaunch& a, cudaStream_t s) {
+  if (a.n > 90000) launch_pair_small_cfg<true>(a, s);
+  else launch_pair_small_cfg<false>(a, s);
+}
+
+void launch_finalize_small(const PairLaunch& a, cudaStream_t s) {
+  const int npairs = a.u * (a.u - 1) / 2;
+  finalize_small_kernel<<<(npairs + 255) / 256, 256, 0, s>>>(a);
 }
 
 void launch_colent(const double* W, int64_t ldw, int64_t n, const double* C, int64_t ldc,

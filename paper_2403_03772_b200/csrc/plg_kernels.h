@@ -62,6 +62,14 @@ struct PairLaunch {
 void launch_pair(const PairLaunch& a, cudaStream_t s);
 void launch_finalize(const PairLaunch& a, cudaStream_t s);
 
+// Small active sets (u <= kSmallU): one thread per unordered pair (p < q, p-major) and
+// sample segment, columns read through L1 (the u columns sit in L2). Computed on every rank
+// (no exchange); part = [nseg][npairs][4]; the finalize writes the same epack layout.
+constexpr int kSmallU = 128;
+constexpr int kSmallThreads = 256;
+void launch_pair_small(const PairLaunch& a, cudaStream_t s);
+void launch_finalize_small(const PairLaunch& a, cudaStream_t s);
+
 // H[p] = entropy(w_col / sqrt(C_col,col)) for active positions p < u. For round > 0 it
 // is also build_cache's ZeroVariance(col) check (ordering.cpp:56-62): a column whose
 // residualisation left it identically zero (nz[col] != round) or whose partial variance

@@ -27,7 +27,7 @@ BT = 32
 
 class RoundPlan(ctypes.Structure):
     _fields_ = [(f, ctypes.c_int32) for f in
-                ("nb", "ntiles", "tiles_per_rank", "tile_begin", "tile_count", "nseg", "seg_len")]
+                ("nb", "ntiles", "tiles_per_rank", "tile_begin", "tile_count", "nseg", "seg_len", "replicated")]
 
 
 def tile_index(bi, bj, nb):
@@ -90,10 +90,14 @@ def _worker(rank, world, port, X, result_q):
                     e_ij, e_ji = pair_entropies(oracle, Z, i, j)
                     slot[tl, 0, x, y] = e_ij
                     slot[tl, 1, y, x] = e_ji
-        send = torch.from_numpy(slot.reshape(-1).copy())
-        recv = [torch.zeros_like(send) for _ in range(world)]
-        dist.all_gather(recv, send)  # the engine's in-place ncclAllGather of rank slots
-        epack = torch.cat(recv).numpy().reshape(-1, 2, BT, BT)
+        if plan.replicated:  # small round: every rank holds every tile, no exchange
+            assert plan.tile_count == plan.ntiles
+            epack = slot
+        else:
+            send = torch.from_numpy(slot.reshape(-1).copy())
+            recv = [torch.zeros_like(send) for _ in range(world)]
+            dist.all_gather(recv, send)  # the engine's in-place ncclAllGather of rank slots
+            epack = torch.cat(recv).numpy().reshape(-1, 2, BT, BT)
         k = kreduce(epack, H, u, plan.nb)
         chosen = int(np.argmin(k))  # np.argmin returns the lowest index on ties
         result_q.put((rank, chosen, k.tobytes()))
@@ -107,10 +111,12 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_sharded_round_matches_single_process(world, oracle):
+@pytest.mark.parametrize("world,d", [(2, 150), (3, 150), (2, 70)])
+def test_sharded_round_matches_single_process(world, d, oracle):
+    # d = 150: 5 position blocks -> 15 tiles, uneven over 2 ranks; d = 70 is a replicated
+    # small round (u <= 128)
     rng = np.random.default_rng(11)
-    d, n = 70, 300  # 3 position blocks -> 6 tiles, uneven over 3 ranks
+    n = 300
     X = np.asfortranarray(rng.uniform(-1, 1, size=(n, d)) + 0.5 * rng.laplace(size=(n, d)))
     chosen_ref, scores_ref = oracle.search_causal_order(X, list(range(d)))
     ctx = mp.get_context("spawn")

@@ -16,7 +16,7 @@ LIB = os.path.join(ROOT, "paper_2403_03772_b200", "libplingam_b200.so")
 
 class RoundPlan(ctypes.Structure):
     _fields_ = [(f, ctypes.c_int32) for f in
-                ("nb", "ntiles", "tiles_per_rank", "tile_begin", "tile_count", "nseg", "seg_len")]
+                ("nb", "ntiles", "tiles_per_rank", "tile_begin", "tile_count", "nseg", "seg_len", "replicated")]
 
 
 @pytest.fixture(scope="module")
@@ -40,7 +40,7 @@ def test_library_exports_every_declared_symbol(cabi):
 
 
 def test_round_plan_partitions_tiles(cabi):
-    for u in (2, 3, 31, 32, 33, 100, 999, 2000):
+    for u in (2, 3, 31, 32, 33, 100, 128, 129, 999, 2000):
         for world in (1, 2, 3, 4, 8):
             covered = []
             segs = set()
@@ -48,15 +48,21 @@ def test_round_plan_partitions_tiles(cabi):
                 p = RoundPlan()
                 assert cabi.plg_plan_round(u, 10000, rank, world, ctypes.byref(p)) == 0
                 assert p.nb == (u + 31) // 32 and p.ntiles == p.nb * (p.nb + 1) // 2
-                covered += list(range(p.tile_begin, p.tile_begin + p.tile_count))
+                assert p.replicated == (u <= 128)
                 segs.add((p.nseg, p.seg_len))
+                if p.replicated:  # small rounds: every rank evaluates every pair, no exchange
+                    assert (p.tile_begin, p.tile_count, p.tiles_per_rank) == (0, p.ntiles, p.ntiles)
+                    continue
+                covered += list(range(p.tile_begin, p.tile_begin + p.tile_count))
                 assert p.tiles_per_rank * world >= p.ntiles
                 assert p.tile_begin == min(p.ntiles, rank * p.tiles_per_rank)
-            assert covered == list(range(p.ntiles)), (u, world)
+            if u > 128:
+                assert covered == list(range(p.ntiles)), (u, world)
             # segmentation (hence every entropy bit) does not depend on the rank count
             assert len(segs) == 1
             nseg, seg_len = segs.pop()
-            assert seg_len % 64 == 0 and (nseg - 1) * seg_len < 10000 <= nseg * seg_len
+            assert seg_len % (16 if u <= 128 else 64) == 0
+            assert (nseg - 1) * seg_len < 10000 <= nseg * seg_len
 
 
 def test_round_plan_segmentation_independent_of_world(cabi):

@@ -3,6 +3,7 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I../../paper_2403_03772_b200/csrc ede_probe.cu
 #include <cmath>
 #include <cstdio>
+#include <cstring>
 #include <vector>
 
 #include "plg_math.cuh"
@@ -62,7 +63,13 @@ void run(const double* de, const double2* dl, double* out, int blocks_per_sm, in
 int main() {
   std::vector<double> e(kExpN);
   std::vector<double2> l(kLogMasterN);
-  for (int j = 0; j < kExpN; ++j) e[j] = (double)exp2l((long double)j / kExpN);
+  for (int j = 0; j < kExpN; ++j) {  // pre-compensated rows (plg_math.cuh exp2_k)
+    double v = (double)exp2l((long double)j / kExpN);
+    unsigned long long b;
+    memcpy(&b, &v, 8);
+    b -= (unsigned long long)j << 45;
+    memcpy(&e[j], &b, 8);
+  }
   for (int j = 0; j < kLogMasterN; ++j) {
     const double c = (j == kLogMasterN - 1) ? 0.5 : (double)(1.0L / (1.0L + ((long double)j + 0.5L) / 128));
     l[j] = make_double2(c, (double)(-logl((long double)c) - logl(2.0L)));
