@@ -149,6 +149,13 @@ int plg_round_state(plg_ctx* ctx, const double* X, int64_t n, int32_t d, int64_t
                     int32_t rounds, int32_t* active_out, int32_t* n_active, double* cols_out,
                     int32_t* order_prefix_out, plg_status* st);
 
+/* Analysis hook (not part of the reference surface): when set, causal_order on a
+ * single-rank context synchronises after every round's k reduction and calls
+ * hook(user, round, u, active (u ints, position -> variable), E (u*u doubles,
+ * E[p*u+q] = E(p|q)), H (u), k (u)). Pass NULL to clear. */
+typedef void (*plg_round_hook)(void* user, int32_t round, int32_t u, const int32_t* active,
+                               const double* E, const double* H, const double* k);
+int plg_debug_set_round_hook(plg_ctx* ctx, plg_round_hook hook, void* user);
 /* Test hook: element functions on device for a host vector u (n values): out[4i..4i+3] =
  * {log cosh (table path), u e^{-u^2/2} (table path), libdevice log cosh, libdevice pdf}. */
 int plg_math_probe(plg_ctx* ctx, const double* u, int64_t n, double* out, plg_status* st);

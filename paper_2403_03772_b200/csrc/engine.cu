@@ -159,6 +159,8 @@ struct plg_ctx {
   std::vector<cudaEvent_t> ev;  // pool: [0]=start [1]=end [2]=h2d end, then 2 per round
   plg_stats last{};
   int64_t launches = 0;
+  plg_round_hook hook = nullptr;  // analysis hook (plg_debug_set_round_hook), null in production
+  void* hook_user = nullptr;
 
   cudaError_t events(size_t count) {
     while (ev.size() < count) {
@@ -406,6 +408,30 @@ void finish_stats(plg_ctx* c, int64_t n, int d, int rounds, bool host_in) {
   s.pair_ms = pair_ms;
 }
 
+// Analysis hook: copy the round's full entropy table to the host as a dense u x u matrix
+// (E[p*u+q] = E(p|q), positions in the active list) and hand it to the hook.
+int call_round_hook(plg_ctx* c, int u, int round, const int* act_cur, plg_status* st) {
+  const int nb = (u + kBT - 1) / kBT;
+  const size_t ntiles = static_cast<size_t>(nb) * (nb + 1) / 2;
+  std::vector<double> ep(ntiles * 2 * kTilePairs), H(u), k(u), E(static_cast<size_t>(u) * u, 0.0);
+  std::vector<int> act(u);
+  PLG_CUDA(cudaStreamSynchronize(c->stream));
+  PLG_CUDA(cudaMemcpy(ep.data(), c->epack.p, ep.size() * sizeof(double), cudaMemcpyDeviceToHost));
+  PLG_CUDA(cudaMemcpy(H.data(), c->H.p, u * sizeof(double), cudaMemcpyDeviceToHost));
+  PLG_CUDA(cudaMemcpy(k.data(), c->k.p, u * sizeof(double), cudaMemcpyDeviceToHost));
+  PLG_CUDA(cudaMemcpy(act.data(), act_cur, u * sizeof(int), cudaMemcpyDeviceToHost));
+  auto tidx = [nb](int bi, int bj) { return static_cast<size_t>(bi) * nb - (static_cast<size_t>(bi) * (bi - 1)) / 2 + (bj - bi); };
+  for (int p = 0; p < u; ++p)
+    for (int q = p + 1; q < u; ++q) {
+      const int bp = p / kBT, xp = p % kBT, bq = q / kBT, xq = q % kBT;
+      const double* tile = ep.data() + tidx(bp, bq) * 2 * kTilePairs;
+      E[static_cast<size_t>(p) * u + q] = tile[xp * kBT + xq];
+      E[static_cast<size_t>(q) * u + p] = tile[kTilePairs + xq * kBT + xp];
+    }
+  c->hook(c->hook_user, round, u, act.data(), E.data(), H.data(), k.data());
+  return 0;
+}
+
 // The recursive loop (ordering.cpp:213-244) on device-resident X.
 int causal_order_impl(plg_ctx* c, const double* dX, int64_t ldx, int64_t n, int d, int max_rounds,
                       int32_t* order_out, bool host_in, plg_status* st) {
@@ -427,6 +453,8 @@ int causal_order_impl(plg_ctx* c, const double* dX, int64_t ldx, int64_t n, int 
     int* act_cur = (r & 1) ? c->act1.p : c->act0.p;
     int* act_nxt = (r & 1) ? c->act0.p : c->act1.p;
     if (int rc = search_round(c, n, ldw, d, u, act_cur, r, 3 + 2 * static_cast<size_t>(r), st)) return rc;
+    if (c->hook && c->world == 1)
+      if (int rc = call_round_hook(c, u, r, act_cur, st)) return rc;
     plg::launch_commit(c->k.p, act_cur, act_nxt, u, c->colvar.p, c->order.p, r, nullptr, c->rs.p,
                        c->err.p, c->stream);
     ++c->launches;
@@ -818,6 +846,13 @@ int plg_tile_decode(int32_t t, int32_t nb, int32_t* bi, int32_t* bj) {
   plg::tile_decode(t, nb, a, b);
   *bi = a;
   *bj = b;
+  return 0;
+}
+
+int plg_debug_set_round_hook(plg_ctx* c, plg_round_hook hook, void* user) {
+  if (!c) return PLG_OutOfRange;
+  c->hook = hook;
+  c->hook_user = user;
   return 0;
 }
 
