@@ -54,6 +54,8 @@ typedef struct plg_stats {
   double h2d_ms;        /* host->device copy of X (host entry points only) */
   int64_t pair_evals;   /* ordered (i, j) pair evaluations of the reference's Alg. 1 */
   int64_t ede;          /* element-direction evaluations (= n * pair_evals) */
+  int64_t pairs_evaluated; /* unordered pairs whose two residual entropies were actually
+                              computed (exact pruning skips pairs that cannot change the order) */
   int64_t launches;     /* kernels launched by the call */
   int32_t rounds;
   int32_t world;
@@ -87,6 +89,13 @@ int plg_causal_order(plg_ctx* ctx, const double* X, int64_t n, int32_t d, int64_
 int plg_causal_order_device(plg_ctx* ctx, const double* dX, int64_t n, int32_t d, int64_t ld,
                             int32_t* order_out, plg_status* st);
 
+/* Exact pruning of causal_order's search rounds (default on; environment PLG_PRUNE=0 turns
+ * it off at context creation). A pruned round evaluates only the pairs needed to prove its
+ * argmin: rows whose partial k (a sum over a subset of non-negative terms) already exceeds
+ * an exactly computed k cannot win. The order is identical to the exhaustive rounds' and
+ * the winner's k has the same bits; only non-winning scores are left uncomputed, which
+ * causal_order never returns. plg_search always evaluates every pair. */
+int plg_set_prune(plg_ctx* ctx, int32_t enable, plg_status* st);
 /* plingam::search_causal_order(X, U) — ordering.hpp:27, ordering.cpp:101-168.
  * scores_out: d doubles, -inf for non-candidates, -k for candidates. */
 int plg_search(plg_ctx* ctx, const double* X, int64_t n, int32_t d, int64_t ld, const int32_t* U,

@@ -17,6 +17,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <initializer_list>
 #include <limits>
@@ -139,6 +140,14 @@ SegPlan seg_plan(int u, int64_t n) {
   return {static_cast<int>((n + seg_len - 1) / seg_len), static_cast<int>(seg_len)};
 }
 
+// Segmentation of a pruned round: fine (256-sample) segments so that even a short pair list
+// spreads over every SM; at most 64 segments. Pure function of n.
+SegPlan prune_seg_plan(int64_t n) {
+  const int64_t seg_len = std::max<int64_t>(256, round_up((n + 63) / 64, 4));
+  return {static_cast<int>((n + seg_len - 1) / seg_len), static_cast<int>(seg_len)};
+}
+constexpr int kPruneBatch = 32768;  // pairs per batch of the list kernel
+
 }  // namespace
 
 struct plg_ctx {
@@ -159,8 +168,19 @@ struct plg_ctx {
   std::vector<cudaEvent_t> ev;  // pool: [0]=start [1]=end [2]=h2d end, then 2 per round
   plg_stats last{};
   int64_t launches = 0;
+  int64_t pairs_done = 0;  // unordered pairs evaluated by exhaustive rounds of the last call
   plg_round_hook hook = nullptr;  // analysis hook (plg_debug_set_round_hook), null in production
   void* hook_user = nullptr;
+
+  // exact pruned rounds of causal_order (prune_kernels.cu); PLG_PRUNE="R:T:f1,f2,..." or "0"
+  bool prune = true;
+  int prune_R = 8;
+  int prune_T = 3;
+  std::vector<double> prune_fracs{0.05, 0.15};
+  bool prune_tile_seg = false;  // PLG_PRUNE_TILESEG=1: the exhaustive rounds' segmentation (bit-identity tests)
+  DevBuf<double> Md, KN, pk, L, ppart;
+  DevBuf<int> st0, st1, rowsel, off;
+  DevBuf<unsigned long long> kstar, evals;
 
   cudaError_t events(size_t count) {
     while (ev.size() < count) {
@@ -201,8 +221,33 @@ int make_tables(plg_ctx* ctx, plg_status* st) {
   return 0;
 }
 
+void parse_prune_env(plg_ctx* ctx) {
+  if (const char* v = std::getenv("PLG_PRUNE")) {
+    if (!strcmp(v, "0")) {
+      ctx->prune = false;
+    } else {
+      int R = 0, T = 0, used = 0;
+      if (sscanf(v, "%d:%d:%n", &R, &T, &used) == 2 && R >= 1 && T >= 1) {
+        ctx->prune_R = R;
+        ctx->prune_T = T;
+        ctx->prune_fracs.clear();
+        const char* f = v + used;
+        while (*f) {
+          char* end = nullptr;
+          const double x = strtod(f, &end);
+          if (end == f) break;
+          if (x > 0.0 && x < 1.0) ctx->prune_fracs.push_back(x);
+          f = (*end == ',') ? end + 1 : end;
+        }
+      }
+    }
+  }
+  if (const char* v = std::getenv("PLG_PRUNE_TILESEG")) ctx->prune_tile_seg = !strcmp(v, "1");
+}
+
 int ctx_init(plg_ctx* ctx, int device, plg_status* st) {
   ctx->device = device;
+  parse_prune_env(ctx);
   PLG_CUDA(cudaSetDevice(device));
   PLG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
   if (int rc = make_tables(ctx, st)) return rc;
@@ -266,7 +311,7 @@ size_t part_doubles(const RoundPlan& rp, int u) {
 
 // One search round over the active list act_cur (u >= 2): H, pairs, exchange, k.
 int search_round(plg_ctx* c, int64_t n, int64_t ldw, int ldc, int u, const int* act_cur,
-                 int round, size_t ev_base, plg_status* st) {
+                 int round, size_t ev_base, plg_status* st, double* KN = nullptr) {
   const RoundPlan rp = plan_round(u, n, c->rank, c->world);
   plg::launch_colent(c->W.p, ldw, n, c->C.p, ldc, act_cur, u, c->H.p, c->g_exp, c->g_log, c->nz.p,
                      c->colvar.p, round, c->err.p, c->stream);
@@ -317,8 +362,72 @@ int search_round(plg_ctx* c, int64_t n, int64_t ldw, int ldc, int u, const int* 
                         api.GetErrorString(r != ncclSuccess ? r : (r2 != ncclSuccess ? r2 : r3)));
   }
   plg::launch_kreduce(c->epack.p, c->H.p, u, rp.nb, c->k.p, c->err.p, exchange ? c->errs.p : c->err.p,
-                      exchange ? c->world : 1, c->stream);
+                      exchange ? c->world : 1, act_cur, KN, ldc, c->stream);
   ++c->launches;
+  c->pairs_done += static_cast<int64_t>(u) * (u - 1) / 2;
+  return 0;
+}
+
+// One exact pruned round (prune_kernels.cu): same chosen root and winner-k bits as
+// search_round, evaluating only the pairs needed to prove the argmin. Needs KN from an
+// earlier round of the same run.
+int search_round_pruned(plg_ctx* c, int64_t n, int64_t ldw, int d, int u, const int* act_cur, int round,
+                        size_t ev_base, plg_status* st) {
+  plg::launch_colent(c->W.p, ldw, n, c->C.p, d, act_cur, u, c->H.p, c->g_exp, c->g_log, c->nz.p,
+                     c->colvar.p, round, c->err.p, c->stream);
+  ++c->launches;
+  if (c->timing) cudaEventRecord(c->ev[ev_base], c->stream);
+  const SegPlan sp = c->prune_tile_seg ? seg_plan(u, n) : prune_seg_plan(n);
+  PLG_CUDA(cudaMemsetAsync(c->Md.p, 0xff, static_cast<size_t>(u) * u * sizeof(double), c->stream));
+  plg::PruneArgs a{};
+  a.W = c->W.p;
+  a.ldw = ldw;
+  a.n = n;
+  a.C = c->C.p;
+  a.ldc = d;
+  a.act = act_cur;
+  a.u = u;
+  a.d = d;
+  a.H = c->H.p;
+  a.Md = c->Md.p;
+  a.KN = c->KN.p;
+  a.L = c->L.p;
+  a.kstar = c->kstar.p;
+  a.pk = c->pk.p;
+  a.rowsel = c->rowsel.p;
+  a.off = c->off.p;
+  a.part = c->ppart.p;
+  a.batch = kPruneBatch;
+  a.seg_len = sp.seg_len;
+  a.nseg = sp.nseg;
+  a.g_exp = c->g_exp;
+  a.g_log = c->g_log;
+  a.err = c->err.p;
+  a.round = round;
+  a.k = c->k.p;
+  a.evals = c->evals.p;
+  int* sa = c->st0.p;
+  int* sb = c->st1.p;
+  a.state_in = sa;
+  a.state_out = sa;
+  plg::launch_prune_predict(a, c->stream);
+  plg::launch_prune_top(a, c->prune_R, c->stream);
+  c->launches += 2;
+  auto stage = [&](int kind, int m, bool final_pass) {
+    a.state_in = sa;
+    a.state_out = sb;
+    plg::launch_prune_select(a, kind, m, c->stream);
+    plg::launch_prune_scan(a, c->stream);
+    plg::launch_prune_pairs(a, c->stream);
+    std::swap(sa, sb);
+    a.state_in = sa;
+    plg::launch_prune_bound(a, final_pass, c->stream);
+    c->launches += 4;
+  };
+  stage(plg::kStageProbe, c->prune_T, false);
+  for (double f : c->prune_fracs) stage(plg::kStageRefine, std::max(1, static_cast<int>(f * u)), false);
+  stage(plg::kStageFull, 0, true);
+  if (c->timing) cudaEventRecord(c->ev[ev_base + 1], c->stream);
   return 0;
 }
 
@@ -347,6 +456,27 @@ int reserve_run(plg_ctx* c, int64_t n, int ncols, int64_t ldw, plg_status* st) {
   PLG_CUDA(c->idx.reserve(ncols));
   PLG_CUDA(c->nz.reserve(ncols));
   PLG_CUDA(c->events(3 + 2 * static_cast<size_t>(std::max(ncols, 1))));
+  return 0;
+}
+
+// Buffers of the pruned rounds (causal_order only).
+int reserve_prune(plg_ctx* c, int64_t n, int d, plg_status* st) {
+  const size_t dd = static_cast<size_t>(d) * d;
+  size_t nseg = static_cast<size_t>(prune_seg_plan(n).nseg);
+  if (c->prune_tile_seg)
+    for (int u = d; u > plg::kSmallU; --u) nseg = std::max(nseg, static_cast<size_t>(seg_plan(u, n).nseg));
+  PLG_CUDA(c->Md.reserve(dd));
+  PLG_CUDA(c->KN.reserve(dd));
+  PLG_CUDA(c->rowsel.reserve(dd));
+  PLG_CUDA(c->off.reserve(static_cast<size_t>(d) + 1));
+  PLG_CUDA(c->pk.reserve(d));
+  PLG_CUDA(c->L.reserve(d));
+  PLG_CUDA(c->st0.reserve(d));
+  PLG_CUDA(c->st1.reserve(d));
+  PLG_CUDA(c->kstar.reserve(1));
+  PLG_CUDA(c->evals.reserve(1));
+  PLG_CUDA(c->ppart.reserve(2 * nseg * kPruneBatch * 4));
+  PLG_CUDA(cudaMemsetAsync(c->evals.p, 0, sizeof(unsigned long long), c->stream));
   return 0;
 }
 
@@ -448,11 +578,22 @@ int causal_order_impl(plg_ctx* c, const double* dX, int64_t ldx, int64_t n, int 
   plg::launch_gram(c->W.p, ldw, n, d, c->C.p, d, c->gscr.p, c->stream);
   ++c->launches;
   const int rounds = (max_rounds < 0) ? d - 1 : std::min(max_rounds, d - 1);
+  // Exact pruning needs a previous exhaustive round's knowledge and pays off above the
+  // replicated small-round size; single-rank runs only.
+  const bool prune = c->prune && c->world == 1 && !c->hook && d > plg::kSmallU + 1 && rounds > 1;
+  c->pairs_done = 0;
+  if (prune)
+    if (int rc = reserve_prune(c, n, d, st)) return rc;
   for (int r = 0; r < rounds; ++r) {
     const int u = d - r;
     int* act_cur = (r & 1) ? c->act1.p : c->act0.p;
     int* act_nxt = (r & 1) ? c->act0.p : c->act1.p;
-    if (int rc = search_round(c, n, ldw, d, u, act_cur, r, 3 + 2 * static_cast<size_t>(r), st)) return rc;
+    const size_t evb = 3 + 2 * static_cast<size_t>(r);
+    if (prune && r > 0 && u > plg::kSmallU) {
+      if (int rc = search_round_pruned(c, n, ldw, d, u, act_cur, r, evb, st)) return rc;
+    } else if (int rc = search_round(c, n, ldw, d, u, act_cur, r, evb, st, (prune && r == 0) ? c->KN.p : nullptr)) {
+      return rc;
+    }
     if (c->hook && c->world == 1)
       if (int rc = call_round_hook(c, u, r, act_cur, st)) return rc;
     plg::launch_commit(c->k.p, act_cur, act_nxt, u, c->colvar.p, c->order.p, r, nullptr, c->rs.p,
@@ -467,14 +608,17 @@ int causal_order_impl(plg_ctx* c, const double* dX, int64_t ldx, int64_t n, int 
     }
   }
   if (c->timing) cudaEventRecord(c->ev[1], c->stream);
-  unsigned long long key = 0;
+  unsigned long long key = 0, pruned_pairs = 0;
   PLG_CUDA(cudaMemcpyAsync(&key, c->err.p, sizeof(key), cudaMemcpyDeviceToHost, c->stream));
+  if (prune)
+    PLG_CUDA(cudaMemcpyAsync(&pruned_pairs, c->evals.p, sizeof(pruned_pairs), cudaMemcpyDeviceToHost, c->stream));
   const int nout = (rounds == d - 1) ? d : rounds;
   PLG_CUDA(cudaMemcpyAsync(order_out, c->order.p, nout * sizeof(int32_t), cudaMemcpyDeviceToHost,
                            c->stream));
   PLG_CUDA(cudaStreamSynchronize(c->stream));
   PLG_CUDA(cudaGetLastError());
   finish_stats(c, n, d, rounds, host_in);
+  c->last.pairs_evaluated = c->pairs_done + static_cast<int64_t>(pruned_pairs);
   c->last.d2h_bytes = nout * sizeof(int32_t);
   if (key != plg::kNoError) return report_error(key, nullptr, st);
   return ok(st);
@@ -847,6 +991,12 @@ int plg_tile_decode(int32_t t, int32_t nb, int32_t* bi, int32_t* bj) {
   *bi = a;
   *bj = b;
   return 0;
+}
+
+int plg_set_prune(plg_ctx* c, int32_t enable, plg_status* st) {
+  if (!c) return set_status(st, PLG_OutOfRange, -1, -1, "null context");
+  c->prune = enable != 0;
+  return ok(st);
 }
 
 int plg_debug_set_round_hook(plg_ctx* c, plg_round_hook hook, void* user) {

@@ -517,6 +517,13 @@ PYBIND11_MODULE(_core, m) {
             return out;
           },
           py::arg("u"))
+      .def(
+          "set_prune",
+          [](Engine& e, bool enable) {
+            plg_status st{};
+            gpu::check(plg_set_prune(e.ctx, enable ? 1 : 0, &st), &st);
+          },
+          py::arg("enable"))
       .def("stats", [](Engine& e) {
         plg_stats s{};
         plg_last_stats(e.ctx, &s);
@@ -525,6 +532,7 @@ PYBIND11_MODULE(_core, m) {
         d["pair_ms"] = s.pair_ms;
         d["h2d_ms"] = s.h2d_ms;
         d["pair_evals"] = s.pair_evals;
+        d["pairs_evaluated"] = s.pairs_evaluated;
         d["ede"] = s.ede;
         d["launches"] = s.launches;
         d["rounds"] = s.rounds;

@@ -22,6 +22,7 @@
 
 #include "plg_kernels.h"
 #include "plg_math.cuh"
+#include "plg_pair.cuh"
 
 namespace plg {
 
@@ -67,29 +68,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
-// Per-pair scales of both directions from the maintained Gram: u'_1 = x s1 - y bs1 is the
-// scaled residual of i on j, u'_2 = y s2 - x bs2 that of j on i (u' = K u, plg_math.cuh).
-// Zeros (and the error key) for an exactly collinear pair.
+// Per-pair scales of both directions (plg_pair.cuh); zeros and the error key for an exactly
+// collinear pair.
 __device__ __forceinline__ void pair_params(const PairLaunch& a, int ci, int cj, double& s1, double& bs1,
                                             double& s2, double& bs2) {
-  const double cii = a.C[static_cast<int64_t>(ci) * a.ldc + ci];
-  const double cjj = a.C[static_cast<int64_t>(cj) * a.ldc + cj];
-  const double cij = a.C[static_cast<int64_t>(ci) * a.ldc + cj];
-  const double b1 = cij / cjj;  // slope of i on j (ordering.cpp:89, cov / col_var[q])
-  const double v1 = cii - cij * b1;
-  const double b2 = cij / cii;  // slope of j on i (ordering.cpp:90)
-  const double v2 = cjj - cij * b2;
-  if (!(v1 > 0.0) || !(v2 > 0.0)) {
-    // exactly collinear pair (e.g. bit-identical standardised columns): the residual is
-    // identically zero and entropy_of_normalized throws (kernels.cpp:136-139)
-    atomicMin(a.err, err_key(a.round, kErrPairCollinear, -1));
-    s1 = bs1 = s2 = bs2 = 0.0;
-    return;
-  }
-  s1 = kUScale / sqrt(v1);
-  bs1 = b1 * s1;
-  s2 = kUScale / sqrt(v2);
-  bs2 = b2 * s2;
+  if (!pair_scales(a.C, a.ldc, ci, cj, s1, bs1, s2, bs2)) atomicMin(a.err, err_key(a.round, kErrPairCollinear, -1));
 }
 
 constexpr int kStages = 3;

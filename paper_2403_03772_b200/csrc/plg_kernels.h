@@ -117,8 +117,54 @@ void launch_gram(const double* W, int64_t ldw, int64_t n, int ncol, double* C, i
 
 // k[p] = sum_{q != p} min(0, M_pq)^2 with M_pq = (H_q + E(p|q)) - (H_p + E(q|p)).
 // errs[0..world): error keys gathered from every rank (world = 1: errs = err).
+// KN (optional, d x d by variable): KN[act[p] * d + act[q]] = min(0, M_pq)^2 for every pair
+// (the pruned rounds' knowledge, prune_kernels.cu).
 void launch_kreduce(const double* epack, const double* H, int u, int nb, double* k,
-                    unsigned long long* err, const unsigned long long* errs, int world, cudaStream_t s);
+                    unsigned long long* err, const unsigned long long* errs, int world,
+                    const int* act, double* KN, int d, cudaStream_t s);
+
+// ---- exact pruned search round (prune_kernels.cu) ----
+// Row states: 0 pruned (k provably > k*), 1 alive, 2 top (full row from the start).
+struct PruneArgs {
+  const double* W;
+  int64_t ldw;
+  int64_t n;
+  const double* C;
+  int64_t ldc;
+  const int* act;
+  int u;
+  int d;
+  const double* H;              // [u] column entropies of the round
+  double* Md;                   // [u * u] M_pq of evaluated pairs, NaN otherwise
+  double* KN;                   // [d * d] last evaluated min(0, M)^2 by variable pair
+  const int* state_in;          // [u]
+  int* state_out;               // [u]
+  double* L;                    // [u] partial k over the evaluated pairs
+  unsigned long long* kstar;    // bits of min exact k over the top rows
+  double* pk;                   // [u] predicted k (sum of KN over the active row)
+  int* rowsel;                  // [u * u] selected partner positions of each row, ascending
+  int* off;                     // [u + 1] per-row counts -> exclusive offsets, off[u] = total
+  double* part;                 // [2][nseg][batch][4] segment partial sums
+  int batch;                    // pairs per batch of the list kernel
+  int seg_len;
+  int nseg;
+  const double* g_exp;
+  const double2* g_log;
+  unsigned long long* err;
+  int round;
+  double* k;                    // [u] exact k of alive/top rows, +inf for pruned rows
+  unsigned long long* evals;    // running count of list entries evaluated (statistics)
+};
+enum PruneStage : int { kStageProbe = 0, kStageRefine = 1, kStageFull = 2 };
+void launch_prune_predict(const PruneArgs& a, cudaStream_t s);
+void launch_prune_top(const PruneArgs& a, int R, cudaStream_t s);
+// m: partners per row (probe: suspects per non-top row; refine: top-m predicted)
+void launch_prune_select(const PruneArgs& a, int stage, int m, cudaStream_t s);
+void launch_prune_scan(const PruneArgs& a, cudaStream_t s);
+void launch_prune_pairs(const PruneArgs& a, cudaStream_t s);
+// final: k[] and KN of the evaluated pairs, else L[] and k* over the top rows
+void launch_prune_bound(const PruneArgs& a, bool final_pass, cudaStream_t s);
+int prune_pairs_grid();  // co-resident CTAs of the cooperative list kernel
 
 // argmin over k (lowest position on ties), order/score bookkeeping, active-list compaction.
 void launch_commit(const double* k, const int* act_cur, int* act_nxt, int u, const int* col_var,

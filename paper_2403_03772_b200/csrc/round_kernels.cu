@@ -158,7 +158,8 @@ __device__ __forceinline__ int tile_index(int bi, int bj, int nb) {
 // are the ranks' error keys gathered with the entropy tiles (a pair error is seen only by
 // the rank that owns the tile): every rank adopts the smallest, so all report the same.
 __global__ void kreduce_kernel(const double* epack, const double* H, int u, int nb, double* k,
-                               unsigned long long* err, const unsigned long long* errs, int world) {
+                               unsigned long long* err, const unsigned long long* errs, int world,
+                               const int* act, double* KN, int d) {
   unsigned long long key = *err;
   for (int r = 0; r < world; ++r) key = min(key, errs[r]);
   if (key != kNoError) {
@@ -170,6 +171,7 @@ __global__ void kreduce_kernel(const double* epack, const double* H, int u, int 
   if (p >= u) return;
   const int bp = p / kBT, xp = p % kBT;
   const double hp = H[p];
+  double* kn = KN ? KN + static_cast<int64_t>(act[p]) * d : nullptr;
   double acc = 0.0;
   for (int q = lane; q < u; q += 32) {
     if (q == p) continue;
@@ -188,6 +190,7 @@ __global__ void kreduce_kernel(const double* epack, const double* H, int u, int 
     const double mi = (H[q] + e_pq) - (hp + e_qp);
     const double c = (mi < 0.0) ? mi : 0.0;
     acc = __dadd_rn(acc, __dmul_rn(c, c));
+    if (kn) kn[act[q]] = __dmul_rn(c, c);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -339,8 +342,9 @@ void launch_gram(const double* W, int64_t ldw, int64_t n, int ncol, double* C, i
 }
 
 void launch_kreduce(const double* epack, const double* H, int u, int nb, double* k,
-                    unsigned long long* err, const unsigned long long* errs, int world, cudaStream_t s) {
-  kreduce_kernel<<<(u + 7) / 8, 256, 0, s>>>(epack, H, u, nb, k, err, errs, world);
+                    unsigned long long* err, const unsigned long long* errs, int world,
+                    const int* act, double* KN, int d, cudaStream_t s) {
+  kreduce_kernel<<<(u + 7) / 8, 256, 0, s>>>(epack, H, u, nb, k, err, errs, world, act, KN, d);
 }
 
 void launch_commit(const double* k, const int* act_cur, int* act_nxt, int u, const int* col_var,
