@@ -96,6 +96,9 @@ int plg_causal_order_device(plg_ctx* ctx, const double* dX, int64_t n, int32_t d
  * the winner's k has the same bits; only non-winning scores are left uncomputed, which
  * causal_order never returns. plg_search always evaluates every pair. */
 int plg_set_prune(plg_ctx* ctx, int32_t enable, plg_status* st);
+/* The winning k (= -score of the chosen variable) of every round of the last causal_order on
+ * ctx, in round order (count = min(cap, rounds)). Diagnostics and parity tests. */
+int plg_last_round_k(plg_ctx* ctx, double* out, int32_t cap, int32_t* count, plg_status* st);
 /* plingam::search_causal_order(X, U) — ordering.hpp:27, ordering.cpp:101-168.
  * scores_out: d doubles, -inf for non-candidates, -k for candidates. */
 int plg_search(plg_ctx* ctx, const double* X, int64_t n, int32_t d, int64_t ld, const int32_t* U,

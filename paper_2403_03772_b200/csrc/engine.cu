@@ -161,7 +161,7 @@ struct plg_ctx {
   double* g_exp = nullptr;
   double2* g_log = nullptr;
 
-  DevBuf<double> Xd, W, C, part, epack, H, k, scores, msd, gscr;
+  DevBuf<double> Xd, W, C, part, epack, H, k, scores, msd, gscr, rk;
   DevBuf<int> act0, act1, colvar, order, stat, idx, nz;
   DevBuf<plg::RoundState> rs;
   DevBuf<unsigned long long> err, errs;
@@ -446,6 +446,7 @@ int reserve_run(plg_ctx* c, int64_t n, int ncols, int64_t ldw, plg_status* st) {
   PLG_CUDA(c->epack.reserve(epack_max));
   PLG_CUDA(c->H.reserve(ncols));
   PLG_CUDA(c->k.reserve(ncols));
+  PLG_CUDA(c->rk.reserve(ncols));
   PLG_CUDA(c->scores.reserve(ncols));
   PLG_CUDA(c->act0.reserve(ncols));
   PLG_CUDA(c->act1.reserve(ncols));
@@ -597,7 +598,7 @@ int causal_order_impl(plg_ctx* c, const double* dX, int64_t ldx, int64_t n, int 
     if (c->hook && c->world == 1)
       if (int rc = call_round_hook(c, u, r, act_cur, st)) return rc;
     plg::launch_commit(c->k.p, act_cur, act_nxt, u, c->colvar.p, c->order.p, r, nullptr, c->rs.p,
-                       c->err.p, c->stream);
+                       c->err.p, c->stream, c->rk.p);
     ++c->launches;
     if (u - 1 >= 2 || (u - 1 == 1 && max_rounds >= 0)) {
       // the next round's build_cache check only exists when it has >= 2 candidates
@@ -991,6 +992,14 @@ int plg_tile_decode(int32_t t, int32_t nb, int32_t* bi, int32_t* bj) {
   *bi = a;
   *bj = b;
   return 0;
+}
+
+int plg_last_round_k(plg_ctx* c, double* out, int32_t cap, int32_t* count, plg_status* st) {
+  if (!c || !count) return set_status(st, PLG_OutOfRange, -1, -1, "null argument");
+  const int n = std::min(cap, c->last.rounds);
+  *count = n;
+  if (n > 0) PLG_CUDA(cudaMemcpy(out, c->rk.p, n * sizeof(double), cudaMemcpyDeviceToHost));
+  return ok(st);
 }
 
 int plg_set_prune(plg_ctx* c, int32_t enable, plg_status* st) {

@@ -517,6 +517,17 @@ PYBIND11_MODULE(_core, m) {
             return out;
           },
           py::arg("u"))
+      .def("round_k",
+           [](Engine& e) {
+             plg_stats s{};
+             plg_last_stats(e.ctx, &s);
+             std::vector<double> k(static_cast<std::size_t>(std::max(s.rounds, 0)));
+             int32_t cnt = 0;
+             plg_status st{};
+             gpu::check(plg_last_round_k(e.ctx, k.data(), static_cast<int32_t>(k.size()), &cnt, &st), &st);
+             k.resize(static_cast<std::size_t>(cnt));
+             return k;
+           })
       .def(
           "set_prune",
           [](Engine& e, bool enable) {

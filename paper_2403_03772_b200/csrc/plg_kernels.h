@@ -166,10 +166,11 @@ void launch_prune_pairs(const PruneArgs& a, cudaStream_t s);
 void launch_prune_bound(const PruneArgs& a, bool final_pass, cudaStream_t s);
 int prune_pairs_grid();  // co-resident CTAs of the cooperative list kernel
 
-// argmin over k (lowest position on ties), order/score bookkeeping, active-list compaction.
+// argmin over k (lowest position on ties), order/score bookkeeping, active-list compaction;
+// round_k (optional): the winning k of each round.
 void launch_commit(const double* k, const int* act_cur, int* act_nxt, int u, const int* col_var,
                    int* order, int round, double* scores, RoundState* rs,
-                   const unsigned long long* err, cudaStream_t s);
+                   const unsigned long long* err, cudaStream_t s, double* round_k = nullptr);
 
 // Rank-1 Schur update of the remaining Gram block.
 void launch_update_gram(double* C, int64_t ldc, const int* act_nxt, int ur, const RoundState* rs,

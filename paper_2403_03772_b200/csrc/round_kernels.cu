@@ -204,7 +204,7 @@ constexpr int kCommitThreads = 1024;
 __global__ void __launch_bounds__(kCommitThreads)
     commit_kernel(const double* k, const int* act_cur, int* act_nxt, int u, const int* col_var,
                   int* order, int round, double* scores, RoundState* rs,
-                  const unsigned long long* err) {
+                  const unsigned long long* err, double* round_k) {
   __shared__ double sk[kCommitThreads];
   __shared__ int sp[kCommitThreads];
   if (*err != kNoError) return;
@@ -237,6 +237,7 @@ __global__ void __launch_bounds__(kCommitThreads)
   if (threadIdx.x == 0) {
     rs->chosen_pos = pc;
     rs->chosen_col = m;
+    if (round_k) round_k[round] = sk[0];
     if (order) {
       order[round] = col_var[m];
       if (u == 2) order[round + 1] = col_var[act_cur[1 - pc]];  // ordering.cpp:242
@@ -349,9 +350,9 @@ void launch_kreduce(const double* epack, const double* H, int u, int nb, double*
 
 void launch_commit(const double* k, const int* act_cur, int* act_nxt, int u, const int* col_var,
                    int* order, int round, double* scores, RoundState* rs,
-                   const unsigned long long* err, cudaStream_t s) {
+                   const unsigned long long* err, cudaStream_t s, double* round_k) {
   commit_kernel<<<1, kCommitThreads, 0, s>>>(k, act_cur, act_nxt, u, col_var, order, round, scores,
-                                             rs, err);
+                                             rs, err, round_k);
 }
 
 void launch_update_gram(double* C, int64_t ldc, const int* act_nxt, int ur, const RoundState* rs,

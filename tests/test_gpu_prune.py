@@ -1,0 +1,82 @@
+"""Exact pruned search rounds (prune_kernels.cu): causal_order evaluates only the pairs that
+prove each round's argmin. Contracts:
+
+* the order is identical to the exhaustive rounds' (and to the oracle's on the goldens,
+  tests/test_gpu_parity.py, which run with pruning on);
+* with the exhaustive rounds' sample segmentation (PLG_PRUNE_TILESEG=1) every winning k has
+  the same bits as the exhaustive round's — pruning changes which pairs are evaluated,
+  never a value;
+* with the default fine segmentation the winning k agree to rounding (the 1e-9 relative
+  score bar of test_gpu_parity.py);
+* pruning evaluates a small fraction of the pairs on sparse-DAG data, and none of its
+  decisions depend on the data being "nice": on exchangeable Gaussian data (nothing to
+  prune) it still returns the exhaustive order.
+"""
+
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+_CHILD = r"""
+import json, sys
+sys.path.insert(0, %r)
+import numpy as np
+import paper_2403_03772_b200 as plg
+d, n, seed, kind = %d, %d, %d, %r
+if kind == "gauss":
+    X = np.asfortranarray(np.random.default_rng(seed).normal(size=(n, d)))
+else:
+    dag = plg.gen_sparse_dag(d, avg_parents=2.0, seed=seed)
+    X = plg.sample_lingam(dag, n, seed=seed, kind=kind)
+eng = plg.Engine(0)
+out = {}
+for mode in ("prune", "full"):
+    eng.set_prune(mode == "prune")
+    order = eng.causal_order(X)
+    out[mode] = {"order": order, "k": [float(v).hex() for v in eng.round_k()],
+                 "pairs": eng.stats()["pairs_evaluated"]}
+print(json.dumps(out))
+"""
+
+
+def _run(d, n, seed, kind, tileseg):
+    env = dict(os.environ, PLG_PRUNE_TILESEG="1" if tileseg else "0")
+    env.pop("PLG_PRUNE", None)
+    out = subprocess.run([sys.executable, "-c", _CHILD % (ROOT, d, n, seed, kind)], env=env,
+                         capture_output=True, text=True, check=True, timeout=900)
+    return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+@pytest.mark.parametrize("d,n,seed,kind", [(300, 4000, 7, "laplace"), (260, 3001, 11, "t3"),
+                                           (200, 2000, 5, "uniform")])
+def test_pruned_rounds_bit_identical_with_exhaustive_segmentation(d, n, seed, kind):
+    r = _run(d, n, seed, kind, tileseg=True)
+    assert r["prune"]["order"] == r["full"]["order"]
+    assert r["prune"]["k"] == r["full"]["k"]  # every round's winning k, bit for bit
+    full_pairs = sum(u * (u - 1) // 2 for u in range(2, d + 1))
+    assert r["full"]["pairs"] == full_pairs
+    assert r["prune"]["pairs"] < 0.5 * full_pairs
+
+
+def test_pruned_rounds_default_segmentation():
+    r = _run(400, 10000, 3, "laplace", tileseg=False)
+    assert r["prune"]["order"] == r["full"]["order"]
+    kp = np.array([float.fromhex(v) for v in r["prune"]["k"]])
+    kf = np.array([float.fromhex(v) for v in r["full"]["k"]])
+    # different sample segmentation: k agree to rounding (the score parity bar of test_gpu_parity)
+    assert np.all(np.abs(kp - kf) <= 1e-9 * np.abs(kf) + 1e-15)
+    assert r["prune"]["pairs"] < 0.25 * r["full"]["pairs"]
+
+
+def test_pruned_rounds_on_exchangeable_gaussian_data():
+    # no causal structure: every candidate's k is noise of one size; pruning must still be exact
+    r = _run(180, 1500, 2, "gauss", tileseg=True)
+    assert r["prune"]["order"] == r["full"]["order"]
+    assert r["prune"]["k"] == r["full"]["k"]
