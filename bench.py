@@ -10,7 +10,11 @@ A step is one full causal_order over the synthetic matrix. `value` is measured w
 matrix already resident in HBM (device time from CUDA events on the engine stream, max
 over ranks); `e2e` is the same metric through the public API with the matrix in pinned
 host memory (H2D copy and D2H of the order inside the timed region).
-pair-evals = P(d) = (d+1) d (d-1) / 3 ordered (i, j) evaluations of Alg. 1 per fit.
+pair-evals = P(d) = (d+1) d (d-1) / 3 ordered (i, j) evaluations of Alg. 1 per fit: the
+reference's work for the same order, so value = P(d) / wall is reference-equivalent. The
+engine's exact pruning (prune_kernels.cu) evaluates only the pairs that decide each round's
+argmin; `pruning` reports how many it actually evaluated, and the roofline is computed on
+those executed evaluations. --no-prune times the exhaustive rounds instead.
 """
 
 import argparse
@@ -110,12 +114,12 @@ class ClockSampler:
                 "power_w_max": float(max(float(r[3]) for r in rows if r[3].replace(".", "").isdigit()))}
 
 
-def load_ncu_traffic():
-    """dram bytes per pair-kernel launch from the committed ncu --set full summary, if any."""
+def load_ncu_traffic(suffix):
+    """dram bytes per launch of the dominant kernel from the committed ncu --set full summary."""
     for path in sorted(
             [os.path.join(ROOT, "profiles", f) for f in os.listdir(os.path.join(ROOT, "profiles"))]
             if os.path.isdir(os.path.join(ROOT, "profiles")) else [], reverse=True):
-        if path.endswith("pair_kernel_ncu.json"):
+        if path.endswith(suffix):
             try:
                 return json.load(open(path)).get("dram_bytes_per_launch")
             except (OSError, ValueError):
@@ -222,6 +226,7 @@ def run_ours(args, world, rank, local):
     else:
         torch.cuda.set_device(local)
         eng = plg.Engine(local)
+    eng.set_prune(not args.no_prune)
     X = make_input(args.config)
     dX = torch.from_numpy(np.ascontiguousarray(X.T)).to(f"cuda:{local}")  # column j contiguous
     ptr = dX.data_ptr()
@@ -229,7 +234,7 @@ def run_ours(args, world, rank, local):
         order = eng.causal_order_device(ptr, n, d, n)
     barrier(world)
 
-    dev_ms, pair_ms, launches = [], [], 0
+    dev_ms, pair_ms, launches, pair_launches, pairs_done = [], [], 0, 0, 0
     with ClockSampler(local) as clocks:
         barrier(world)
         t0 = time.perf_counter()
@@ -239,6 +244,8 @@ def run_ours(args, world, rank, local):
             dev_ms.append(st["total_ms"])
             pair_ms.append(st["pair_ms"])
             launches += st["launches"]
+            pair_launches += st["pair_launches"]
+            pairs_done += st["pairs_evaluated"]
         barrier(world)
         wall = time.perf_counter() - t0
     clk = clocks.summary()
@@ -263,10 +270,13 @@ def run_ours(args, world, rank, local):
 
     if rank != 0:
         return
-    ede = n * P
     pair_s = sum(pair_ms) / 1e3 / args.steps
-    # the pair kernel's share of the step and its FP64-pipe roofline
+    # executed work: every evaluated unordered pair computes both residual entropies over n
+    pairs_step = pairs_done / args.steps
+    ede = 2 * n * pairs_step
+    # the pair-evaluation kernels' share of the step and their FP64-pipe roofline
     achieved = FP64_OPS_PER_EDE * 2 * ede / (pair_s * world) / 1e12 if pair_s > 0 else None
+    pruned = not args.no_prune
     line = {
         "metric": "causal-order pair-evals/s (and wall s) at d=2000,n=10k",
         "value": value, "unit": "pair-evals/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -278,16 +288,26 @@ def run_ours(args, world, rank, local):
                    "parallelism": f"pair tiles sharded over {world} GPU(s), one ncclAllGather per round"
                    if world > 1 else "single GPU",
                    "l2": "input larger than L2 (FP64 matrix %.0f MB vs 126 MB L2)" % (8 * n * d / 1e6)},
-        "roofline": {"bound": "fp64", "kernel": "pair_kernel+finalize", "unit": "TFLOP/s",
+        "pruning": {"enabled": pruned, "pairs_evaluated_per_step": pairs_step,
+                    "pairs_exhaustive_per_step": P // 2,
+                    "fraction_evaluated": pairs_step / (P // 2),
+                    "executed_pair_evals_per_s": 2 * pairs_step * args.steps / dev_s,
+                    "note": "exact branch and bound on each round's k: rows whose partial k (a sum of "
+                            "non-negative terms) exceeds an exactly computed k cannot win; the order and "
+                            "the winner's k bits equal the exhaustive rounds' (tests/test_gpu_prune.py)"},
+        "roofline": {"bound": "fp64",
+                     "kernel": "prune_pairs_kernel (pair lists) + pair_kernel (round 0)" if pruned
+                     else "pair_kernel+finalize", "unit": "TFLOP/s",
                      "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
                      "frac": achieved / FP64_PEAK_TFLOPS if achieved else None,
-                     "traffic": load_ncu_traffic(),
-                     "traffic_note": "dram read+write bytes of one u=2000 pair-kernel launch (ncu --set full, "
-                                     "profiles/r1_pair_kernel_ncu.md); its algorithmic bytes are one pass over W "
-                                     "(160 MB) — compute-bound, L2 serves the tile re-reads",
-                     "basis": f"{FP64_OPS_PER_EDE} FP64-pipe instructions per EDE (SASS) x 2 flops, "
-                              f"EDE = n * pair-evals; peak = measured DFMA rate (no FP64 figure in "
-                              f"MEASURED_PEAKS.json)",
+                     "traffic": load_ncu_traffic("prune_pairs_ncu.json" if pruned else "pair_kernel_ncu.json"),
+                     "traffic_note": "dram read+write bytes of one launch of the dominant kernel (ncu --set full, "
+                                     "profiles/); algorithmic bytes: one pass over the listed pairs' columns "
+                                     "per launch — compute-bound, L2 serves the re-reads",
+                     "basis": f"{FP64_OPS_PER_EDE} FP64-pipe instructions per EDE (SASS of both kernels' inner "
+                              f"loops) x 2 flops over the EXECUTED EDE = 2 n x pairs evaluated; time = CUDA "
+                              f"events around every pair-evaluation launch ({pair_launches // max(1, args.steps)} "
+                              f"per step); peak = measured DFMA rate (no FP64 figure in MEASURED_PEAKS.json)",
                      "libdevice_basis_frac": (LIBDEVICE_OPS_PER_EDE * 2 * ede / (pair_s * world) / 1e12)
                      / FP64_PEAK_TFLOPS if pair_s > 0 else None,
                      "pair_share_of_step": pair_s / (dev_s / args.steps)},
@@ -305,12 +325,13 @@ def run_ours(args, world, rank, local):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c5")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-prune", action="store_true", help="exhaustive rounds (every pair, every round)")
     args = ap.parse_args()
     world, rank, local = dist_setup(args)
     try:

@@ -50,13 +50,15 @@ enum plg_error_code {
 /* Per-call measurements of the last causal_order / search on this context. */
 typedef struct plg_stats {
   double total_ms;      /* device time of the whole call (CUDA events on the engine stream) */
-  double pair_ms;       /* sum over rounds of pair kernel + finalize device time */
+  double pair_ms;       /* device time of the pair-evaluation launches (exhaustive rounds: pair
+                           kernel + finalize; pruned rounds: the pair-list kernel) */
   double h2d_ms;        /* host->device copy of X (host entry points only) */
   int64_t pair_evals;   /* ordered (i, j) pair evaluations of the reference's Alg. 1 */
   int64_t ede;          /* element-direction evaluations (= n * pair_evals) */
   int64_t pairs_evaluated; /* unordered pairs whose two residual entropies were actually
                               computed (exact pruning skips pairs that cannot change the order) */
   int64_t launches;     /* kernels launched by the call */
+  int64_t pair_launches; /* pair-evaluation launches timed into pair_ms */
   int32_t rounds;
   int32_t world;
   int64_t h2d_bytes;

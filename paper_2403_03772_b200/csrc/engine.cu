@@ -146,7 +146,7 @@ SegPlan prune_seg_plan(int64_t n) {
   const int64_t seg_len = std::max<int64_t>(256, round_up((n + 63) / 64, 4));
   return {static_cast<int>((n + seg_len - 1) / seg_len), static_cast<int>(seg_len)};
 }
-constexpr int kPruneBatch = 32768;  // pairs per batch of the list kernel
+constexpr int kPruneBatch = 131072;  // pairs per batch of the list kernel (part-buffer capacity)
 
 }  // namespace
 
@@ -179,8 +179,10 @@ struct plg_ctx {
   std::vector<double> prune_fracs{0.05, 0.15};
   bool prune_tile_seg = false;  // PLG_PRUNE_TILESEG=1: the exhaustive rounds' segmentation (bit-identity tests)
   DevBuf<double> Md, KN, pk, L, ppart;
-  DevBuf<int> st0, st1, rowsel, off;
+  DevBuf<int> st0, st1, rowsel, off, pwork, pdone;
   DevBuf<unsigned long long> kstar, evals;
+
+  size_t ev_pairs = 0;  // pair-kernel timing intervals recorded by this call (ev[3 + 2 i], ev[4 + 2 i])
 
   cudaError_t events(size_t count) {
     while (ev.size() < count) {
@@ -194,6 +196,20 @@ struct plg_ctx {
 };
 
 namespace {
+
+// CUDA-event interval around one pair-evaluation launch (plg_stats.pair_ms / pair_launches).
+size_t pair_timer_begin(plg_ctx* c) {
+  if (!c->timing) return 0;
+  const size_t i = 3 + 2 * c->ev_pairs;
+  if (c->events(i + 2) != cudaSuccess) return 0;
+  cudaEventRecord(c->ev[i], c->stream);
+  return i;
+}
+void pair_timer_end(plg_ctx* c, size_t i) {
+  if (!c->timing || i == 0) return;
+  cudaEventRecord(c->ev[i + 1], c->stream);
+  ++c->ev_pairs;
+}
 
 int make_tables(plg_ctx* ctx, plg_status* st) {
   std::vector<double> e(plg::kExpN);
@@ -311,7 +327,7 @@ size_t part_doubles(const RoundPlan& rp, int u) {
 
 // One search round over the active list act_cur (u >= 2): H, pairs, exchange, k.
 int search_round(plg_ctx* c, int64_t n, int64_t ldw, int ldc, int u, const int* act_cur,
-                 int round, size_t ev_base, plg_status* st, double* KN = nullptr) {
+                 int round, plg_status* st, double* KN = nullptr) {
   const RoundPlan rp = plan_round(u, n, c->rank, c->world);
   plg::launch_colent(c->W.p, ldw, n, c->C.p, ldc, act_cur, u, c->H.p, c->g_exp, c->g_log, c->nz.p,
                      c->colvar.p, round, c->err.p, c->stream);
@@ -335,7 +351,7 @@ int search_round(plg_ctx* c, int64_t n, int64_t ldw, int ldc, int u, const int* 
   a.g_log = c->g_log;
   a.err = c->err.p;
   a.round = round;
-  if (c->timing) cudaEventRecord(c->ev[ev_base], c->stream);
+  const size_t tm = pair_timer_begin(c);
   if (rp.replicated) {
     plg::launch_pair_small(a, c->stream);
     plg::launch_finalize_small(a, c->stream);
@@ -345,7 +361,7 @@ int search_round(plg_ctx* c, int64_t n, int64_t ldw, int ldc, int u, const int* 
     plg::launch_finalize(a, c->stream);
     c->launches += 2;
   }
-  if (c->timing) cudaEventRecord(c->ev[ev_base + 1], c->stream);
+  pair_timer_end(c, tm);
   const bool exchange = c->world > 1 && !rp.replicated;
   if (exchange) {
     // One grouped exchange per round: the entropy tiles (in place, rank slots of tpr tiles)
@@ -372,11 +388,10 @@ int search_round(plg_ctx* c, int64_t n, int64_t ldw, int ldc, int u, const int* 
 // search_round, evaluating only the pairs needed to prove the argmin. Needs KN from an
 // earlier round of the same run.
 int search_round_pruned(plg_ctx* c, int64_t n, int64_t ldw, int d, int u, const int* act_cur, int round,
-                        size_t ev_base, plg_status* st) {
+                        plg_status* st) {
   plg::launch_colent(c->W.p, ldw, n, c->C.p, d, act_cur, u, c->H.p, c->g_exp, c->g_log, c->nz.p,
                      c->colvar.p, round, c->err.p, c->stream);
   ++c->launches;
-  if (c->timing) cudaEventRecord(c->ev[ev_base], c->stream);
   const SegPlan sp = c->prune_tile_seg ? seg_plan(u, n) : prune_seg_plan(n);
   PLG_CUDA(cudaMemsetAsync(c->Md.p, 0xff, static_cast<size_t>(u) * u * sizeof(double), c->stream));
   plg::PruneArgs a{};
@@ -397,6 +412,8 @@ int search_round_pruned(plg_ctx* c, int64_t n, int64_t ldw, int d, int u, const 
   a.rowsel = c->rowsel.p;
   a.off = c->off.p;
   a.part = c->ppart.p;
+  a.work = c->pwork.p;
+  a.done = c->pdone.p;
   a.batch = kPruneBatch;
   a.seg_len = sp.seg_len;
   a.nseg = sp.nseg;
@@ -418,7 +435,9 @@ int search_round_pruned(plg_ctx* c, int64_t n, int64_t ldw, int d, int u, const 
     a.state_out = sb;
     plg::launch_prune_select(a, kind, m, c->stream);
     plg::launch_prune_scan(a, c->stream);
+    const size_t tm = pair_timer_begin(c);
     plg::launch_prune_pairs(a, c->stream);
+    pair_timer_end(c, tm);
     std::swap(sa, sb);
     a.state_in = sa;
     plg::launch_prune_bound(a, final_pass, c->stream);
@@ -427,7 +446,6 @@ int search_round_pruned(plg_ctx* c, int64_t n, int64_t ldw, int d, int u, const 
   stage(plg::kStageProbe, c->prune_T, false);
   for (double f : c->prune_fracs) stage(plg::kStageRefine, std::max(1, static_cast<int>(f * u)), false);
   stage(plg::kStageFull, 0, true);
-  if (c->timing) cudaEventRecord(c->ev[ev_base + 1], c->stream);
   return 0;
 }
 
@@ -456,7 +474,7 @@ int reserve_run(plg_ctx* c, int64_t n, int ncols, int64_t ldw, plg_status* st) {
   PLG_CUDA(c->msd.reserve(2 * static_cast<size_t>(ncols)));
   PLG_CUDA(c->idx.reserve(ncols));
   PLG_CUDA(c->nz.reserve(ncols));
-  PLG_CUDA(c->events(3 + 2 * static_cast<size_t>(std::max(ncols, 1))));
+  PLG_CUDA(c->events(3 + 2 * static_cast<size_t>(std::max(ncols, 1)) * (3 + c->prune_fracs.size())));
   return 0;
 }
 
@@ -476,7 +494,11 @@ int reserve_prune(plg_ctx* c, int64_t n, int d, plg_status* st) {
   PLG_CUDA(c->st1.reserve(d));
   PLG_CUDA(c->kstar.reserve(1));
   PLG_CUDA(c->evals.reserve(1));
-  PLG_CUDA(c->ppart.reserve(2 * nseg * kPruneBatch * 4));
+  PLG_CUDA(c->ppart.reserve(nseg * kPruneBatch * 4));
+  const size_t max_list = dd + d;  // per-stage list bound: u (u - 1) entries + slack
+  PLG_CUDA(c->pwork.reserve(max_list / kPruneBatch + 2));
+  PLG_CUDA(c->pdone.reserve(kPruneBatch / 32));
+  PLG_CUDA(cudaMemsetAsync(c->pdone.p, 0, (kPruneBatch / 32) * sizeof(int), c->stream));
   PLG_CUDA(cudaMemsetAsync(c->evals.p, 0, sizeof(unsigned long long), c->stream));
   return 0;
 }
@@ -533,10 +555,11 @@ void finish_stats(plg_ctx* c, int64_t n, int d, int rounds, bool host_in) {
     s.h2d_ms = ms;
   }
   double pair_ms = 0.0;
-  for (int r = 0; r < rounds; ++r) {
-    if (cudaEventElapsedTime(&ms, c->ev[3 + 2 * r], c->ev[4 + 2 * r]) == cudaSuccess) pair_ms += ms;
+  for (size_t i = 0; i < c->ev_pairs; ++i) {
+    if (cudaEventElapsedTime(&ms, c->ev[3 + 2 * i], c->ev[4 + 2 * i]) == cudaSuccess) pair_ms += ms;
   }
   s.pair_ms = pair_ms;
+  s.pair_launches = static_cast<int64_t>(c->ev_pairs);
 }
 
 // Analysis hook: copy the round's full entropy table to the host as a dense u x u matrix
@@ -589,10 +612,9 @@ int causal_order_impl(plg_ctx* c, const double* dX, int64_t ldx, int64_t n, int 
     const int u = d - r;
     int* act_cur = (r & 1) ? c->act1.p : c->act0.p;
     int* act_nxt = (r & 1) ? c->act0.p : c->act1.p;
-    const size_t evb = 3 + 2 * static_cast<size_t>(r);
     if (prune && r > 0 && u > plg::kSmallU) {
-      if (int rc = search_round_pruned(c, n, ldw, d, u, act_cur, r, evb, st)) return rc;
-    } else if (int rc = search_round(c, n, ldw, d, u, act_cur, r, evb, st, (prune && r == 0) ? c->KN.p : nullptr)) {
+      if (int rc = search_round_pruned(c, n, ldw, d, u, act_cur, r, st)) return rc;
+    } else if (int rc = search_round(c, n, ldw, d, u, act_cur, r, st, (prune && r == 0) ? c->KN.p : nullptr)) {
       return rc;
     }
     if (c->hook && c->world == 1)
@@ -628,6 +650,7 @@ int causal_order_impl(plg_ctx* c, const double* dX, int64_t ldx, int64_t n, int 
 int begin_call(plg_ctx* c, plg_status* st) {
   PLG_CUDA(cudaSetDevice(c->device));
   c->launches = 0;
+  c->ev_pairs = 0;
   c->last = plg_stats{};
   if (c->timing) {
     PLG_CUDA(c->events(3));
@@ -792,7 +815,7 @@ int plg_search(plg_ctx* c, const double* X, int64_t n, int32_t d, int64_t ld, co
   PLG_CUDA(cudaMemsetAsync(c->err.p, 0xff, sizeof(unsigned long long), c->stream));
   plg::launch_gram(c->W.p, ldw, n, u, c->C.p, u, c->gscr.p, c->stream);
   ++c->launches;
-  if (int rc = search_round(c, n, ldw, u, u, c->act0.p, 0, 3, st)) return rc;
+  if (int rc = search_round(c, n, ldw, u, u, c->act0.p, 0, st)) return rc;
   PLG_CUDA(c->scores.reserve(d));
   std::vector<double> ninf(d, -std::numeric_limits<double>::infinity());
   PLG_CUDA(cudaMemcpyAsync(c->scores.p, ninf.data(), d * sizeof(double), cudaMemcpyHostToDevice, c->stream));

@@ -546,6 +546,7 @@ PYBIND11_MODULE(_core, m) {
         d["pairs_evaluated"] = s.pairs_evaluated;
         d["ede"] = s.ede;
         d["launches"] = s.launches;
+        d["pair_launches"] = s.pair_launches;
         d["rounds"] = s.rounds;
         d["world"] = s.world;
         d["h2d_bytes"] = s.h2d_bytes;

@@ -144,7 +144,9 @@ struct PruneArgs {
   double* pk;                   // [u] predicted k (sum of KN over the active row)
   int* rowsel;                  // [u * u] selected partner positions of each row, ascending
   int* off;                     // [u + 1] per-row counts -> exclusive offsets, off[u] = total
-  double* part;                 // [2][nseg][batch][4] segment partial sums
+  double* part;                 // [nseg][batch][4] segment partial sums
+  int* work;                    // per-batch item counters (zeroed by the scan kernel)
+  int* done;                    // [batch / 32] per-chunk finished-segment counters (self-resetting)
   int batch;                    // pairs per batch of the list kernel
   int seg_len;
   int nseg;

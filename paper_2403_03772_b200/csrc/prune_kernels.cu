@@ -288,6 +288,7 @@ __global__ void __launch_bounds__(1024) prune_scan_kernel(const PruneArgs a) {
     a.off[a.u] = s_carry;
     atomicAdd(a.evals, static_cast<unsigned long long>(s_carry));
   }
+  for (int b = threadIdx.x; b <= s_carry / a.batch; b += blockDim.x) a.work[b] = 0;  // fetch counters
 }
 
 // ---- pairs: cooperative persistent evaluation of the list ----
@@ -311,6 +312,39 @@ __device__ __forceinline__ void ede2(double xa, double ya, double s1, double bs1
   ede_accumulate<kClampA>(fma(xa, -bs2, ya * s2), acc2, tp);
 }
 
+// Finalise one 32-pair chunk once all its sample segments are in: segments in ascending
+// order (finalize_kernel's order), both entropies, then M_pq and M_qp = -M_pq.
+__device__ __forceinline__ void finalize_chunk(const PruneArgs& a, const double* part, int base, int m, int chunk,
+                                               int lane) {
+  const int kk = chunk * 32 + lane;
+  if (kk >= m) return;
+  int p, q;
+  list_entry(a, base + kk, p, q);
+  double l1 = 0.0, p1 = 0.0, l2 = 0.0, p2 = 0.0;
+  const double2* src = reinterpret_cast<const double2*>(part + static_cast<int64_t>(kk) * 4);
+  const int64_t stride = static_cast<int64_t>(a.batch) * 2;  // double2 per segment
+  for (int s = 0; s < a.nseg; ++s) {
+    const double2 v1 = __ldcg(src);  // written by other SMs: bypass L1
+    const double2 v2 = __ldcg(src + 1);
+    l1 += v1.x;
+    p1 += v1.y;
+    l2 += v2.x;
+    p2 += v2.y;
+    src += stride;
+  }
+  const double inv_n = 1.0 / static_cast<double>(a.n);
+  const double e_pq = entropy_from_sums(l1, p1, inv_n);  // E(p | q)
+  const double e_qp = entropy_from_sums(l2, p2, inv_n);  // E(q | p)
+  // ordering.cpp:93-94 (kreduce_kernel's expression); M_qp = -M_pq exactly
+  const double mpq = (a.H[q] + e_pq) - (a.H[p] + e_qp);
+  a.Md[static_cast<int64_t>(p) * a.u + q] = mpq;
+  a.Md[static_cast<int64_t>(q) * a.u + p] = -mpq;
+}
+
+// Work items (chunk of 32 list entries, sample segment) are fetched dynamically, chunk-major;
+// the warp completing a chunk's last segment finalises it, so a batch needs no grid barrier.
+// Lists longer than one batch (part-buffer capacity) run batch after batch with a grid
+// barrier between them (the kernel is launched cooperatively).
 template <bool kClampA>
 __global__ void __launch_bounds__(kListThreads, 2) prune_pairs_kernel(const PruneArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -318,87 +352,72 @@ __global__ void __launch_bounds__(kListThreads, 2) prune_pairs_kernel(const Prun
   __syncthreads();
   cg::grid_group grid = cg::this_grid();
   const int lane = threadIdx.x & 31;
-  const int gwarp = static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-  const int nwarps = static_cast<int>((gridDim.x * blockDim.x) >> 5);
-  const int gthread = blockIdx.x * blockDim.x + threadIdx.x;
-  const int nthreads = gridDim.x * blockDim.x;
   const bool skip = (*a.err != kNoError);  // only skips work: every CTA still meets the barriers
   const TabPtr tp = table_ptrs(smem, lane);
   const int total = a.off[a.u];
   const int nbatch = (total + a.batch - 1) / a.batch;
-  const int64_t slab = static_cast<int64_t>(a.nseg) * a.batch * 4;
   for (int b = 0; b < nbatch; ++b) {
+    if (b > 0) grid.sync();  // every chunk of batch b - 1 is finalised: the part slab is free
     const int base = b * a.batch;
     const int m = min(a.batch, total - base);
     const int chunks = (m + 31) / 32;
     const int items = chunks * a.nseg;
-    double* part = a.part + (b & 1) * slab;
-    for (int it = gwarp; !skip && it < items; it += nwarps) {
-      const int seg = it / chunks;
-      const int kk = (it - seg * chunks) * 32 + lane;
-      if (kk >= m) continue;
-      int p, q;
-      list_entry(a, base + kk, p, q);
-      const int ci = a.act[p], cj = a.act[q];
-      double s1, bs1, s2, bs2;
-      pair_scales(a.C, a.ldc, ci, cj, s1, bs1, s2, bs2);  // collinear pairs: zeros (flagged by predict)
-      const double* wi = a.W + static_cast<int64_t>(ci) * a.ldw;
-      const double* wj = a.W + static_cast<int64_t>(cj) * a.ldw;
-      const int64_t t0 = static_cast<int64_t>(seg) * a.seg_len;  // multiple of 4: 32-byte aligned
-      const int64_t t1 = lmin(a.n, t0 + a.seg_len);
-      EdeAcc acc1, acc2;
-      int64_t t = t0;
-      if (t + 3 < t1) {
-        double2 xa = __ldg(reinterpret_cast<const double2*>(wi + t));
-        double2 xb = __ldg(reinterpret_cast<const double2*>(wi + t + 2));
-        double2 ya = __ldg(reinterpret_cast<const double2*>(wj + t));
-        double2 yb = __ldg(reinterpret_cast<const double2*>(wj + t + 2));
+    while (!skip) {
+      int it = 0;
+      if (lane == 0) it = atomicAdd(&a.work[b], 1);
+      it = __shfl_sync(0xffffffffu, it, 0);
+      if (it >= items) break;
+      const int chunk = it / a.nseg;
+      const int seg = it - chunk * a.nseg;
+      const int kk = chunk * 32 + lane;
+      if (kk < m) {
+        int p, q;
+        list_entry(a, base + kk, p, q);
+        const int ci = a.act[p], cj = a.act[q];
+        double s1, bs1, s2, bs2;
+        pair_scales(a.C, a.ldc, ci, cj, s1, bs1, s2, bs2);  // collinear pairs: zeros (flagged by predict)
+        const double* wi = a.W + static_cast<int64_t>(ci) * a.ldw;
+        const double* wj = a.W + static_cast<int64_t>(cj) * a.ldw;
+        const int64_t t0 = static_cast<int64_t>(seg) * a.seg_len;  // multiple of 4: 32-byte aligned
+        const int64_t t1 = lmin(a.n, t0 + a.seg_len);
+        EdeAcc acc1, acc2;
+        int64_t t = t0;
+        if (t + 3 < t1) {
+          double2 xa = __ldg(reinterpret_cast<const double2*>(wi + t));
+          double2 xb = __ldg(reinterpret_cast<const double2*>(wi + t + 2));
+          double2 ya = __ldg(reinterpret_cast<const double2*>(wj + t));
+          double2 yb = __ldg(reinterpret_cast<const double2*>(wj + t + 2));
 #pragma unroll 1
-        for (; t + 3 < t1; t += 4) {
-          const double2 cxa = xa, cxb = xb, cya = ya, cyb = yb;
-          if (t + 7 < t1) {  // prefetch the next 4 samples
-            xa = __ldg(reinterpret_cast<const double2*>(wi + t + 4));
-            xb = __ldg(reinterpret_cast<const double2*>(wi + t + 6));
-            ya = __ldg(reinterpret_cast<const double2*>(wj + t + 4));
-            yb = __ldg(reinterpret_cast<const double2*>(wj + t + 6));
+          for (; t + 3 < t1; t += 4) {
+            const double2 cxa = xa, cxb = xb, cya = ya, cyb = yb;
+            if (t + 7 < t1) {  // prefetch the next 4 samples
+              xa = __ldg(reinterpret_cast<const double2*>(wi + t + 4));
+              xb = __ldg(reinterpret_cast<const double2*>(wi + t + 6));
+              ya = __ldg(reinterpret_cast<const double2*>(wj + t + 4));
+              yb = __ldg(reinterpret_cast<const double2*>(wj + t + 6));
+            }
+            ede2<kClampA>(cxa.x, cya.x, s1, bs1, s2, bs2, acc1, acc2, tp);
+            ede2<kClampA>(cxa.y, cya.y, s1, bs1, s2, bs2, acc1, acc2, tp);
+            ede2<kClampA>(cxb.x, cyb.x, s1, bs1, s2, bs2, acc1, acc2, tp);
+            ede2<kClampA>(cxb.y, cyb.y, s1, bs1, s2, bs2, acc1, acc2, tp);
           }
-          ede2<kClampA>(cxa.x, cya.x, s1, bs1, s2, bs2, acc1, acc2, tp);
-          ede2<kClampA>(cxa.y, cya.y, s1, bs1, s2, bs2, acc1, acc2, tp);
-          ede2<kClampA>(cxb.x, cyb.x, s1, bs1, s2, bs2, acc1, acc2, tp);
-          ede2<kClampA>(cxb.y, cyb.y, s1, bs1, s2, bs2, acc1, acc2, tp);
         }
+        for (; t < t1; ++t) ede2<kClampA>(wi[t], wj[t], s1, bs1, s2, bs2, acc1, acc2, tp);
+        double2* dst = reinterpret_cast<double2*>(a.part + (static_cast<int64_t>(seg) * a.batch + kk) * 4);
+        __stcg(dst, make_double2(acc_lc(acc1), acc_pdf(acc1)));
+        __stcg(dst + 1, make_double2(acc_lc(acc2), acc_pdf(acc2)));
       }
-      for (; t < t1; ++t) ede2<kClampA>(wi[t], wj[t], s1, bs1, s2, bs2, acc1, acc2, tp);
-      double2* dst = reinterpret_cast<double2*>(part + (static_cast<int64_t>(seg) * a.batch + kk) * 4);
-      dst[0] = make_double2(acc_lc(acc1), acc_pdf(acc1));
-      dst[1] = make_double2(acc_lc(acc2), acc_pdf(acc2));
-    }
-    grid.sync();
-    // finalise batch b: segments in ascending order (finalize_kernel's order), then M
-    const double inv_n = 1.0 / static_cast<double>(a.n);
-    for (int kk = gthread; !skip && kk < m; kk += nthreads) {
-      int p, q;
-      list_entry(a, base + kk, p, q);
-      double l1 = 0.0, p1 = 0.0, l2 = 0.0, p2 = 0.0;
-      const double* src = part + static_cast<int64_t>(kk) * 4;
-      for (int s = 0; s < a.nseg; ++s) {
-        const double2 v1 = reinterpret_cast<const double2*>(src)[0];
-        const double2 v2 = reinterpret_cast<const double2*>(src)[1];
-        l1 += v1.x;
-        p1 += v1.y;
-        l2 += v2.x;
-        p2 += v2.y;
-        src += static_cast<int64_t>(a.batch) * 4;
+      __threadfence();  // release this segment's partials before counting it
+      __syncwarp();
+      int last = 0;
+      if (lane == 0) last = (atomicAdd(&a.done[chunk], 1) == a.nseg - 1);
+      last = __shfl_sync(0xffffffffu, last, 0);
+      if (last) {
+        __threadfence();  // acquire the other segments' partials
+        finalize_chunk(a, a.part, base, m, chunk, lane);
+        if (lane == 0) a.done[chunk] = 0;  // ready for the next batch / launch
       }
-      const double e_pq = entropy_from_sums(l1, p1, inv_n);  // E(p | q)
-      const double e_qp = entropy_from_sums(l2, p2, inv_n);  // E(q | p)
-      // ordering.cpp:93-94 (kreduce_kernel's expression); M_qp = -M_pq exactly
-      const double mpq = (a.H[q] + e_pq) - (a.H[p] + e_qp);
-      a.Md[static_cast<int64_t>(p) * a.u + q] = mpq;
-      a.Md[static_cast<int64_t>(q) * a.u + p] = -mpq;
     }
-    // part slab (b & 1) is rewritten by batch b + 2 only after the barrier of batch b + 1,
-    // which every CTA reaches after finishing this finalisation
   }
 }
 
