@@ -142,8 +142,16 @@ SegPlan seg_plan(int u, int64_t n) {
 
 // Segmentation of a pruned round: fine (256-sample) segments so that even a short pair list
 // spreads over every SM; at most 64 segments. Pure function of n.
+int64_t prune_seg_min() {
+  static const int64_t v = [] {
+    const char* e = std::getenv("PLG_PRUNE_SEGLEN");  // tuning knob (multiple of 4)
+    const int64_t x = e ? std::atoll(e) : 256;
+    return x >= 16 ? x / 4 * 4 : int64_t{256};
+  }();
+  return v;
+}
 SegPlan prune_seg_plan(int64_t n) {
-  const int64_t seg_len = std::max<int64_t>(256, round_up((n + 63) / 64, 4));
+  const int64_t seg_len = std::max<int64_t>(prune_seg_min(), round_up((n + 127) / 128, 4));
   return {static_cast<int>((n + seg_len - 1) / seg_len), static_cast<int>(seg_len)};
 }
 constexpr int kPruneBatch = 131072;  // pairs per batch of the list kernel (part-buffer capacity)
@@ -161,7 +169,7 @@ struct plg_ctx {
   double* g_exp = nullptr;
   double2* g_log = nullptr;
 
-  DevBuf<double> Xd, W, C, part, epack, H, k, scores, msd, gscr, rk;
+  DevBuf<double> Xd, W, C, part, epack, H, k, scores, msd, gscr, rk, hpart;
   DevBuf<int> act0, act1, colvar, order, stat, idx, nz;
   DevBuf<plg::RoundState> rs;
   DevBuf<unsigned long long> err, errs;
@@ -174,9 +182,9 @@ struct plg_ctx {
 
   // exact pruned rounds of causal_order (prune_kernels.cu); PLG_PRUNE="R:T:f1,f2,..." or "0"
   bool prune = true;
-  int prune_R = 8;
-  int prune_T = 3;
-  std::vector<double> prune_fracs{0.05, 0.15};
+  int prune_R = 4;
+  int prune_T = 2;
+  std::vector<double> prune_fracs{0.02, 0.05, 0.12, 0.25};
   bool prune_tile_seg = false;  // PLG_PRUNE_TILESEG=1: the exhaustive rounds' segmentation (bit-identity tests)
   DevBuf<double> Md, KN, pk, L, ppart;
   DevBuf<int> st0, st1, rowsel, off, pwork, pdone;
@@ -252,7 +260,7 @@ void parse_prune_env(plg_ctx* ctx) {
           char* end = nullptr;
           const double x = strtod(f, &end);
           if (end == f) break;
-          if (x > 0.0 && x < 1.0) ctx->prune_fracs.push_back(x);
+          if (x > 0.0) ctx->prune_fracs.push_back(x);
           f = (*end == ',') ? end + 1 : end;
         }
       }
@@ -326,12 +334,23 @@ size_t part_doubles(const RoundPlan& rp, int u) {
 }
 
 // One search round over the active list act_cur (u >= 2): H, pairs, exchange, k.
-int search_round(plg_ctx* c, int64_t n, int64_t ldw, int ldc, int u, const int* act_cur,
-                 int round, plg_status* st, double* KN = nullptr) {
-  const RoundPlan rp = plan_round(u, n, c->rank, c->world);
-  plg::launch_colent(c->W.p, ldw, n, c->C.p, ldc, act_cur, u, c->H.p, c->g_exp, c->g_log, c->nz.p,
-                     c->colvar.p, round, c->err.p, c->stream);
+// Column entropies of the round: from the fused residualisation's chunk sums (rounds >= 1 of
+// causal_order) or computed directly (round 0, search).
+void round_entropies(plg_ctx* c, int64_t n, int64_t ldw, int ldc, int u, const int* act_cur, int round,
+                     bool from_resid) {
+  if (from_resid)
+    plg::launch_hfin(c->hpart.p, n, c->C.p, ldc, act_cur, u, c->H.p, c->nz.p, c->colvar.p, round, c->err.p,
+                     c->stream);
+  else
+    plg::launch_colent(c->W.p, ldw, n, c->C.p, ldc, act_cur, u, c->H.p, c->g_exp, c->g_log, c->nz.p,
+                       c->colvar.p, round, c->err.p, c->stream);
   ++c->launches;
+}
+
+int search_round(plg_ctx* c, int64_t n, int64_t ldw, int ldc, int u, const int* act_cur,
+                 int round, plg_status* st, double* KN = nullptr, bool h_from_resid = false) {
+  const RoundPlan rp = plan_round(u, n, c->rank, c->world);
+  round_entropies(c, n, ldw, ldc, u, act_cur, round, h_from_resid);
   plg::PairLaunch a;
   a.W = c->W.p;
   a.ldw = ldw;
@@ -389,9 +408,7 @@ int search_round(plg_ctx* c, int64_t n, int64_t ldw, int ldc, int u, const int* 
 // earlier round of the same run.
 int search_round_pruned(plg_ctx* c, int64_t n, int64_t ldw, int d, int u, const int* act_cur, int round,
                         plg_status* st) {
-  plg::launch_colent(c->W.p, ldw, n, c->C.p, d, act_cur, u, c->H.p, c->g_exp, c->g_log, c->nz.p,
-                     c->colvar.p, round, c->err.p, c->stream);
-  ++c->launches;
+  round_entropies(c, n, ldw, d, u, act_cur, round, true);
   const SegPlan sp = c->prune_tile_seg ? seg_plan(u, n) : prune_seg_plan(n);
   PLG_CUDA(cudaMemsetAsync(c->Md.p, 0xff, static_cast<size_t>(u) * u * sizeof(double), c->stream));
   plg::PruneArgs a{};
@@ -430,22 +447,37 @@ int search_round_pruned(plg_ctx* c, int64_t n, int64_t ldw, int d, int u, const 
   plg::launch_prune_predict(a, c->stream);
   plg::launch_prune_top(a, c->prune_R, c->stream);
   c->launches += 2;
-  auto stage = [&](int kind, int m, bool final_pass) {
+  int stage_idx = 0;
+  auto stage = [&](int kind, int m, double beta, int pass) {
+    a.stage_idx = std::min(stage_idx++, plg::kMaxPruneStages - 1);
     a.state_in = sa;
     a.state_out = sb;
-    plg::launch_prune_select(a, kind, m, c->stream);
+    plg::launch_prune_select(a, kind, m, beta, c->stream);
     plg::launch_prune_scan(a, c->stream);
     const size_t tm = pair_timer_begin(c);
     plg::launch_prune_pairs(a, c->stream);
     pair_timer_end(c, tm);
     std::swap(sa, sb);
     a.state_in = sa;
-    plg::launch_prune_bound(a, final_pass, c->stream);
-    c->launches += 4;
+    c->launches += 3;
+    if (pass != 1) {  // refinement stages: the next selection computes each row's partial k
+      plg::launch_prune_bound(a, pass, c->stream);
+      ++c->launches;
+    }
   };
-  stage(plg::kStageProbe, c->prune_T, false);
-  for (double f : c->prune_fracs) stage(plg::kStageRefine, std::max(1, static_cast<int>(f * u)), false);
-  stage(plg::kStageFull, 0, true);
+  stage(plg::kStageProbe, c->prune_T, 0.0, 0);
+  // refinement ladder: values < 1 are cumulative fractions of the row (count mode: the step
+  // to the next fraction), values >= 1 deficit multipliers (prune_kernels.cu select)
+  double prev = 0.0;
+  for (double f : c->prune_fracs) {
+    if (f >= 1.0) {
+      stage(plg::kStageRefine, 0, f, 1);
+    } else {
+      stage(plg::kStageRefine, std::max(1, static_cast<int>((f - prev) * u)), 0.0, 1);
+      prev = f;
+    }
+  }
+  stage(plg::kStageFull, 0, 0.0, 2);
   return 0;
 }
 
@@ -465,6 +497,7 @@ int reserve_run(plg_ctx* c, int64_t n, int ncols, int64_t ldw, plg_status* st) {
   PLG_CUDA(c->H.reserve(ncols));
   PLG_CUDA(c->k.reserve(ncols));
   PLG_CUDA(c->rk.reserve(ncols));
+  PLG_CUDA(c->hpart.reserve(static_cast<size_t>(ncols) * plg::resid_chunks(n) * 2));
   PLG_CUDA(c->scores.reserve(ncols));
   PLG_CUDA(c->act0.reserve(ncols));
   PLG_CUDA(c->act1.reserve(ncols));
@@ -493,13 +526,13 @@ int reserve_prune(plg_ctx* c, int64_t n, int d, plg_status* st) {
   PLG_CUDA(c->st0.reserve(d));
   PLG_CUDA(c->st1.reserve(d));
   PLG_CUDA(c->kstar.reserve(1));
-  PLG_CUDA(c->evals.reserve(1));
+  PLG_CUDA(c->evals.reserve(1 + plg::kMaxPruneStages));
   PLG_CUDA(c->ppart.reserve(nseg * kPruneBatch * 4));
   const size_t max_list = dd + d;  // per-stage list bound: u (u - 1) entries + slack
   PLG_CUDA(c->pwork.reserve(max_list / kPruneBatch + 2));
   PLG_CUDA(c->pdone.reserve(kPruneBatch / 32));
   PLG_CUDA(cudaMemsetAsync(c->pdone.p, 0, (kPruneBatch / 32) * sizeof(int), c->stream));
-  PLG_CUDA(cudaMemsetAsync(c->evals.p, 0, sizeof(unsigned long long), c->stream));
+  PLG_CUDA(cudaMemsetAsync(c->evals.p, 0, (1 + plg::kMaxPruneStages) * sizeof(unsigned long long), c->stream));
   return 0;
 }
 
@@ -614,7 +647,8 @@ int causal_order_impl(plg_ctx* c, const double* dX, int64_t ldx, int64_t n, int 
     int* act_nxt = (r & 1) ? c->act0.p : c->act1.p;
     if (prune && r > 0 && u > plg::kSmallU) {
       if (int rc = search_round_pruned(c, n, ldw, d, u, act_cur, r, st)) return rc;
-    } else if (int rc = search_round(c, n, ldw, d, u, act_cur, r, st, (prune && r == 0) ? c->KN.p : nullptr)) {
+    } else if (int rc = search_round(c, n, ldw, d, u, act_cur, r, st, (prune && r == 0) ? c->KN.p : nullptr,
+                                     r > 0)) {
       return rc;
     }
     if (c->hook && c->world == 1)
@@ -625,23 +659,31 @@ int causal_order_impl(plg_ctx* c, const double* dX, int64_t ldx, int64_t n, int 
     if (u - 1 >= 2 || (u - 1 == 1 && max_rounds >= 0)) {
       // the next round's build_cache check only exists when it has >= 2 candidates
       plg::launch_update_gram(c->C.p, d, act_nxt, u - 1, c->rs.p, c->err.p, c->stream);
-      plg::launch_residualize(c->W.p, ldw, n, c->C.p, d, act_nxt, u - 1, c->rs.p, c->nz.p, r + 1,
-                              c->err.p, c->stream);
+      plg::launch_resid_ent(c->W.p, ldw, n, c->C.p, d, act_nxt, u - 1, c->rs.p, c->nz.p, r + 1, c->err.p,
+                            c->hpart.p, c->g_exp, c->g_log, c->stream);
       c->launches += 2;
     }
   }
   if (c->timing) cudaEventRecord(c->ev[1], c->stream);
-  unsigned long long key = 0, pruned_pairs = 0;
+  unsigned long long key = 0, pruned_pairs = 0, per_stage[1 + plg::kMaxPruneStages] = {};
   PLG_CUDA(cudaMemcpyAsync(&key, c->err.p, sizeof(key), cudaMemcpyDeviceToHost, c->stream));
   if (prune)
-    PLG_CUDA(cudaMemcpyAsync(&pruned_pairs, c->evals.p, sizeof(pruned_pairs), cudaMemcpyDeviceToHost, c->stream));
+    PLG_CUDA(cudaMemcpyAsync(per_stage, c->evals.p, sizeof(per_stage), cudaMemcpyDeviceToHost, c->stream));
   const int nout = (rounds == d - 1) ? d : rounds;
   PLG_CUDA(cudaMemcpyAsync(order_out, c->order.p, nout * sizeof(int32_t), cudaMemcpyDeviceToHost,
                            c->stream));
   PLG_CUDA(cudaStreamSynchronize(c->stream));
   PLG_CUDA(cudaGetLastError());
   finish_stats(c, n, d, rounds, host_in);
+  pruned_pairs = per_stage[0];
   c->last.pairs_evaluated = c->pairs_done + static_cast<int64_t>(pruned_pairs);
+  if (prune && std::getenv("PLG_PRUNE_DEBUG")) {
+    std::fprintf(stderr, "[plg prune] R=%d T=%d stages:", c->prune_R, c->prune_T);
+    for (int i = 0; i < 2 + static_cast<int>(c->prune_fracs.size()) && i < plg::kMaxPruneStages; ++i)
+      std::fprintf(stderr, " %llu", per_stage[1 + i]);
+    std::fprintf(stderr, " exhaustive-rounds %lld total %lld\n", static_cast<long long>(c->pairs_done),
+                 static_cast<long long>(c->last.pairs_evaluated));
+  }
   c->last.d2h_bytes = nout * sizeof(int32_t);
   if (key != plg::kNoError) return report_error(key, nullptr, st);
   return ok(st);

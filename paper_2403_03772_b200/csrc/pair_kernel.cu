@@ -394,6 +394,88 @@ __global__ void __launch_bounds__(kColentThreads)
   }
 }
 
+// Residualisation fused with the next round's column entropies: w_r <- w_r - (C_rm / C_mm) w_m
+// in place (residualize_kernel's arithmetic) and, from the new values already in registers,
+// the entropy sums of w_r / sqrt(C_rr) (C after the rank-1 update) per sample chunk:
+// hpart[(r * nch + c) * 2] = {sum lc, sum pdf}. hfin_kernel adds the chunks in ascending
+// order next round. Persistent CTAs so the tables are staged once per CTA, not per column.
+constexpr int kResidThreads = 256;
+__global__ void __launch_bounds__(kResidThreads)
+    resid_ent_kernel(double* W, int64_t ldw, int64_t n, const double* C, int64_t ldc, const int* act_nxt,
+                     int ur, const RoundState* rs, int* nz, int tag, const unsigned long long* err,
+                     int64_t chunk, int nch, double* hpart, const double* g_exp, const double2* g_log) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ double s_red[2][kResidThreads / 32];
+  if (*err != kNoError) return;
+  load_tables(smem, g_exp, g_log);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const TabPtr tp = table_ptrs(smem, lane);
+  const int m = rs->chosen_col;
+  const double cmm = C[static_cast<int64_t>(m) * ldc + m];
+  const double2* wm = reinterpret_cast<const double2*>(W + static_cast<int64_t>(m) * ldw);
+  const int items = ur * nch;
+  for (int it = blockIdx.x; it < items; it += gridDim.x) {
+    const int pos = it / nch, c = it - pos * nch;
+    const int r = act_nxt[pos];
+    const double beta = C[static_cast<int64_t>(r) * ldc + m] / cmm;
+    const double su = kUScale / sqrt(C[static_cast<int64_t>(r) * ldc + r]);
+    double2* wr = reinterpret_cast<double2*>(W + static_cast<int64_t>(r) * ldw);
+    const int64_t t0 = c * chunk, t1 = lmin(n, t0 + chunk);  // samples; chunk is even
+    EdeAcc acc;
+    bool any = false;
+    for (int64_t t = t0 + 2 * threadIdx.x; t < t1; t += 2 * kResidThreads) {
+      const double2 x = wr[t >> 1];
+      const double2 y = wm[t >> 1];
+      const double2 o = make_double2(__dsub_rn(x.x, __dmul_rn(beta, y.x)), __dsub_rn(x.y, __dmul_rn(beta, y.y)));
+      wr[t >> 1] = o;
+      any |= (o.x != 0.0) | (o.y != 0.0);
+      ede_accumulate<true>(o.x * su, acc, tp);
+      if (t + 1 < t1) ede_accumulate<true>(o.y * su, acc, tp);
+    }
+    if (__any_sync(0xffffffffu, any) && lane == 0) nz[r] = tag;
+    double lc = acc_lc(acc), pd = acc_pdf(acc);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      lc += __shfl_xor_sync(0xffffffffu, lc, o);
+      pd += __shfl_xor_sync(0xffffffffu, pd, o);
+    }
+    if (lane == 0) {
+      s_red[0][warp] = lc;
+      s_red[1][warp] = pd;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double l = 0.0, q = 0.0;
+      for (int w2 = 0; w2 < kResidThreads / 32; ++w2) {
+        l += s_red[0][w2];
+        q += s_red[1][w2];
+      }
+      hpart[static_cast<int64_t>(it) * 2] = l;
+      hpart[static_cast<int64_t>(it) * 2 + 1] = q;
+    }
+    __syncthreads();
+  }
+}
+
+// H[p] from resid_ent_kernel's chunk sums (ascending chunks), plus build_cache's
+// ZeroVariance(col) check of the round (ordering.cpp:56-62), as colent_kernel does.
+__global__ void hfin_kernel(const double* hpart, int nch, int64_t n, const double* C, int64_t ldc, const int* act,
+                            int u, double* H, const int* nz, const int* col_var, int round,
+                            unsigned long long* err) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= u) return;
+  const int col = act[p];
+  const double ccc = C[static_cast<int64_t>(col) * ldc + col];
+  if (nz[col] != round || !(ccc > 0.0)) atomicMin(err, err_key(round, kErrColZeroVar, col_var[col]));
+  double l = 0.0, q = 0.0;
+  for (int c = 0; c < nch; ++c) {
+    l += hpart[(static_cast<int64_t>(p) * nch + c) * 2];
+    q += hpart[(static_cast<int64_t>(p) * nch + c) * 2 + 1];
+  }
+  H[p] = entropy_from_sums(l, q, 1.0 / static_cast<double>(n));
+}
+
 // entropy_approx(u * scale) of one vector (kernels.cpp:123-148), fixed-shape reduction.
 __global__ void __launch_bounds__(kColentThreads)
     entropy_vec_kernel(const double* u, int64_t n, double scale, double* out, const double* g_exp,
@@ -523,6 +605,32 @@ void launch_colent(const double* W, int64_t ldw, int64_t n, const double* C, int
   const int grid = u < 4 * 148 ? u : 4 * 148;
   colent_kernel<<<grid, kColentThreads, kTableBytes, s>>>(W, ldw, n, C, ldc, act, u, H, g_exp,
                                                           g_log, nz, col_var, round, err);
+}
+
+int resid_chunks(int64_t n) { return static_cast<int>((n + kResidChunk - 1) / kResidChunk); }
+
+void launch_resid_ent(double* W, int64_t ldw, int64_t n, const double* C, int64_t ldc, const int* act_nxt, int ur,
+                      const RoundState* rs, int* nz, int tag, const unsigned long long* err, double* hpart,
+                      const double* g_exp, const double2* g_log, cudaStream_t s) {
+  static int grid = 0;
+  if (!grid) {
+    cudaFuncSetAttribute(resid_ent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTableBytes);
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, resid_ent_kernel, kResidThreads, kTableBytes);
+    grid = sms * (per > 0 ? per : 1);
+  }
+  const int nch = resid_chunks(n);
+  const int g = ur * nch < grid ? ur * nch : grid;
+  resid_ent_kernel<<<g, kResidThreads, kTableBytes, s>>>(W, ldw, n, C, ldc, act_nxt, ur, rs, nz, tag, err,
+                                                        kResidChunk, nch, hpart, g_exp, g_log);
+}
+
+void launch_hfin(const double* hpart, int64_t n, const double* C, int64_t ldc, const int* act, int u, double* H,
+                 const int* nz, const int* col_var, int round, unsigned long long* err, cudaStream_t s) {
+  hfin_kernel<<<(u + 127) / 128, 128, 0, s>>>(hpart, resid_chunks(n), n, C, ldc, act, u, H, nz, col_var, round,
+                                              err);
 }
 
 void launch_entropy_vec(const double* u, int64_t n, double scale, double* out, const double* g_exp,

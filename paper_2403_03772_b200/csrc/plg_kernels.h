@@ -79,6 +79,17 @@ void launch_colent(const double* W, int64_t ldw, int64_t n, const double* C, int
                    const int* nz, const int* col_var, int round, unsigned long long* err,
                    cudaStream_t s);
 
+// Residualisation (as launch_residualize) fused with the next round's column-entropy sums per
+// chunk of kResidChunk samples (hpart: [ur][resid_chunks(n)][2]); launch_hfin turns them into
+// H (and runs colent's zero-variance check). Rounds >= 1 of causal_order use this pair.
+constexpr int64_t kResidChunk = 2048;
+int resid_chunks(int64_t n);
+void launch_resid_ent(double* W, int64_t ldw, int64_t n, const double* C, int64_t ldc, const int* act_nxt, int ur,
+                      const RoundState* rs, int* nz, int tag, const unsigned long long* err, double* hpart,
+                      const double* g_exp, const double2* g_log, cudaStream_t s);
+void launch_hfin(const double* hpart, int64_t n, const double* C, int64_t ldc, const int* act, int u, double* H,
+                 const int* nz, const int* col_var, int round, unsigned long long* err, cudaStream_t s);
+
 // Validation + round-0 standardisation with the reference's left-to-right sums
 // (types.cpp:21-47, kernels.cpp:44-57,92-104). col_map[c] = source column of local c.
 // stat[c] = {first non-finite row or -1, zero-variance flag}.
@@ -155,18 +166,22 @@ struct PruneArgs {
   unsigned long long* err;
   int round;
   double* k;                    // [u] exact k of alive/top rows, +inf for pruned rows
-  unsigned long long* evals;    // running count of list entries evaluated (statistics)
+  unsigned long long* evals;    // [1 + stages] list entries evaluated: total, per stage index
+  int stage_idx;
 };
 enum PruneStage : int { kStageProbe = 0, kStageRefine = 1, kStageFull = 2 };
 void launch_prune_predict(const PruneArgs& a, cudaStream_t s);
 void launch_prune_top(const PruneArgs& a, int R, cudaStream_t s);
-// m: partners per row (probe: suspects per non-top row; refine: top-m predicted)
-void launch_prune_select(const PruneArgs& a, int stage, int m, cudaStream_t s);
+// m: partners per row (probe: suspects per non-top row; refine: top-m predicted);
+// beta > 0 (refine): deficit mode — predicted contributions reaching beta x the row's deficit
+void launch_prune_select(const PruneArgs& a, int stage, int m, double beta, cudaStream_t s);
 void launch_prune_scan(const PruneArgs& a, cudaStream_t s);
 void launch_prune_pairs(const PruneArgs& a, cudaStream_t s);
-// final: k[] and KN of the evaluated pairs, else L[] and k* over the top rows
-void launch_prune_bound(const PruneArgs& a, bool final_pass, cudaStream_t s);
+// pass 0: every row's partial k L[] and k* over the top rows; 1: alive rows' L[]; 2: exact k[]
+// of the top and alive rows (+inf for pruned rows)
+void launch_prune_bound(const PruneArgs& a, int pass, cudaStream_t s);
 int prune_pairs_grid();  // co-resident CTAs of the cooperative list kernel
+constexpr int kMaxPruneStages = 8;
 
 // argmin over k (lowest position on ties), order/score bookkeeping, active-list compaction;
 // round_k (optional): the winning k of each round.

@@ -58,15 +58,34 @@ __global__ void __launch_bounds__(256) prune_predict_kernel(const PruneArgs a) {
   if (p >= a.u) return;
   const int vp = a.act[p];
   const double* kn = a.KN + static_cast<int64_t>(vp) * a.d;
+  const double* crow = a.C + static_cast<int64_t>(vp) * a.ldc;
+  const double cii = crow[vp];
   double acc = 0.0;
   bool collinear = false;
-  for (int q = lane; q < a.u; q += 32) {
-    if (q == p) continue;
-    const int vq = a.act[q];
-    acc += kn[vq];
-    if (q > p) {  // the exhaustive round checks every pair (pair_kernel.cu pair_params)
-      double s1, bs1, s2, bs2;
-      collinear |= !pair_scales(a.C, a.ldc, vp, vq, s1, bs1, s2, bs2);
+  for (int q0 = lane; q0 < a.u; q0 += 128) {
+    int vq[4];
+    double kv[4], cjj[4], cij[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {  // independent loads first
+      const int q = q0 + 32 * j;
+      vq[j] = q < a.u ? a.act[q] : vp;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      kv[j] = kn[vq[j]];
+      cjj[j] = a.C[static_cast<int64_t>(vq[j]) * a.ldc + vq[j]];
+      cij[j] = crow[vq[j]];
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int q = q0 + 32 * j;
+      if (q >= a.u) continue;
+      acc += (q == p) ? 0.0 : kv[j];
+      if (q > p) {  // pair_scales' test: the exhaustive round checks every pair
+        double b1, v1, b2, v2;
+        pair_vars(cii, cjj[j], cij[j], b1, v1, b2, v2);
+        collinear |= pair_collinear(v1, v2);
+      }
     }
   }
 #pragma unroll
@@ -80,54 +99,70 @@ __global__ void __launch_bounds__(256) prune_predict_kernel(const PruneArgs a) {
 }
 
 // ---- top: the R rows with the lowest pk (ties: lowest position) become full rows ----
-constexpr int kTopThreads = 1024;
-__global__ void __launch_bounds__(kTopThreads) prune_top_kernel(const PruneArgs a, int R) {
-  __shared__ double sv[kTopThreads / 32];
-  __shared__ int sp[kTopThreads / 32];
-  __shared__ int chosen;
-  int* state = a.state_out;
-  if (threadIdx.x == 0) *a.kstar = kInfBits;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int r = 0; r < R && r < a.u; ++r) {
-    double best = 0.0;
-    int bp = -1;
-    for (int p = threadIdx.x; p < a.u; p += kTopThreads) {
-      if (state[p] != 1) continue;
-      const double v = a.pk[p];
-      if (bp < 0 || v < best) {
-        best = v;
-        bp = p;
-      }
-    }
+// Each warp keeps its lanes' best R (insertion) and merges them by shuffles; warp 0 merges
+// the warps' lists. Two block barriers in all.
+constexpr int kTopThreads = 256;
+constexpr int kMaxR = 16;
+
+__device__ __forceinline__ bool pk_better(double v1, int p1, double v2, int p2) {
+  return p2 < 0 || (p1 >= 0 && (v1 < v2 || (v1 == v2 && p1 < p2)));
+}
+
+// Merge the lanes' sorted lists (length kMaxR, first R used) into the warp's best R, in order.
+__device__ __forceinline__ void warp_merge_best(double (&bv)[kMaxR], int (&bp)[kMaxR], int R, double* ov, int* op) {
+  const int lane = threadIdx.x & 31;
+  for (int r = 0; r < R; ++r) {
+    double v = bv[0];
+    int p = bp[0];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-      const double ov = __shfl_xor_sync(0xffffffffu, best, o);
-      const int op = __shfl_xor_sync(0xffffffffu, bp, o);
-      if (op >= 0 && (bp < 0 || ov < best || (ov == best && op < bp))) {
-        best = ov;
-        bp = op;
-      }
+      const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+      const int p2 = __shfl_xor_sync(0xffffffffu, p, o);
+      if (pk_better(v2, p2, v, p)) v = v2, p = p2;
     }
-    if (lane == 0) {
-      sv[warp] = best;
-      sp[warp] = bp;
+    if (lane == 0) ov[r] = v, op[r] = p;
+    if (p >= 0 && bp[0] == p) {
+#pragma unroll
+      for (int i = 0; i + 1 < kMaxR; ++i) bv[i] = bv[i + 1], bp[i] = bp[i + 1];
+      bp[kMaxR - 1] = -1;
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double b = 0.0;
-      int c = -1;
-      for (int w = 0; w < kTopThreads / 32; ++w) {
-        if (sp[w] >= 0 && (c < 0 || sv[w] < b || (sv[w] == b && sp[w] < c))) {
-          b = sv[w];
-          c = sp[w];
-        }
-      }
-      chosen = c;
-      if (c >= 0) state[c] = 2;
-    }
-    __syncthreads();
-    if (chosen < 0) break;
   }
+}
+
+__device__ __forceinline__ void insert_best(double (&bv)[kMaxR], int (&bp)[kMaxR], int R, double v, int p) {
+#pragma unroll
+  for (int i = 0; i < kMaxR; ++i) {
+    if (i < R && pk_better(v, p, bv[i], bp[i])) {
+      const double tv = bv[i];
+      const int tp = bp[i];
+      bv[i] = v, bp[i] = p;
+      v = tv, p = tp;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kTopThreads) prune_top_kernel(const PruneArgs a, int R) {
+  __shared__ double sv[kTopThreads / 32][kMaxR];
+  __shared__ int sp[kTopThreads / 32][kMaxR];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) *a.kstar = kInfBits;
+  double bv[kMaxR];
+  int bp[kMaxR];
+#pragma unroll
+  for (int i = 0; i < kMaxR; ++i) bv[i] = 0.0, bp[i] = -1;
+  for (int p = threadIdx.x; p < a.u; p += kTopThreads) insert_best(bv, bp, R, a.pk[p], p);
+  warp_merge_best(bv, bp, R, sv[warp], sp[warp]);
+  __syncthreads();
+  if (warp != 0) return;
+#pragma unroll
+  for (int i = 0; i < kMaxR; ++i) bv[i] = 0.0, bp[i] = -1;
+  for (int w = lane; w < kTopThreads / 32; w += 32)
+    for (int r = 0; r < R; ++r) insert_best(bv, bp, R, sv[w][r], sp[w][r]);
+  __shared__ double fv[kMaxR];
+  __shared__ int fp[kMaxR];
+  warp_merge_best(bv, bp, R, fv, fp);
+  __syncwarp();
+  if (lane < R && fp[lane] >= 0) a.state_out[fp[lane]] = 2;
 }
 
 // ---- select: each row's partners for one stage, ascending, into rowsel[p * u + i] ----
@@ -157,64 +192,112 @@ __device__ __forceinline__ int block_prefix(bool pred, int* s_warp, int& excl) {
   return total;
 }
 
-__global__ void __launch_bounds__(kSelThreads) prune_select_kernel(const PruneArgs a, int stage, int m) {
+// Refinement selection, two modes. Count mode (beta <= 0): the m partners with the largest
+// predicted contribution. Deficit mode (beta > 0): partners in descending predicted
+// contribution until their predicted sum reaches beta (thr - L_p), the amount the row's
+// partial k still lacks to be pruned; if all its predictions together fall short, every
+// remaining partner (the row is a contender and needs its exact k anyway). Selection works
+// on exponent bins of the predicted value (2^k granularity) with fixed-point weights, so it
+// is deterministic; inside the boundary bin partners are taken in ascending position.
+__global__ void __launch_bounds__(kSelThreads) prune_select_kernel(const PruneArgs a, int stage, int m,
+                                                                   double beta) {
   __shared__ int hist[kBins];
+  __shared__ unsigned long long wt[kBins];
   __shared__ int s_warp[kSelThreads / 32];
   __shared__ int s_cut[2];  // boundary bin, entries of it to take
+  __shared__ double s_red[kSelThreads / 32];
   const int p = blockIdx.x;
   const int u = a.u;
   const int st = a.state_in[p];
   const double thr = (stage == kStageProbe) ? 0.0 : kstar_threshold(a);
-  auto alive_now = [&](int r) { return a.state_in[r] == 1 && a.L[r] <= thr; };
+  const double* md = a.Md + static_cast<int64_t>(p) * u;
+  // Refinement / full stages: the row's partial k over its evaluated partners (a lower bound
+  // of its k whatever the summation order; fixed block shape, so deterministic).
+  double Lp = 0.0;
+  if (stage != kStageProbe && st == 1) {
+    double acc = 0.0;
+    for (int q = threadIdx.x; q < u; q += kSelThreads) {
+      const double mi = md[q];
+      if (q != p && is_eval(mi)) {
+        const double c = (mi < 0.0) ? mi : 0.0;
+        acc = __dadd_rn(acc, __dmul_rn(c, c));
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    for (int w = 0; w < kSelThreads / 32; ++w) Lp += s_red[w];
+  }
   bool active = false, full = false;
   if (stage == kStageProbe) {
     active = true;
     full = (st == 2);
   } else {
-    active = alive_now(p);
+    active = (st == 1 && Lp <= thr);
     full = (stage == kStageFull);
   }
   if (threadIdx.x == 0) {
     a.state_out[p] = (st == 1 && stage != kStageProbe && !active) ? 0 : st;
+    if (stage != kStageProbe) a.L[p] = Lp;
     if (!active) a.off[p] = 0;
   }
   if (!active) return;
-  const double* md = a.Md + static_cast<int64_t>(p) * u;
   const double* kn = a.KN + static_cast<int64_t>(a.act[p]) * a.d;
+  // A pair of two full rows is listed twice in the full stage (both rows are still alive,
+  // rare); its two evaluations have identical bits and the same writes.
   auto eligible = [&](int q) -> bool {
     if (q == p || is_eval(md[q])) return false;
     if (stage == kStageProbe) return full ? !(a.state_in[q] == 2 && q < p) : a.state_in[q] != 2;
-    if (stage == kStageFull) return !(q < p && alive_now(q));  // the pair is row q's
     return true;
   };
+  const bool deficit = beta > 0.0;
+  constexpr double kOne = 16777216.0;  // fixed-point unit of the deficit target (2^24)
+  const double target = fmax(beta * (thr - Lp), thr * 1e-6);
+  const double wscale = deficit ? kOne / target : 0.0;
+  const unsigned long long need_total = deficit ? static_cast<unsigned long long>(kOne)
+                                                : static_cast<unsigned long long>(m);
   int cut_bin = -1, cut_take = 0;  // full: every eligible partner
   if (!full) {
-    for (int i = threadIdx.x; i < kBins; i += kSelThreads) hist[i] = 0;
+    for (int i = threadIdx.x; i < kBins; i += kSelThreads) hist[i] = 0, wt[i] = 0ull;
     __syncthreads();
-    for (int q = threadIdx.x; q < u; q += kSelThreads)
-      if (eligible(q)) atomicAdd(&hist[key_bin(kn[a.act[q]])], 1);
+    for (int q0 = 0; q0 < u; q0 += kSelThreads) {  // warp-aggregated bin increments
+      const int q = q0 + threadIdx.x;
+      const bool e = q < u && eligible(q);
+      const double v = e ? kn[a.act[q]] : 0.0;
+      const int b = e ? key_bin(v) : -1;
+      const unsigned grp = __match_any_sync(0xffffffffu, b);
+      const int leader = __ffs(grp) - 1;
+      if (e && (threadIdx.x & 31) == leader) atomicAdd(&hist[b], __popc(grp));
+      if (deficit && e) atomicAdd(&wt[b], static_cast<unsigned long long>(fmin(v * wscale, 1099511627776.0)));
+    }
     __syncthreads();
-    if (threadIdx.x < 32) {  // suffix scan from the top bin: the bin where the count reaches m
+    if (!deficit)
+      for (int i = threadIdx.x; i < kBins; i += kSelThreads) wt[i] = static_cast<unsigned long long>(hist[i]);
+    __syncthreads();
+    if (threadIdx.x < 32) {  // suffix scan from the top bin: the bin where the weight reaches need
       const int lane = threadIdx.x;
       constexpr int per = (kBins + 31) / 32;
       const int hi = kBins - 1 - lane * per;  // lane covers bins (hi - per, hi]
-      int own = 0;
-      for (int b = hi; b > hi - per && b >= 0; --b) own += hist[b];
-      int incl = own;  // inclusive prefix over lanes = count in bins >= lane's lowest bin
+      unsigned long long own = 0;
+      for (int b = hi; b > hi - per && b >= 0; --b) own += wt[b];
+      unsigned long long incl = own;  // weight in bins >= this lane's lowest bin
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        const unsigned long long v = __shfl_up_sync(0xffffffffu, incl, o);
         if (lane >= o) incl += v;
       }
-      const int above = incl - own;  // count in bins above this lane's range
-      const unsigned hit = __ballot_sync(0xffffffffu, incl >= m);
+      const unsigned hit = __ballot_sync(0xffffffffu, incl >= need_total);
       if (hit == 0) {
-        if (lane == 0) s_cut[0] = -1, s_cut[1] = 0;  // fewer than m eligible: take all
+        if (lane == 0) s_cut[0] = -1, s_cut[1] = 0;  // not enough: take all
       } else if (lane == __ffs(hit) - 1) {
-        int cnt = above, b = hi;
-        while (cnt + hist[b] < m) cnt += hist[b--];
+        unsigned long long cum = incl - own;  // weight in bins above this lane's range
+        int b = hi;
+        while (cum + wt[b] < need_total) cum += wt[b--];
+        const unsigned long long need = need_total - cum;  // > 0, <= wt[b]
         s_cut[0] = b;
-        s_cut[1] = m - cnt;
+        s_cut[1] = deficit ? static_cast<int>((need * static_cast<unsigned long long>(hist[b]) + wt[b] - 1) / wt[b])
+                           : static_cast<int>(need);
       }
     }
     __syncthreads();
@@ -248,6 +331,100 @@ __global__ void __launch_bounds__(kSelThreads) prune_select_kernel(const PruneAr
     written += ns;
   }
   if (threadIdx.x == 0) a.off[p] = written;
+}
+
+// ---- probe select (warp per row): top rows take every partner (a pair of two top rows
+// belongs to the lower row), other rows their T strongest predicted partners among the
+// non-top rows (largest KN, ties to the lowest position) ----
+constexpr int kMaxT = 8;
+
+__device__ __forceinline__ bool key_better(unsigned long long k1, int q1, unsigned long long k2, int q2) {
+  return q2 < 0 || (q1 >= 0 && (k1 > k2 || (k1 == k2 && q1 < q2)));
+}
+
+__global__ void __launch_bounds__(256) prune_probe_select_kernel(const PruneArgs a, int T) {
+  const int p = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (p >= a.u) return;
+  const int u = a.u;
+  const int st = a.state_in[p];
+  int* out = a.rowsel + static_cast<int64_t>(p) * u;
+  if (lane == 0) a.state_out[p] = st;
+  if (st == 2) {
+    int written = 0;
+    for (int base = 0; base < u; base += 32) {
+      const int q = base + lane;
+      const bool sel = q < u && q != p && !(q < p && a.state_in[q] == 2);
+      const unsigned bal = __ballot_sync(0xffffffffu, sel);
+      if (sel) out[written + __popc(bal & ((1u << lane) - 1u))] = q;
+      written += __popc(bal);
+    }
+    if (lane == 0) a.off[p] = written;
+    return;
+  }
+  const double* kn = a.KN + static_cast<int64_t>(a.act[p]) * a.d;
+  unsigned long long bk[kMaxT];
+  int bq[kMaxT];
+#pragma unroll
+  for (int i = 0; i < kMaxT; ++i) bk[i] = 0ull, bq[i] = -1;
+  for (int q0 = lane; q0 < u; q0 += 128) {
+    unsigned long long keys[4];
+    bool ok[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {  // independent loads first
+      const int q = q0 + 32 * j;
+      ok[j] = q < u && q != p && a.state_in[q] != 2;
+      keys[j] = ok[j] ? static_cast<unsigned long long>(__double_as_longlong(kn[a.act[q]])) : 0ull;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+    if (!ok[j]) continue;
+    unsigned long long key = keys[j];
+    int qq = q0 + 32 * j;
+#pragma unroll
+    for (int i = 0; i < kMaxT; ++i) {  // insertion into the lane's sorted list
+      if (i < T && key_better(key, qq, bk[i], bq[i])) {
+        const unsigned long long tk = bk[i];
+        const int tq = bq[i];
+        bk[i] = key, bq[i] = qq;
+        key = tk, qq = tq;
+      }
+    }
+    }
+  }
+  int sel[kMaxT];
+  int nsel = 0;
+#pragma unroll
+  for (int r = 0; r < kMaxT; ++r) {
+    if (r >= T) break;
+    unsigned long long k = bk[0];
+    int q = bq[0];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long ok = __shfl_xor_sync(0xffffffffu, k, o);
+      const int oq = __shfl_xor_sync(0xffffffffu, q, o);
+      if (key_better(ok, oq, k, q)) k = ok, q = oq;
+    }
+    if (q < 0) break;  // fewer than T partners
+    sel[r] = q;
+    nsel = r + 1;
+    if (bq[0] == q) {  // the owner pops its head
+#pragma unroll
+      for (int i = 0; i + 1 < kMaxT; ++i) bk[i] = bk[i + 1], bq[i] = bq[i + 1];
+      bk[kMaxT - 1] = 0ull, bq[kMaxT - 1] = -1;
+    }
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 1; i < kMaxT; ++i)  // ascending partner order
+      for (int j = i; j > 0 && j < nsel && sel[j] < sel[j - 1]; --j) {
+        const int t = sel[j];
+        sel[j] = sel[j - 1];
+        sel[j - 1] = t;
+      }
+    for (int i = 0; i < nsel; ++i) out[i] = sel[i];
+    a.off[p] = nsel;
+  }
 }
 
 // ---- scan: off[0..u) counts -> exclusive offsets, off[u] = total ----
@@ -287,6 +464,7 @@ __global__ void __launch_bounds__(1024) prune_scan_kernel(const PruneArgs a) {
   if (threadIdx.x == 0) {
     a.off[a.u] = s_carry;
     atomicAdd(a.evals, static_cast<unsigned long long>(s_carry));
+    atomicAdd(a.evals + 1 + a.stage_idx, static_cast<unsigned long long>(s_carry));
   }
   for (int b = threadIdx.x; b <= s_carry / a.batch; b += blockDim.x) a.work[b] = 0;  // fetch counters
 }
@@ -339,6 +517,11 @@ __device__ __forceinline__ void finalize_chunk(const PruneArgs& a, const double*
   const double mpq = (a.H[q] + e_pq) - (a.H[p] + e_qp);
   a.Md[static_cast<int64_t>(p) * a.u + q] = mpq;
   a.Md[static_cast<int64_t>(q) * a.u + p] = -mpq;
+  // knowledge for the next rounds' predictions: min(0, M)^2 in both directions
+  const int vp = a.act[p], vq = a.act[q];
+  const double cp = mpq < 0.0 ? mpq : 0.0, cq = mpq > 0.0 ? -mpq : 0.0;
+  a.KN[static_cast<int64_t>(vp) * a.d + vq] = __dmul_rn(cp, cp);
+  a.KN[static_cast<int64_t>(vq) * a.d + vp] = __dmul_rn(cq, cq);
 }
 
 // Work items (chunk of 32 list entries, sample segment) are fetched dynamically, chunk-major;
@@ -422,29 +605,35 @@ __global__ void __launch_bounds__(kListThreads, 2) prune_pairs_kernel(const Prun
 }
 
 // ---- bound: partial (or exact) k per row from the evaluated pairs ----
-__global__ void __launch_bounds__(256) prune_bound_kernel(const PruneArgs a, int final_pass) {
+// pass 0 (after the probe): k* over the top rows' exact k; pass 1: alive rows' L (unused:
+// the selection kernels compute L themselves); pass 2 (final): exact k of the top and alive
+// rows, +inf else.
+__global__ void __launch_bounds__(256) prune_bound_kernel(const PruneArgs a, int pass) {
   const int p = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (p >= a.u) return;
   if (*a.err != kNoError) return;
+  const int st = a.state_in[p];
+  if (pass == 2 && st == 0) {
+    if (lane == 0) a.k[p] = __longlong_as_double(static_cast<long long>(kInfBits));
+    return;
+  }
+  if ((pass == 0 && st != 2) || (pass == 1 && st != 1)) return;
   const double* md = a.Md + static_cast<int64_t>(p) * a.u;
-  double* kn = final_pass ? a.KN + static_cast<int64_t>(a.act[p]) * a.d : nullptr;
   // kreduce_kernel's lane-strided order: for a fully evaluated row this is its exact k bits
   double acc = 0.0;
+#pragma unroll 4
   for (int q = lane; q < a.u; q += 32) {
-    if (q == p) continue;
     const double mi = md[q];
-    if (!is_eval(mi)) continue;
+    if (q == p || !is_eval(mi)) continue;
     const double c = (mi < 0.0) ? mi : 0.0;
     acc = __dadd_rn(acc, __dmul_rn(c, c));
-    if (kn) kn[a.act[q]] = __dmul_rn(c, c);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   if (lane != 0) return;
-  const int st = a.state_in[p];
-  if (final_pass) {
-    a.k[p] = (st >= 1) ? acc : __longlong_as_double(static_cast<long long>(kInfBits));
+  if (pass == 2) {
+    a.k[p] = acc;
   } else {
     a.L[p] = acc;
     if (st == 2) atomicMin(a.kstar, static_cast<unsigned long long>(__double_as_longlong(acc)));
@@ -481,11 +670,12 @@ void launch_prune_predict(const PruneArgs& a, cudaStream_t s) {
 }
 
 void launch_prune_top(const PruneArgs& a, int R, cudaStream_t s) {
-  prune_top_kernel<<<1, kTopThreads, 0, s>>>(a, R);
+  prune_top_kernel<<<1, kTopThreads, 0, s>>>(a, R < kMaxR ? R : kMaxR);
 }
 
-void launch_prune_select(const PruneArgs& a, int stage, int m, cudaStream_t s) {
-  prune_select_kernel<<<a.u, kSelThreads, 0, s>>>(a, stage, m);
+void launch_prune_select(const PruneArgs& a, int stage, int m, double beta, cudaStream_t s) {
+  if (stage == kStageProbe) prune_probe_select_kernel<<<(a.u + 7) / 8, 256, 0, s>>>(a, m < kMaxT ? m : kMaxT);
+  else prune_select_kernel<<<a.u, kSelThreads, 0, s>>>(a, stage, m, beta);
 }
 
 void launch_prune_scan(const PruneArgs& a, cudaStream_t s) { prune_scan_kernel<<<1, 1024, 0, s>>>(a); }
@@ -495,8 +685,8 @@ void launch_prune_pairs(const PruneArgs& a, cudaStream_t s) {
   else launch_pairs_cfg<false>(a, s);
 }
 
-void launch_prune_bound(const PruneArgs& a, bool final_pass, cudaStream_t s) {
-  prune_bound_kernel<<<(a.u + 7) / 8, 256, 0, s>>>(a, final_pass ? 1 : 0);
+void launch_prune_bound(const PruneArgs& a, int pass, cudaStream_t s) {
+  prune_bound_kernel<<<(a.u + 7) / 8, 256, 0, s>>>(a, pass);
 }
 
 int prune_pairs_grid() { return pairs_grid_for<false>(); }
