@@ -83,11 +83,11 @@ constexpr int kMinScaledK = -100 * kExpN;
 
 // Fill the shared-memory tables (every thread of the block, then __syncthreads()).
 // g_exp: kExpN doubles; g_log: kLogMasterN double2 (host-computed in long double).
-__device__ __forceinline__ void load_tables(unsigned char* s_tab, const double* g_exp,
-                                            const double2* g_log) {
-  double* e = reinterpret_cast<double*>(s_tab);
+__device__ __forceinline__ void load_tables_into(unsigned char* exp_tab, unsigned char* log_tab, const double* g_exp,
+                                                 const double2* g_log) {
+  double* e = reinterpret_cast<double*>(exp_tab);
   for (int i = threadIdx.x; i < kExpN * kExpRep; i += blockDim.x) e[i] = g_exp[i / kExpRep];
-  double2* l = reinterpret_cast<double2*>(s_tab + kExpTableBytes);
+  double2* l = reinterpret_cast<double2*>(log_tab);
   for (int i = threadIdx.x; i < kLogRows * kLogRep; i += blockDim.x) {
     const int row = i / kLogRep;
     double2 v = make_double2(0.0, 0.0);
@@ -95,6 +95,10 @@ __device__ __forceinline__ void load_tables(unsigned char* s_tab, const double* 
     else if (row >= 128) v = g_log[row - 128];
     l[i] = v;
   }
+}
+__device__ __forceinline__ void load_tables(unsigned char* s_tab, const double* g_exp,
+                                            const double2* g_log) {
+  load_tables_into(s_tab, s_tab + kExpTableBytes, g_exp, g_log);
 }
 
 // Per-lane row bases (byte pointers into shared memory).
@@ -105,6 +109,37 @@ struct TabPtr {
 
 __device__ __forceinline__ TabPtr table_ptrs(const unsigned char* s_tab, int lane) {
   return {s_tab + (lane & (kExpRep - 1)) * 8, s_tab + kExpTableBytes + (lane & (kLogRep - 1)) * 16};
+}
+
+// Alternative table addressing for kernels whose shared-memory base would otherwise cost an
+// integer add per lookup: 32-bit shared-window addresses whose table bases are aligned (log
+// table 32 KB, exp table 16 KB) so the row offset is OR-ed in by the same LOP3 that masks it.
+struct TabAddr {
+  uint32_t exp;  // exp table base | lane slot
+  uint32_t log;  // log table base | lane slot
+};
+constexpr int kTableAlignedBytes = kTableBytes + 32768;  // dynamic smem to request (alignment slack)
+
+// Copy the tables into the aligned layout (log at a 32 KB boundary, exp right after it).
+__device__ __forceinline__ TabAddr load_tables_aligned(unsigned char* dyn, const double* g_exp, const double2* g_log,
+                                                       int lane) {
+  const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(dyn));
+  const uint32_t logb = (base + 32767u) & ~32767u;
+  const uint32_t expb = logb + kLogTableBytes;  // 32 KB after a 32 KB boundary: 16 KB aligned
+  unsigned char* lp = dyn + (logb - base);
+  load_tables_into(lp + kLogTableBytes, lp, g_exp, g_log);
+  return {expb | static_cast<uint32_t>((lane & (kExpRep - 1)) * 8), logb | static_cast<uint32_t>((lane & (kLogRep - 1)) * 16)};
+}
+
+__device__ __forceinline__ double lds_f64(uint32_t addr) {
+  double v;
+  asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ double2 lds_f64x2(uint32_t addr) {
+  double2 v;
+  asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+  return v;
 }
 
 // 2^(k/128), optionally clamped below at 2^-100. Entry j = k & 127 of the table holds
@@ -118,6 +153,20 @@ __device__ __forceinline__ double exp2_k(const TabPtr& tp, int k) {
   if (kClamp) k = max(k, kMinScaledK);
   const double t = *reinterpret_cast<const double*>(tp.exp + (k & (kExpN - 1)) * kExpRowBytes);
   return __hiloint2double(__double2hiint(t) + k * (1 << (20 - kExpBits)), __double2loint(t));
+}
+
+template <bool kClamp>
+__device__ __forceinline__ double exp2_k(const TabAddr& tp, int k) {
+  if (kClamp) k = max(k, kMinScaledK);
+  const double t = lds_f64(tp.exp | (static_cast<uint32_t>(k << 7) & ((kExpN - 1) << 7)));
+  return __hiloint2double(__double2hiint(t) + k * (1 << (20 - kExpBits)), __double2loint(t));
+}
+__device__ __forceinline__ double2 log_row(const TabAddr& tp, unsigned hi) {
+  return lds_f64x2(tp.log | ((hi >> (20 - kLogBits - 7)) & ((kLogRows - 1) << 7)));
+}
+__device__ __forceinline__ double2 log_row(const TabPtr& tp, unsigned hi) {
+  const unsigned row = (hi >> (20 - kLogBits)) & (kLogRows - 1);
+  return *reinterpret_cast<const double2*>(tp.log + row * kLogRowBytes);
 }
 
 // Horner p(x) = 1 + x (c1 + x (c2 + x (c3 + lead x))) with the leading step as
@@ -138,8 +187,8 @@ struct EdeAcc {
 
 // Accumulate one EDE. us = K u (K = 256/ln2). kClampA must be true when |u| can exceed
 // ~350 (n > ~1.2e5 samples); |u| <= sqrt(n) for a normalised residual.
-template <bool kClampA>
-__device__ __forceinline__ void ede_accumulate(double us, EdeAcc& acc, const TabPtr& tp) {
+template <bool kClampA, typename Tab>
+__device__ __forceinline__ void ede_accumulate(double us, EdeAcc& acc, const Tab& tp) {
   // pdf = u exp(-u^2/2) in q' = us^2 units (clamped: q' reaches the subnormal range)
   const double q = us * us;
   const double t2 = fma(q, kC[0], kMagic);
@@ -156,8 +205,7 @@ __device__ __forceinline__ void ede_accumulate(double us, EdeAcc& acc, const Tab
   // log1p(v) - ln2: y = 1 + v in (1, 2]; r = y c - 1 (one rounding); log y = -log c + log1p(r).
   // The rounding of 1 + v perturbs the result by <= 1.1e-16.
   const double y = 1.0 + v;
-  const unsigned row = (static_cast<unsigned>(__double2hiint(y)) >> (20 - kLogBits)) & (kLogRows - 1);
-  const double2 cl = *reinterpret_cast<const double2*>(tp.log + row * kLogRowBytes);
+  const double2 cl = log_row(tp, static_cast<unsigned>(__double2hiint(y)));
   const double r = fma(y, cl.x, -1.0);
   acc.tail += fma(r, poly4(r, kLeadL, kC[8], kC[9], kC[10]), cl.y);
   acc.a += a;

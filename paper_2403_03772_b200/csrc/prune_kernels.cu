@@ -31,6 +31,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "plg_kernels.h"
 #include "plg_math.cuh"
@@ -483,11 +484,65 @@ __device__ __forceinline__ void list_entry(const PruneArgs& a, int k, int& p, in
   q = a.rowsel[static_cast<int64_t>(p) * a.u + (k - a.off[p])];
 }
 
-template <bool kClampA>
+template <bool kClampA, typename Tab>
 __device__ __forceinline__ void ede2(double xa, double ya, double s1, double bs1, double s2, double bs2,
-                                     EdeAcc& acc1, EdeAcc& acc2, const TabPtr& tp) {
+                                     EdeAcc& acc1, EdeAcc& acc2, const Tab& tp) {
   ede_accumulate<kClampA>(fma(ya, -bs1, xa * s1), acc1, tp);
   ede_accumulate<kClampA>(fma(xa, -bs2, ya * s2), acc2, tp);
+}
+
+// One pair's two residual directions over samples [t0, t1) (t0 a multiple of 4), samples in
+// ascending order per direction. Loads go straight to registers with a software prefetch:
+// kVar 0: 4 samples per step, 1 step ahead; 1: 2 samples per step, 2 steps ahead;
+// 2: 4 samples per step, 2 steps ahead.
+template <bool kClampA, int kVar, typename Tab>
+__device__ __forceinline__ void eval_segment(const double* wi, const double* wj, int64_t t0, int64_t t1, double s1,
+                                             double bs1, double s2, double bs2, EdeAcc& acc1, EdeAcc& acc2,
+                                             const Tab& tp) {
+  auto ld = [](const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); };
+  int64_t t = t0;
+  if (kVar == 0) {
+    if (t + 3 < t1) {
+      double2 xa = ld(wi + t), xb = ld(wi + t + 2), ya = ld(wj + t), yb = ld(wj + t + 2);
+#pragma unroll 1
+      for (; t + 3 < t1; t += 4) {
+        const double2 cxa = xa, cxb = xb, cya = ya, cyb = yb;
+        if (t + 7 < t1) xa = ld(wi + t + 4), xb = ld(wi + t + 6), ya = ld(wj + t + 4), yb = ld(wj + t + 6);
+        ede2<kClampA>(cxa.x, cya.x, s1, bs1, s2, bs2, acc1, acc2, tp);
+        ede2<kClampA>(cxa.y, cya.y, s1, bs1, s2, bs2, acc1, acc2, tp);
+        ede2<kClampA>(cxb.x, cyb.x, s1, bs1, s2, bs2, acc1, acc2, tp);
+        ede2<kClampA>(cxb.y, cyb.y, s1, bs1, s2, bs2, acc1, acc2, tp);
+      }
+    }
+  } else if (kVar == 1) {
+    if (t + 5 < t1) {
+      double2 x0 = ld(wi + t), y0 = ld(wj + t), x1 = ld(wi + t + 2), y1 = ld(wj + t + 2);
+#pragma unroll 1
+      for (; t + 1 < t1; t += 2) {
+        const double2 cx = x0, cy = y0;
+        x0 = x1, y0 = y1;
+        if (t + 5 < t1) x1 = ld(wi + t + 4), y1 = ld(wj + t + 4);
+        ede2<kClampA>(cx.x, cy.x, s1, bs1, s2, bs2, acc1, acc2, tp);
+        ede2<kClampA>(cx.y, cy.y, s1, bs1, s2, bs2, acc1, acc2, tp);
+      }
+    }
+  } else {
+    if (t + 7 < t1) {
+      double2 xa = ld(wi + t), xb = ld(wi + t + 2), ya = ld(wj + t), yb = ld(wj + t + 2);
+      double2 xc = ld(wi + t + 4), xd = ld(wi + t + 6), yc = ld(wj + t + 4), yd = ld(wj + t + 6);
+#pragma unroll 1
+      for (; t + 3 < t1; t += 4) {
+        const double2 cxa = xa, cxb = xb, cya = ya, cyb = yb;
+        xa = xc, xb = xd, ya = yc, yb = yd;
+        if (t + 11 < t1) xc = ld(wi + t + 8), xd = ld(wi + t + 10), yc = ld(wj + t + 8), yd = ld(wj + t + 10);
+        ede2<kClampA>(cxa.x, cya.x, s1, bs1, s2, bs2, acc1, acc2, tp);
+        ede2<kClampA>(cxa.y, cya.y, s1, bs1, s2, bs2, acc1, acc2, tp);
+        ede2<kClampA>(cxb.x, cyb.x, s1, bs1, s2, bs2, acc1, acc2, tp);
+        ede2<kClampA>(cxb.y, cyb.y, s1, bs1, s2, bs2, acc1, acc2, tp);
+      }
+    }
+  }
+  for (; t < t1; ++t) ede2<kClampA>(wi[t], wj[t], s1, bs1, s2, bs2, acc1, acc2, tp);
 }
 
 // Finalise one 32-pair chunk once all its sample segments are in: segments in ascending
@@ -528,15 +583,14 @@ __device__ __forceinline__ void finalize_chunk(const PruneArgs& a, const double*
 // the warp completing a chunk's last segment finalises it, so a batch needs no grid barrier.
 // Lists longer than one batch (part-buffer capacity) run batch after batch with a grid
 // barrier between them (the kernel is launched cooperatively).
-template <bool kClampA>
+template <bool kClampA, int kVar>
 __global__ void __launch_bounds__(kListThreads, 2) prune_pairs_kernel(const PruneArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
-  load_tables(smem, a.g_exp, a.g_log);
+  const int lane = threadIdx.x & 31;
+  const TabAddr tp = load_tables_aligned(smem, a.g_exp, a.g_log, lane);
   __syncthreads();
   cg::grid_group grid = cg::this_grid();
-  const int lane = threadIdx.x & 31;
   const bool skip = (*a.err != kNoError);  // only skips work: every CTA still meets the barriers
-  const TabPtr tp = table_ptrs(smem, lane);
   const int total = a.off[a.u];
   const int nbatch = (total + a.batch - 1) / a.batch;
   for (int b = 0; b < nbatch; ++b) {
@@ -564,28 +618,7 @@ __global__ void __launch_bounds__(kListThreads, 2) prune_pairs_kernel(const Prun
         const int64_t t0 = static_cast<int64_t>(seg) * a.seg_len;  // multiple of 4: 32-byte aligned
         const int64_t t1 = lmin(a.n, t0 + a.seg_len);
         EdeAcc acc1, acc2;
-        int64_t t = t0;
-        if (t + 3 < t1) {
-          double2 xa = __ldg(reinterpret_cast<const double2*>(wi + t));
-          double2 xb = __ldg(reinterpret_cast<const double2*>(wi + t + 2));
-          double2 ya = __ldg(reinterpret_cast<const double2*>(wj + t));
-          double2 yb = __ldg(reinterpret_cast<const double2*>(wj + t + 2));
-#pragma unroll 1
-          for (; t + 3 < t1; t += 4) {
-            const double2 cxa = xa, cxb = xb, cya = ya, cyb = yb;
-            if (t + 7 < t1) {  // prefetch the next 4 samples
-              xa = __ldg(reinterpret_cast<const double2*>(wi + t + 4));
-              xb = __ldg(reinterpret_cast<const double2*>(wi + t + 6));
-              ya = __ldg(reinterpret_cast<const double2*>(wj + t + 4));
-              yb = __ldg(reinterpret_cast<const double2*>(wj + t + 6));
-            }
-            ede2<kClampA>(cxa.x, cya.x, s1, bs1, s2, bs2, acc1, acc2, tp);
-            ede2<kClampA>(cxa.y, cya.y, s1, bs1, s2, bs2, acc1, acc2, tp);
-            ede2<kClampA>(cxb.x, cyb.x, s1, bs1, s2, bs2, acc1, acc2, tp);
-            ede2<kClampA>(cxb.y, cyb.y, s1, bs1, s2, bs2, acc1, acc2, tp);
-          }
-        }
-        for (; t < t1; ++t) ede2<kClampA>(wi[t], wj[t], s1, bs1, s2, bs2, acc1, acc2, tp);
+        eval_segment<kClampA, kVar>(wi, wj, t0, t1, s1, bs1, s2, bs2, acc1, acc2, tp);
         double2* dst = reinterpret_cast<double2*>(a.part + (static_cast<int64_t>(seg) * a.batch + kk) * 4);
         __stcg(dst, make_double2(acc_lc(acc1), acc_pdf(acc1)));
         __stcg(dst + 1, make_double2(acc_lc(acc2), acc_pdf(acc2)));
@@ -640,27 +673,29 @@ __global__ void __launch_bounds__(256) prune_bound_kernel(const PruneArgs a, int
   }
 }
 
-template <bool kClampA>
+template <bool kClampA, int kVar>
 int pairs_grid_for() {
   static int grid = 0;
   if (!grid) {
-    cudaFuncSetAttribute(prune_pairs_kernel<kClampA>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTableBytes);
+    cudaFuncSetAttribute(prune_pairs_kernel<kClampA, kVar>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kTableAlignedBytes);
     int dev = 0, sms = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, prune_pairs_kernel<kClampA>, kListThreads, kTableBytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, prune_pairs_kernel<kClampA, kVar>, kListThreads,
+                                                  kTableAlignedBytes);
     grid = sms * (per > 0 ? per : 1);
   }
   return grid;
 }
 
-template <bool kClampA>
+template <bool kClampA, int kVar>
 void launch_pairs_cfg(const PruneArgs& a, cudaStream_t s) {
-  const int grid = pairs_grid_for<kClampA>();
+  const int grid = pairs_grid_for<kClampA, kVar>();
   PruneArgs args = a;
   void* params[] = {&args};
-  cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(prune_pairs_kernel<kClampA>), dim3(grid),
-                              dim3(kListThreads), params, kTableBytes, s);
+  cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(prune_pairs_kernel<kClampA, kVar>), dim3(grid),
+                              dim3(kListThreads), params, kTableAlignedBytes, s);
 }
 
 }  // namespace
@@ -681,14 +716,20 @@ void launch_prune_select(const PruneArgs& a, int stage, int m, double beta, cuda
 void launch_prune_scan(const PruneArgs& a, cudaStream_t s) { prune_scan_kernel<<<1, 1024, 0, s>>>(a); }
 
 void launch_prune_pairs(const PruneArgs& a, cudaStream_t s) {
-  if (a.n > 90000) launch_pairs_cfg<true>(a, s);
-  else launch_pairs_cfg<false>(a, s);
+  static const int var = [] {  // PLG_LIST_VAR: load-pipeline variant (tuning knob)
+    const char* v = std::getenv("PLG_LIST_VAR");
+    return v ? std::atoi(v) : 0;
+  }();
+  if (a.n > 90000) launch_pairs_cfg<true, 0>(a, s);
+  else if (var == 1) launch_pairs_cfg<false, 1>(a, s);
+  else if (var == 2) launch_pairs_cfg<false, 2>(a, s);
+  else launch_pairs_cfg<false, 0>(a, s);
 }
 
 void launch_prune_bound(const PruneArgs& a, int pass, cudaStream_t s) {
   prune_bound_kernel<<<(a.u + 7) / 8, 256, 0, s>>>(a, pass);
 }
 
-int prune_pairs_grid() { return pairs_grid_for<false>(); }
+int prune_pairs_grid() { return pairs_grid_for<false, 0>(); }
 
 }  // namespace plg
