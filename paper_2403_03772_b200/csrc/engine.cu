@@ -186,7 +186,8 @@ struct plg_ctx {
   int prune_T = 2;
   std::vector<double> prune_fracs{0.02, 0.05, 0.12, 0.25};
   bool prune_tile_seg = false;  // PLG_PRUNE_TILESEG=1: the exhaustive rounds' segmentation (bit-identity tests)
-  DevBuf<double> Md, KN, pk, L, ppart;
+  int emulate_world = 1;        // PLG_EMULATE_WORLD=W (tests): a single rank runs the W-rank shard schedule
+  DevBuf<double> Md, KN, pk, L, ppart, pres;
   DevBuf<int> st0, st1, rowsel, off, pwork, pdone;
   DevBuf<unsigned long long> kstar, evals;
 
@@ -267,6 +268,7 @@ void parse_prune_env(plg_ctx* ctx) {
     }
   }
   if (const char* v = std::getenv("PLG_PRUNE_TILESEG")) ctx->prune_tile_seg = !strcmp(v, "1");
+  if (const char* v = std::getenv("PLG_EMULATE_WORLD")) ctx->emulate_world = std::max(1, std::atoi(v));
 }
 
 int ctx_init(plg_ctx* ctx, int device, plg_status* st) {
@@ -448,36 +450,76 @@ int search_round_pruned(plg_ctx* c, int64_t n, int64_t ldw, int d, int u, const 
   plg::launch_prune_top(a, c->prune_R, c->stream);
   c->launches += 2;
   int stage_idx = 0;
-  auto stage = [&](int kind, int m, double beta, int pass) {
+  const int shards = c->world > 1 ? c->world : c->emulate_world;
+  a.k_begin = 0;
+  a.k_end = -1;
+  a.res = nullptr;
+  auto stage = [&](int kind, int m, double beta, int pass) -> int {
     a.stage_idx = std::min(stage_idx++, plg::kMaxPruneStages - 1);
     a.state_in = sa;
     a.state_out = sb;
     plg::launch_prune_select(a, kind, m, beta, c->stream);
     plg::launch_prune_scan(a, c->stream);
-    const size_t tm = pair_timer_begin(c);
-    plg::launch_prune_pairs(a, c->stream);
-    pair_timer_end(c, tm);
+    c->launches += 2;
+    if (shards == 1) {
+      const size_t tm = pair_timer_begin(c);
+      plg::launch_prune_pairs(a, c->stream);
+      pair_timer_end(c, tm);
+      ++c->launches;
+    } else {
+      // Multi-rank: the list is identical on every rank (deterministic selection), so rank r
+      // evaluates the contiguous slice [r cnt, (r + 1) cnt) and one in-place all-gather of
+      // the M values gives every rank the whole stage; the scatter writes them into Md / KN.
+      int total = 0;
+      PLG_CUDA(cudaMemcpyAsync(&total, c->off.p + u, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+      PLG_CUDA(cudaStreamSynchronize(c->stream));
+      const int cnt = (total + shards - 1) / shards;
+      a.res = c->pres.p;
+      for (int r = (c->world > 1 ? c->rank : 0); r < (c->world > 1 ? c->rank + 1 : shards); ++r) {
+        a.k_begin = std::min(total, r * cnt);
+        a.k_end = std::min(total, (r + 1) * cnt);
+        if (r > (c->world > 1 ? c->rank : 0))  // emulated ranks share one set of fetch counters
+          PLG_CUDA(cudaMemsetAsync(c->pwork.p, 0, (kPruneBatch > 0 ? (cnt / kPruneBatch + 2) : 2) * sizeof(int),
+                                   c->stream));
+        const size_t tm = pair_timer_begin(c);
+        plg::launch_prune_pairs(a, c->stream);
+        pair_timer_end(c, tm);
+        ++c->launches;
+      }
+      if (c->world > 1 && cnt > 0) {
+        NcclApi& api = nccl();
+        const ncclResult_t r = api.AllGather(c->pres.p + static_cast<size_t>(c->rank) * cnt, c->pres.p, cnt,
+                                             ncclDouble, c->comm, c->stream);
+        if (r != ncclSuccess)
+          return set_status(st, PLG_NcclError, -1, -1, "ncclAllGather: %s", api.GetErrorString(r));
+      }
+      plg::launch_prune_scatter(a, total, c->stream);
+      ++c->launches;
+      a.res = nullptr;
+      a.k_begin = 0;
+      a.k_end = -1;
+    }
     std::swap(sa, sb);
     a.state_in = sa;
-    c->launches += 3;
     if (pass != 1) {  // refinement stages: the next selection computes each row's partial k
       plg::launch_prune_bound(a, pass, c->stream);
       ++c->launches;
     }
+    return 0;
   };
-  stage(plg::kStageProbe, c->prune_T, 0.0, 0);
+  if (int rc = stage(plg::kStageProbe, c->prune_T, 0.0, 0)) return rc;
   // refinement ladder: values < 1 are cumulative fractions of the row (count mode: the step
   // to the next fraction), values >= 1 deficit multipliers (prune_kernels.cu select)
   double prev = 0.0;
   for (double f : c->prune_fracs) {
     if (f >= 1.0) {
-      stage(plg::kStageRefine, 0, f, 1);
+      if (int rc = stage(plg::kStageRefine, 0, f, 1)) return rc;
     } else {
-      stage(plg::kStageRefine, std::max(1, static_cast<int>((f - prev) * u)), 0.0, 1);
+      if (int rc = stage(plg::kStageRefine, std::max(1, static_cast<int>((f - prev) * u)), 0.0, 1)) return rc;
       prev = f;
     }
   }
-  stage(plg::kStageFull, 0, 0.0, 2);
+  if (int rc = stage(plg::kStageFull, 0, 0.0, 2)) return rc;
   return 0;
 }
 
@@ -531,6 +573,7 @@ int reserve_prune(plg_ctx* c, int64_t n, int d, plg_status* st) {
   const size_t max_list = dd + d;  // per-stage list bound: u (u - 1) entries + slack
   PLG_CUDA(c->pwork.reserve(max_list / kPruneBatch + 2));
   PLG_CUDA(c->pdone.reserve(kPruneBatch / 32));
+  if (c->world > 1 || c->emulate_world > 1) PLG_CUDA(c->pres.reserve(max_list + 64));
   PLG_CUDA(cudaMemsetAsync(c->pdone.p, 0, (kPruneBatch / 32) * sizeof(int), c->stream));
   PLG_CUDA(cudaMemsetAsync(c->evals.p, 0, (1 + plg::kMaxPruneStages) * sizeof(unsigned long long), c->stream));
   return 0;
@@ -636,8 +679,8 @@ int causal_order_impl(plg_ctx* c, const double* dX, int64_t ldx, int64_t n, int 
   ++c->launches;
   const int rounds = (max_rounds < 0) ? d - 1 : std::min(max_rounds, d - 1);
   // Exact pruning needs a previous exhaustive round's knowledge and pays off above the
-  // replicated small-round size; single-rank runs only.
-  const bool prune = c->prune && c->world == 1 && !c->hook && d > plg::kSmallU + 1 && rounds > 1;
+  // replicated small-round size.
+  const bool prune = c->prune && !c->hook && d > plg::kSmallU + 1 && rounds > 1;
   c->pairs_done = 0;
   if (prune)
     if (int rc = reserve_prune(c, n, d, st)) return rc;

@@ -168,6 +168,9 @@ struct PruneArgs {
   double* k;                    // [u] exact k of alive/top rows, +inf for pruned rows
   unsigned long long* evals;    // [1 + stages] list entries evaluated: total, per stage index
   int stage_idx;
+  int k_begin;                  // list entries this launch evaluates: [k_begin, k_end)
+  int k_end;                    // (k_end < 0: the whole list from k_begin)
+  double* res;                  // multi-rank: M of every list entry by list index (all-gathered)
 };
 enum PruneStage : int { kStageProbe = 0, kStageRefine = 1, kStageFull = 2 };
 void launch_prune_predict(const PruneArgs& a, cudaStream_t s);
@@ -177,6 +180,8 @@ void launch_prune_top(const PruneArgs& a, int R, cudaStream_t s);
 void launch_prune_select(const PruneArgs& a, int stage, int m, double beta, cudaStream_t s);
 void launch_prune_scan(const PruneArgs& a, cudaStream_t s);
 void launch_prune_pairs(const PruneArgs& a, cudaStream_t s);
+// multi-rank: res[0..total) (all ranks' results, gathered) into Md / KN
+void launch_prune_scatter(const PruneArgs& a, int total, cudaStream_t s);
 // pass 0: every row's partial k L[] and k* over the top rows; 1: alive rows' L[]; 2: exact k[]
 // of the top and alive rows (+inf for pruned rows)
 void launch_prune_bound(const PruneArgs& a, int pass, cudaStream_t s);

@@ -545,6 +545,17 @@ __device__ __forceinline__ void eval_segment(const double* wi, const double* wj,
   for (; t < t1; ++t) ede2<kClampA>(wi[t], wj[t], s1, bs1, s2, bs2, acc1, acc2, tp);
 }
 
+// M_pq and M_qp = -M_pq into the round's table; KN (the next rounds' predictions) gets
+// min(0, M)^2 in both directions.
+__device__ __forceinline__ void store_pair(const PruneArgs& a, int p, int q, double mpq) {
+  a.Md[static_cast<int64_t>(p) * a.u + q] = mpq;
+  a.Md[static_cast<int64_t>(q) * a.u + p] = -mpq;
+  const int vp = a.act[p], vq = a.act[q];
+  const double cp = mpq < 0.0 ? mpq : 0.0, cq = mpq > 0.0 ? -mpq : 0.0;
+  a.KN[static_cast<int64_t>(vp) * a.d + vq] = __dmul_rn(cp, cp);
+  a.KN[static_cast<int64_t>(vq) * a.d + vp] = __dmul_rn(cq, cq);
+}
+
 // Finalise one 32-pair chunk once all its sample segments are in: segments in ascending
 // order (finalize_kernel's order), both entropies, then M_pq and M_qp = -M_pq.
 __device__ __forceinline__ void finalize_chunk(const PruneArgs& a, const double* part, int base, int m, int chunk,
@@ -570,13 +581,8 @@ __device__ __forceinline__ void finalize_chunk(const PruneArgs& a, const double*
   const double e_qp = entropy_from_sums(l2, p2, inv_n);  // E(q | p)
   // ordering.cpp:93-94 (kreduce_kernel's expression); M_qp = -M_pq exactly
   const double mpq = (a.H[q] + e_pq) - (a.H[p] + e_qp);
-  a.Md[static_cast<int64_t>(p) * a.u + q] = mpq;
-  a.Md[static_cast<int64_t>(q) * a.u + p] = -mpq;
-  // knowledge for the next rounds' predictions: min(0, M)^2 in both directions
-  const int vp = a.act[p], vq = a.act[q];
-  const double cp = mpq < 0.0 ? mpq : 0.0, cq = mpq > 0.0 ? -mpq : 0.0;
-  a.KN[static_cast<int64_t>(vp) * a.d + vq] = __dmul_rn(cp, cp);
-  a.KN[static_cast<int64_t>(vq) * a.d + vp] = __dmul_rn(cq, cq);
+  store_pair(a, p, q, mpq);
+  if (a.res) a.res[base + kk] = mpq;  // multi-rank: this rank's slot of the all-gathered results
 }
 
 // Work items (chunk of 32 list entries, sample segment) are fetched dynamically, chunk-major;
@@ -591,12 +597,13 @@ __global__ void __launch_bounds__(kListThreads, 2) prune_pairs_kernel(const Prun
   __syncthreads();
   cg::grid_group grid = cg::this_grid();
   const bool skip = (*a.err != kNoError);  // only skips work: every CTA still meets the barriers
-  const int total = a.off[a.u];
+  // this launch's share of the list: [k_begin, k_end) (k_end < 0: to the end of the list)
+  const int total = (a.k_end >= 0 ? a.k_end : a.off[a.u]) - a.k_begin;
   const int nbatch = (total + a.batch - 1) / a.batch;
   for (int b = 0; b < nbatch; ++b) {
     if (b > 0) grid.sync();  // every chunk of batch b - 1 is finalised: the part slab is free
-    const int base = b * a.batch;
-    const int m = min(a.batch, total - base);
+    const int base = a.k_begin + b * a.batch;
+    const int m = min(a.batch, total - b * a.batch);
     const int chunks = (m + 31) / 32;
     const int items = chunks * a.nseg;
     while (!skip) {
@@ -634,6 +641,15 @@ __global__ void __launch_bounds__(kListThreads, 2) prune_pairs_kernel(const Prun
         if (lane == 0) a.done[chunk] = 0;  // ready for the next batch / launch
       }
     }
+  }
+}
+
+// ---- scatter (multi-rank): every rank's results of the stage's list into Md / KN ----
+__global__ void prune_scatter_kernel(const PruneArgs a, int total) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < total; k += gridDim.x * blockDim.x) {
+    int p, q;
+    list_entry(a, k, p, q);
+    store_pair(a, p, q, a.res[k]);
   }
 }
 
@@ -724,6 +740,13 @@ void launch_prune_pairs(const PruneArgs& a, cudaStream_t s) {
   else if (var == 1) launch_pairs_cfg<false, 1>(a, s);
   else if (var == 2) launch_pairs_cfg<false, 2>(a, s);
   else launch_pairs_cfg<false, 0>(a, s);
+}
+
+void launch_prune_scatter(const PruneArgs& a, int total, cudaStream_t s) {
+  if (total <= 0) return;
+  int grid = (total + 255) / 256;
+  if (grid > 148 * 8) grid = 148 * 8;
+  prune_scatter_kernel<<<grid, 256, 0, s>>>(a, total);
 }
 
 void launch_prune_bound(const PruneArgs& a, int pass, cudaStream_t s) {

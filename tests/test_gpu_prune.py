@@ -46,8 +46,8 @@ print(json.dumps(out))
 """
 
 
-def _run(d, n, seed, kind, tileseg):
-    env = dict(os.environ, PLG_PRUNE_TILESEG="1" if tileseg else "0")
+def _run(d, n, seed, kind, tileseg, emulate_world=1):
+    env = dict(os.environ, PLG_PRUNE_TILESEG="1" if tileseg else "0", PLG_EMULATE_WORLD=str(emulate_world))
     env.pop("PLG_PRUNE", None)
     out = subprocess.run([sys.executable, "-c", _CHILD % (ROOT, d, n, seed, kind)], env=env,
                          capture_output=True, text=True, check=True, timeout=900)
@@ -78,5 +78,16 @@ def test_pruned_rounds_default_segmentation():
 def test_pruned_rounds_on_exchangeable_gaussian_data():
     # no causal structure: every candidate's k is noise of one size; pruning must still be exact
     r = _run(180, 1500, 2, "gauss", tileseg=True)
+    assert r["prune"]["order"] == r["full"]["order"]
+    assert r["prune"]["k"] == r["full"]["k"]
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_pruned_rounds_sharded_schedule(world):
+    # A single rank runs the multi-rank schedule of the pruned rounds (each stage's list split
+    # into `world` contiguous slices, evaluated one after the other, results gathered by list
+    # index and scattered): the order and every winning k must not change. The NCCL
+    # all-gather itself is the only part of the multi-GPU path this does not exercise.
+    r = _run(300, 4000, 7, "laplace", tileseg=True, emulate_world=world)
     assert r["prune"]["order"] == r["full"]["order"]
     assert r["prune"]["k"] == r["full"]["k"]
