@@ -140,13 +140,13 @@ SegPlan seg_plan(int u, int64_t n) {
   return {static_cast<int>((n + seg_len - 1) / seg_len), static_cast<int>(seg_len)};
 }
 
-// Segmentation of a pruned round: fine (256-sample) segments so that even a short pair list
-// spreads over every SM; at most 64 segments. Pure function of n.
+// Segmentation of a pruned round: fine (128-sample) segments so that even a short pair list
+// spreads over every SM and a stage's tail is short; at most 128 segments. Pure function of n.
 int64_t prune_seg_min() {
   static const int64_t v = [] {
     const char* e = std::getenv("PLG_PRUNE_SEGLEN");  // tuning knob (multiple of 4)
-    const int64_t x = e ? std::atoll(e) : 256;
-    return x >= 16 ? x / 4 * 4 : int64_t{256};
+    const int64_t x = e ? std::atoll(e) : 128;
+    return x >= 16 ? x / 4 * 4 : int64_t{128};
   }();
   return v;
 }
@@ -187,8 +187,9 @@ struct plg_ctx {
   std::vector<double> prune_fracs{0.02, 0.05, 0.12, 0.25};
   bool prune_tile_seg = false;  // PLG_PRUNE_TILESEG=1: the exhaustive rounds' segmentation (bit-identity tests)
   int emulate_world = 1;        // PLG_EMULATE_WORLD=W (tests): a single rank runs the W-rank shard schedule
+  double prune_beta = 1.1;      // PLG_PRUNE_BETA > 0: hybrid refinement (deficit cut when smaller than the step)
   DevBuf<double> Md, KN, pk, L, ppart, pres;
-  DevBuf<int> st0, st1, rowsel, off, pwork, pdone;
+  DevBuf<int> st0, st1, rowsel, off, pwork, pdone, crow;
   DevBuf<unsigned long long> kstar, evals;
 
   size_t ev_pairs = 0;  // pair-kernel timing intervals recorded by this call (ev[3 + 2 i], ev[4 + 2 i])
@@ -269,6 +270,7 @@ void parse_prune_env(plg_ctx* ctx) {
   }
   if (const char* v = std::getenv("PLG_PRUNE_TILESEG")) ctx->prune_tile_seg = !strcmp(v, "1");
   if (const char* v = std::getenv("PLG_EMULATE_WORLD")) ctx->emulate_world = std::max(1, std::atoi(v));
+  if (const char* v = std::getenv("PLG_PRUNE_BETA")) ctx->prune_beta = std::atof(v);
 }
 
 int ctx_init(plg_ctx* ctx, int device, plg_status* st) {
@@ -430,6 +432,7 @@ int search_round_pruned(plg_ctx* c, int64_t n, int64_t ldw, int d, int u, const 
   a.pk = c->pk.p;
   a.rowsel = c->rowsel.p;
   a.off = c->off.p;
+  a.crow = c->crow.p;
   a.part = c->ppart.p;
   a.work = c->pwork.p;
   a.done = c->pdone.p;
@@ -515,7 +518,8 @@ int search_round_pruned(plg_ctx* c, int64_t n, int64_t ldw, int d, int u, const 
     if (f >= 1.0) {
       if (int rc = stage(plg::kStageRefine, 0, f, 1)) return rc;
     } else {
-      if (int rc = stage(plg::kStageRefine, std::max(1, static_cast<int>((f - prev) * u)), 0.0, 1)) return rc;
+      if (int rc = stage(plg::kStageRefine, std::max(1, static_cast<int>((f - prev) * u)), c->prune_beta, 1))
+        return rc;
       prev = f;
     }
   }
@@ -573,6 +577,7 @@ int reserve_prune(plg_ctx* c, int64_t n, int d, plg_status* st) {
   const size_t max_list = dd + d;  // per-stage list bound: u (u - 1) entries + slack
   PLG_CUDA(c->pwork.reserve(max_list / kPruneBatch + 2));
   PLG_CUDA(c->pdone.reserve(kPruneBatch / 32));
+  PLG_CUDA(c->crow.reserve(max_list / 32 + 2));
   if (c->world > 1 || c->emulate_world > 1) PLG_CUDA(c->pres.reserve(max_list + 64));
   PLG_CUDA(cudaMemsetAsync(c->pdone.p, 0, (kPruneBatch / 32) * sizeof(int), c->stream));
   PLG_CUDA(cudaMemsetAsync(c->evals.p, 0, (1 + plg::kMaxPruneStages) * sizeof(unsigned long long), c->stream));

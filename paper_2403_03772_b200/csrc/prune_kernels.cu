@@ -252,12 +252,13 @@ __global__ void __launch_bounds__(kSelThreads) prune_select_kernel(const PruneAr
     if (stage == kStageProbe) return full ? !(a.state_in[q] == 2 && q < p) : a.state_in[q] != 2;
     return true;
   };
+  // Modes: count (beta <= 0): the m strongest; deficit (m <= 0): strongest until their
+  // predicted sum reaches beta x deficit, else all; hybrid (both): the deficit cut when it
+  // needs fewer than m partners, else the m strongest.
   const bool deficit = beta > 0.0;
   constexpr double kOne = 16777216.0;  // fixed-point unit of the deficit target (2^24)
   const double target = fmax(beta * (thr - Lp), thr * 1e-6);
   const double wscale = deficit ? kOne / target : 0.0;
-  const unsigned long long need_total = deficit ? static_cast<unsigned long long>(kOne)
-                                                : static_cast<unsigned long long>(m);
   int cut_bin = -1, cut_take = 0;  // full: every eligible partner
   if (!full) {
     for (int i = threadIdx.x; i < kBins; i += kSelThreads) hist[i] = 0, wt[i] = 0ull;
@@ -273,33 +274,61 @@ __global__ void __launch_bounds__(kSelThreads) prune_select_kernel(const PruneAr
       if (deficit && e) atomicAdd(&wt[b], static_cast<unsigned long long>(fmin(v * wscale, 1099511627776.0)));
     }
     __syncthreads();
-    if (!deficit)
-      for (int i = threadIdx.x; i < kBins; i += kSelThreads) wt[i] = static_cast<unsigned long long>(hist[i]);
-    __syncthreads();
-    if (threadIdx.x < 32) {  // suffix scan from the top bin: the bin where the weight reaches need
-      const int lane = threadIdx.x;
-      constexpr int per = (kBins + 31) / 32;
-      const int hi = kBins - 1 - lane * per;  // lane covers bins (hi - per, hi]
-      unsigned long long own = 0;
-      for (int b = hi; b > hi - per && b >= 0; --b) own += wt[b];
-      unsigned long long incl = own;  // weight in bins >= this lane's lowest bin
+    if (threadIdx.x < 32) {
+      // Suffix scan from the top bin (warp 0): the bin where the cumulative weight reaches
+      // need; returns false when the total falls short. cnt_above = entries in higher bins.
+      auto find_cut = [&](bool weighted, unsigned long long need_total, int& bin, int& take, int& cnt_above) -> bool {
+        const int lane = threadIdx.x;
+        constexpr int per = (kBins + 31) / 32;
+        const int hi = kBins - 1 - lane * per;  // lane covers bins (hi - per, hi]
+        unsigned long long own = 0;
+        int own_n = 0;
+        for (int b = hi; b > hi - per && b >= 0; --b) {
+          own += weighted ? wt[b] : static_cast<unsigned long long>(hist[b]);
+          own_n += hist[b];
+        }
+        unsigned long long incl = own;
+        int incl_n = own_n;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned long long v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
-      }
-      const unsigned hit = __ballot_sync(0xffffffffu, incl >= need_total);
-      if (hit == 0) {
-        if (lane == 0) s_cut[0] = -1, s_cut[1] = 0;  // not enough: take all
-      } else if (lane == __ffs(hit) - 1) {
-        unsigned long long cum = incl - own;  // weight in bins above this lane's range
-        int b = hi;
-        while (cum + wt[b] < need_total) cum += wt[b--];
-        const unsigned long long need = need_total - cum;  // > 0, <= wt[b]
-        s_cut[0] = b;
-        s_cut[1] = deficit ? static_cast<int>((need * static_cast<unsigned long long>(hist[b]) + wt[b] - 1) / wt[b])
-                           : static_cast<int>(need);
-      }
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned long long v = __shfl_up_sync(0xffffffffu, incl, o);
+          const int vn = __shfl_up_sync(0xffffffffu, incl_n, o);
+          if (lane >= o) incl += v, incl_n += vn;
+        }
+        const unsigned hit = __ballot_sync(0xffffffffu, incl >= need_total);
+        if (hit == 0) return false;
+        const int src = __ffs(hit) - 1;
+        int r_bin = 0, r_take = 0, r_cnt = 0;
+        if (lane == src) {
+          unsigned long long cum = incl - own;
+          int cn = incl_n - own_n;
+          int b = hi;
+          for (;;) {
+            const unsigned long long wb = weighted ? wt[b] : static_cast<unsigned long long>(hist[b]);
+            if (cum + wb >= need_total) break;
+            cum += wb;
+            cn += hist[b];
+            --b;
+          }
+          const unsigned long long need = need_total - cum;  // > 0, <= the bin's weight
+          r_bin = b;
+          r_take = weighted ? static_cast<int>((need * static_cast<unsigned long long>(hist[b]) + wt[b] - 1) / wt[b])
+                            : static_cast<int>(need);
+          r_cnt = cn;
+        }
+        bin = __shfl_sync(0xffffffffu, r_bin, src);
+        take = __shfl_sync(0xffffffffu, r_take, src);
+        cnt_above = __shfl_sync(0xffffffffu, r_cnt, src);
+        return true;
+      };
+      int bin = -1, take = 0, above = 0;
+      bool done = false;
+      if (deficit && find_cut(true, static_cast<unsigned long long>(kOne), bin, take, above))
+        done = (m <= 0) || (above + take < m);  // hybrid: keep the deficit cut only if smaller
+      else if (deficit && m <= 0)
+        bin = -1, take = 0, done = true;  // pure deficit mode, prediction short: every partner
+      if (!done && !find_cut(false, static_cast<unsigned long long>(m), bin, take, above)) bin = -1, take = 0;
+      if (threadIdx.x == 0) s_cut[0] = bin, s_cut[1] = take;
     }
     __syncthreads();
     cut_bin = s_cut[0];
@@ -468,19 +497,22 @@ __global__ void __launch_bounds__(1024) prune_scan_kernel(const PruneArgs a) {
     atomicAdd(a.evals + 1 + a.stage_idx, static_cast<unsigned long long>(s_carry));
   }
   for (int b = threadIdx.x; b <= s_carry / a.batch; b += blockDim.x) a.work[b] = 0;  // fetch counters
+  __syncthreads();  // every offset visible to the block
+  const int total = s_carry;
+  for (int p = threadIdx.x; p < a.u; p += blockDim.x) {  // chunk -> row of its first entry
+    const int b = a.off[p], e = (p + 1 < a.u) ? a.off[p + 1] : total;
+    for (int c = (b + 31) >> 5; c < ((e + 31) >> 5); ++c) a.crow[c] = p;
+  }
 }
 
 // ---- pairs: cooperative persistent evaluation of the list ----
 constexpr int kListThreads = 256;
 
+// Entry k of the stage's list: the row holding the entry's 32-chunk start (chunk_row, from the
+// scan), then forward over rows that end before k (rows with zero entries share offsets).
 __device__ __forceinline__ void list_entry(const PruneArgs& a, int k, int& p, int& q) {
-  int lo = 0, hi = a.u;  // largest p with off[p] <= k (rows with zero entries share offsets)
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (a.off[mid] <= k) lo = mid;
-    else hi = mid;
-  }
-  p = lo;
+  p = a.crow[k >> 5];
+  while (p + 1 < a.u && a.off[p + 1] <= k) ++p;
   q = a.rowsel[static_cast<int64_t>(p) * a.u + (k - a.off[p])];
 }
 
