@@ -182,14 +182,14 @@ struct plg_ctx {
 
   // exact pruned rounds of causal_order (prune_kernels.cu); PLG_PRUNE="R:T:f1,f2,..." or "0"
   bool prune = true;
-  int prune_R = 4;
-  int prune_T = 2;
-  std::vector<double> prune_fracs{0.02, 0.05, 0.12, 0.25};
+  int prune_R = 3;
+  int prune_T = 1;
+  std::vector<double> prune_fracs{0.03, 0.1, 0.3};
   bool prune_tile_seg = false;  // PLG_PRUNE_TILESEG=1: the exhaustive rounds' segmentation (bit-identity tests)
   int emulate_world = 1;        // PLG_EMULATE_WORLD=W (tests): a single rank runs the W-rank shard schedule
   double prune_beta = 1.1;      // PLG_PRUNE_BETA > 0: hybrid refinement (deficit cut when smaller than the step)
   DevBuf<double> Md, KN, pk, L, ppart, pres;
-  DevBuf<int> st0, st1, rowsel, off, pwork, pdone, crow;
+  DevBuf<int> st0, st1, rowsel, off, pwork, pdone, crow, cand;
   DevBuf<unsigned long long> kstar, evals;
 
   size_t ev_pairs = 0;  // pair-kernel timing intervals recorded by this call (ev[3 + 2 i], ev[4 + 2 i])
@@ -433,6 +433,7 @@ int search_round_pruned(plg_ctx* c, int64_t n, int64_t ldw, int d, int u, const 
   a.rowsel = c->rowsel.p;
   a.off = c->off.p;
   a.crow = c->crow.p;
+  a.cand = c->cand.p;
   a.part = c->ppart.p;
   a.work = c->pwork.p;
   a.done = c->pdone.p;
@@ -578,6 +579,7 @@ int reserve_prune(plg_ctx* c, int64_t n, int d, plg_status* st) {
   PLG_CUDA(c->pwork.reserve(max_list / kPruneBatch + 2));
   PLG_CUDA(c->pdone.reserve(kPruneBatch / 32));
   PLG_CUDA(c->crow.reserve(max_list / 32 + 2));
+  PLG_CUDA(c->cand.reserve(static_cast<size_t>(d) * 8));
   if (c->world > 1 || c->emulate_world > 1) PLG_CUDA(c->pres.reserve(max_list + 64));
   PLG_CUDA(cudaMemsetAsync(c->pdone.p, 0, (kPruneBatch / 32) * sizeof(int), c->stream));
   PLG_CUDA(cudaMemsetAsync(c->evals.p, 0, (1 + plg::kMaxPruneStages) * sizeof(unsigned long long), c->stream));

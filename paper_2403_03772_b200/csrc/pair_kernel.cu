@@ -400,22 +400,24 @@ __global__ void __launch_bounds__(kColentThreads)
 // hpart[(r * nch + c) * 2] = {sum lc, sum pdf}. hfin_kernel adds the chunks in ascending
 // order next round. Persistent CTAs so the tables are staged once per CTA, not per column.
 constexpr int kResidThreads = 256;
+// One warp per (column, chunk) item: lane-strided double2 pairs, a warp shuffle reduction, no
+// block barrier; items are taken warp-strided over the persistent grid.
 __global__ void __launch_bounds__(kResidThreads)
     resid_ent_kernel(double* W, int64_t ldw, int64_t n, const double* C, int64_t ldc, const int* act_nxt,
                      int ur, const RoundState* rs, int* nz, int tag, const unsigned long long* err,
                      int64_t chunk, int nch, double* hpart, const double* g_exp, const double2* g_log) {
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ double s_red[2][kResidThreads / 32];
   if (*err != kNoError) return;
   load_tables(smem, g_exp, g_log);
   __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
   const TabPtr tp = table_ptrs(smem, lane);
   const int m = rs->chosen_col;
   const double cmm = C[static_cast<int64_t>(m) * ldc + m];
   const double2* wm = reinterpret_cast<const double2*>(W + static_cast<int64_t>(m) * ldw);
   const int items = ur * nch;
-  for (int it = blockIdx.x; it < items; it += gridDim.x) {
+  const int warps = gridDim.x * (kResidThreads / 32);
+  for (int it = blockIdx.x * (kResidThreads / 32) + (threadIdx.x >> 5); it < items; it += warps) {
     const int pos = it / nch, c = it - pos * nch;
     const int r = act_nxt[pos];
     const double beta = C[static_cast<int64_t>(r) * ldc + m] / cmm;
@@ -424,7 +426,7 @@ __global__ void __launch_bounds__(kResidThreads)
     const int64_t t0 = c * chunk, t1 = lmin(n, t0 + chunk);  // samples; chunk is even
     EdeAcc acc;
     bool any = false;
-    for (int64_t t = t0 + 2 * threadIdx.x; t < t1; t += 2 * kResidThreads) {
+    for (int64_t t = t0 + 2 * lane; t < t1; t += 64) {
       const double2 x = wr[t >> 1];
       const double2 y = wm[t >> 1];
       const double2 o = make_double2(__dsub_rn(x.x, __dmul_rn(beta, y.x)), __dsub_rn(x.y, __dmul_rn(beta, y.y)));
@@ -441,20 +443,9 @@ __global__ void __launch_bounds__(kResidThreads)
       pd += __shfl_xor_sync(0xffffffffu, pd, o);
     }
     if (lane == 0) {
-      s_red[0][warp] = lc;
-      s_red[1][warp] = pd;
+      hpart[static_cast<int64_t>(it) * 2] = lc;
+      hpart[static_cast<int64_t>(it) * 2 + 1] = pd;
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double l = 0.0, q = 0.0;
-      for (int w2 = 0; w2 < kResidThreads / 32; ++w2) {
-        l += s_red[0][w2];
-        q += s_red[1][w2];
-      }
-      hpart[static_cast<int64_t>(it) * 2] = l;
-      hpart[static_cast<int64_t>(it) * 2 + 1] = q;
-    }
-    __syncthreads();
   }
 }
 
@@ -622,7 +613,8 @@ void launch_resid_ent(double* W, int64_t ldw, int64_t n, const double* C, int64_
     grid = sms * (per > 0 ? per : 1);
   }
   const int nch = resid_chunks(n);
-  const int g = ur * nch < grid ? ur * nch : grid;
+  const int need = (ur * nch + kResidThreads / 32 - 1) / (kResidThreads / 32);
+  const int g = need < grid ? need : grid;
   resid_ent_kernel<<<g, kResidThreads, kTableBytes, s>>>(W, ldw, n, C, ldc, act_nxt, ur, rs, nz, tag, err,
                                                         kResidChunk, nch, hpart, g_exp, g_log);
 }

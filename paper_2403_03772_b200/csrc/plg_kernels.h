@@ -82,7 +82,7 @@ void launch_colent(const double* W, int64_t ldw, int64_t n, const double* C, int
 // Residualisation (as launch_residualize) fused with the next round's column-entropy sums per
 // chunk of kResidChunk samples (hpart: [ur][resid_chunks(n)][2]); launch_hfin turns them into
 // H (and runs colent's zero-variance check). Rounds >= 1 of causal_order use this pair.
-constexpr int64_t kResidChunk = 2048;
+constexpr int64_t kResidChunk = 1024;
 int resid_chunks(int64_t n);
 void launch_resid_ent(double* W, int64_t ldw, int64_t n, const double* C, int64_t ldc, const int* act_nxt, int ur,
                       const RoundState* rs, int* nz, int tag, const unsigned long long* err, double* hpart,
@@ -153,6 +153,7 @@ struct PruneArgs {
   double* L;                    // [u] partial k over the evaluated pairs
   unsigned long long* kstar;    // bits of min exact k over the top rows
   double* pk;                   // [u] predicted k (sum of KN over the active row)
+  int* cand;                    // [u][4] strongest predicted partners of each row (ordered)
   int* rowsel;                  // [u * u] selected partner positions of each row, ascending
   int* off;                     // [u + 1] per-row counts -> exclusive offsets, off[u] = total
   int* crow;                    // [list / 32 + 1] row of each 32-entry chunk's first entry

@@ -44,6 +44,7 @@ namespace plg {
 namespace {
 
 constexpr unsigned long long kInfBits = 0x7ff0000000000000ull;
+constexpr int kPredK = 4;  // predicted partners kept per row by prune_predict (probe suspects; R + T <= 4)
 constexpr double kPruneSlack = 1e-9;  // relative margin over k* (>> u 2^-53)
 
 __device__ __forceinline__ bool is_eval(double m) { return m == m; }  // NaN = not evaluated
@@ -52,7 +53,28 @@ __device__ __forceinline__ double kstar_threshold(const PruneArgs& a) {
   return __longlong_as_double(static_cast<long long>(*a.kstar)) * (1.0 + kPruneSlack);
 }
 
-// ---- predict: pk[p] = sum_q KN(p, q); collinearity of every pair; state = alive ----
+// Partner order of the predictions: larger KN first, ties to the lower position.
+__device__ __forceinline__ bool key_better(unsigned long long k1, int q1, unsigned long long k2, int q2) {
+  return q2 < 0 || (q1 >= 0 && (k1 > k2 || (k1 == k2 && q1 < q2)));
+}
+
+// Lane-sorted top-K insertion (registers; K compile-time).
+template <int K>
+__device__ __forceinline__ void insert_key(unsigned long long (&bk)[K], int (&bq)[K], unsigned long long key, int q) {
+  if (!key_better(key, q, bk[K - 1], bq[K - 1])) return;  // the common case: not in the lane's top K
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    if (key_better(key, q, bk[i], bq[i])) {
+      const unsigned long long tk = bk[i];
+      const int tq = bq[i];
+      bk[i] = key, bq[i] = q;
+      key = tk, q = tq;
+    }
+  }
+}
+
+// ---- predict: pk[p] = sum_q KN(p, q); the row's kPredK strongest predicted partners (the
+// probe stage's suspects come from them); collinearity of every pair; state = alive ----
 __global__ void __launch_bounds__(256) prune_predict_kernel(const PruneArgs a) {
   const int p = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -63,6 +85,10 @@ __global__ void __launch_bounds__(256) prune_predict_kernel(const PruneArgs a) {
   const double cii = crow[vp];
   double acc = 0.0;
   bool collinear = false;
+  unsigned long long bk[kPredK];
+  int bq[kPredK];
+#pragma unroll
+  for (int i = 0; i < kPredK; ++i) bk[i] = 0ull, bq[i] = -1;
   for (int q0 = lane; q0 < a.u; q0 += 128) {
     int vq[4];
     double kv[4], cjj[4], cij[4];
@@ -82,6 +108,7 @@ __global__ void __launch_bounds__(256) prune_predict_kernel(const PruneArgs a) {
       const int q = q0 + 32 * j;
       if (q >= a.u) continue;
       acc += (q == p) ? 0.0 : kv[j];
+      if (q != p) insert_key<kPredK>(bk, bq, static_cast<unsigned long long>(__double_as_longlong(kv[j])), q);
       if (q > p) {  // pair_scales' test: the exhaustive round checks every pair
         double b1, v1, b2, v2;
         pair_vars(cii, cjj[j], cij[j], b1, v1, b2, v2);
@@ -92,6 +119,24 @@ __global__ void __launch_bounds__(256) prune_predict_kernel(const PruneArgs a) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   if (__any_sync(0xffffffffu, collinear) && lane == 0) atomicMin(a.err, err_key(a.round, kErrPairCollinear, -1));
+  int* cand = a.cand + static_cast<int64_t>(p) * kPredK;
+#pragma unroll
+  for (int r = 0; r < kPredK; ++r) {  // warp merge of the lanes' sorted lists
+    unsigned long long k = bk[0];
+    int q = bq[0];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long ok = __shfl_xor_sync(0xffffffffu, k, o);
+      const int oq = __shfl_xor_sync(0xffffffffu, q, o);
+      if (key_better(ok, oq, k, q)) k = ok, q = oq;
+    }
+    if (lane == 0) cand[r] = q;
+    if (q >= 0 && bq[0] == q) {
+#pragma unroll
+      for (int i = 0; i + 1 < kPredK; ++i) bk[i] = bk[i + 1], bq[i] = bq[i + 1];
+      bk[kPredK - 1] = 0ull, bq[kPredK - 1] = -1;
+    }
+  }
   if (lane == 0) {
     a.pk[p] = acc;
     a.state_out[p] = 1;
@@ -368,9 +413,6 @@ __global__ void __launch_bounds__(kSelThreads) prune_select_kernel(const PruneAr
 // non-top rows (largest KN, ties to the lowest position) ----
 constexpr int kMaxT = 8;
 
-__device__ __forceinline__ bool key_better(unsigned long long k1, int q1, unsigned long long k2, int q2) {
-  return q2 < 0 || (q1 >= 0 && (k1 > k2 || (k1 == k2 && q1 < q2)));
-}
 
 __global__ void __launch_bounds__(256) prune_probe_select_kernel(const PruneArgs a, int T) {
   const int p = blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -391,6 +433,30 @@ __global__ void __launch_bounds__(256) prune_probe_select_kernel(const PruneArgs
     }
     if (lane == 0) a.off[p] = written;
     return;
+  }
+  {  // the T strongest non-top partners from predict's candidate list (kPredK >= T + R)
+    const int* cand = a.cand + static_cast<int64_t>(p) * kPredK;
+    int sel[kMaxT];
+    int nsel = 0, seen = 0;
+    for (int i = 0; i < kPredK && nsel < T; ++i) {
+      const int q = cand[i];
+      if (q < 0) break;
+      ++seen;
+      if (a.state_in[q] != 2) sel[nsel++] = q;
+    }
+    if (nsel == T || seen < kPredK) {  // complete (or the row has fewer partners): done
+      if (lane == 0) {
+        for (int i = 1; i < nsel; ++i)
+          for (int j = i; j > 0 && sel[j] < sel[j - 1]; --j) {
+            const int t = sel[j];
+            sel[j] = sel[j - 1];
+            sel[j - 1] = t;
+          }
+        for (int i = 0; i < nsel; ++i) out[i] = sel[i];
+        a.off[p] = nsel;
+      }
+      return;
+    }
   }
   const double* kn = a.KN + static_cast<int64_t>(a.act[p]) * a.d;
   unsigned long long bk[kMaxT];

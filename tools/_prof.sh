@@ -1,3 +1,3 @@
-export PLG_PRUNE_SEGLEN=128
-for b in 0.8 0.9 1.0 1.05; do PLG_PRUNE_BETA=$b python tools/prune_sweep.py --config c5 --specs "4:2:0.02,0.05,0.12,0.25"; done
-PLG_PRUNE_BETA=1.0 python tools/prune_sweep.py --config c5 --specs "4:2:0.01,0.03,0.08,0.2" "4:2:0.02,0.05,0.1,0.2,0.35" "4:2:0.04,0.12,0.3" "4:3:0.02,0.05,0.12,0.25" "2:2:0.02,0.05,0.12,0.25"
+python -m pytest tests/test_gpu_prune.py -q -x 2>&1 | tail -1
+python tools/prune_sweep.py --config c5 --specs "3:1:0.03,0.1,0.3"
+ncu --metrics gpu__time_duration.sum --clock-control none --launch-skip 2200 --launch-count 1100 --csv --log-file gpurun_out/win_early.csv python tools/profile_round.py --config c5 --mode order --reps 1 > /dev/null 2>&1
