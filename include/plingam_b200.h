@@ -149,6 +149,11 @@ typedef struct plg_round_plan {
                              that of the compact small-round kernel */
 } plg_round_plan;
 int plg_plan_round(int32_t u, int64_t n, int32_t rank, int32_t world, plg_round_plan* out);
+/* Pruned rounds across ranks (host-only): each stage's pair list (identical on every rank)
+ * is split into contiguous slices; rank r evaluates entries [begin, end) and contributes a
+ * slot of `slot` entries (= ceil(total / world)) to the stage's in-place all-gather of M. */
+int plg_plan_list_shard(int32_t total, int32_t rank, int32_t world, int32_t* begin, int32_t* end,
+                        int32_t* slot);
 /* tile index -> (bi, bj), bi <= bj, row-major over the upper triangle */
 int plg_tile_decode(int32_t t, int32_t nb, int32_t* bi, int32_t* bj);
 

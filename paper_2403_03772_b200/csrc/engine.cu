@@ -440,6 +440,11 @@ int search_round_pruned(plg_ctx* c, int64_t n, int64_t ldw, int d, int u, const 
   a.batch = kPruneBatch;
   a.seg_len = sp.seg_len;
   a.nseg = sp.nseg;
+  static const int seg_major = [] {
+    const char* v = std::getenv("PLG_SEG_MAJOR");
+    return v ? std::atoi(v) : 0;
+  }();
+  a.seg_major = seg_major;
   a.g_exp = c->g_exp;
   a.g_log = c->g_log;
   a.err = c->err.p;
@@ -477,11 +482,13 @@ int search_round_pruned(plg_ctx* c, int64_t n, int64_t ldw, int d, int u, const 
       int total = 0;
       PLG_CUDA(cudaMemcpyAsync(&total, c->off.p + u, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
       PLG_CUDA(cudaStreamSynchronize(c->stream));
-      const int cnt = (total + shards - 1) / shards;
+      int32_t cnt = 0, kb = 0, ke = 0;
+      plg_plan_list_shard(total, 0, shards, &kb, &ke, &cnt);
       a.res = c->pres.p;
       for (int r = (c->world > 1 ? c->rank : 0); r < (c->world > 1 ? c->rank + 1 : shards); ++r) {
-        a.k_begin = std::min(total, r * cnt);
-        a.k_end = std::min(total, (r + 1) * cnt);
+        plg_plan_list_shard(total, r, shards, &kb, &ke, &cnt);
+        a.k_begin = kb;
+        a.k_end = ke;
         if (r > (c->world > 1 ? c->rank : 0))  // emulated ranks share one set of fetch counters
           PLG_CUDA(cudaMemsetAsync(c->pwork.p, 0, (kPruneBatch > 0 ? (cnt / kPruneBatch + 2) : 2) * sizeof(int),
                                    c->stream));
@@ -1097,6 +1104,16 @@ int plg_plan_round(int32_t u, int64_t n, int32_t rank, int32_t world, plg_round_
   out->nseg = rp.seg.nseg;
   out->seg_len = rp.seg.seg_len;
   out->replicated = rp.replicated ? 1 : 0;
+  return 0;
+}
+
+int plg_plan_list_shard(int32_t total, int32_t rank, int32_t world, int32_t* begin, int32_t* end,
+                        int32_t* slot) {
+  if (world < 1 || rank < 0 || rank >= world || total < 0 || !begin || !end || !slot) return PLG_OutOfRange;
+  const int32_t cnt = (total + world - 1) / world;
+  *slot = cnt;
+  *begin = std::min(total, rank * cnt);
+  *end = std::min(total, (rank + 1) * cnt);
   return 0;
 }
 

@@ -163,6 +163,7 @@ struct PruneArgs {
   int batch;                    // pairs per batch of the list kernel
   int seg_len;
   int nseg;
+  int seg_major;                // pair-list item order: segment-major (1) or chunk-major (0)
   const double* g_exp;
   const double2* g_log;
   unsigned long long* err;

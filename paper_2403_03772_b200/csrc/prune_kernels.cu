@@ -709,8 +709,14 @@ __global__ void __launch_bounds__(kListThreads, 2) prune_pairs_kernel(const Prun
       if (lane == 0) it = atomicAdd(&a.work[b], 1);
       it = __shfl_sync(0xffffffffu, it, 0);
       if (it >= items) break;
-      const int chunk = it / a.nseg;
-      const int seg = it - chunk * a.nseg;
+      int chunk, seg;
+      if (a.seg_major) {  // a sample window of every chunk at a time: column slices stay in L2
+        seg = it / chunks;
+        chunk = it - seg * chunks;
+      } else {  // a chunk's segments back to back: its partial sums stay in L2
+        chunk = it / a.nseg;
+        seg = it - chunk * a.nseg;
+      }
       const int kk = chunk * 32 + lane;
       if (kk < m) {
         int p, q;
