@@ -109,7 +109,9 @@ __global__ void __launch_bounds__(256) prune_predict_kernel(const PruneArgs a) {
       if (q >= a.u) continue;
       acc += (q == p) ? 0.0 : kv[j];
       if (q != p) insert_key<kPredK>(bk, bq, static_cast<unsigned long long>(__double_as_longlong(kv[j])), q);
-      if (q > p) {  // pair_scales' test: the exhaustive round checks every pair
+      // pair_scales' test (the exhaustive round checks every pair). Pairs with
+      // C_ij^2 < C_ii C_jj (1 - 1e-6) have both residual variances > 0 whatever the rounding.
+      if (q > p && !(cij[j] * cij[j] < cii * cjj[j] * (1.0 - 1e-6))) {
         double b1, v1, b2, v2;
         pair_vars(cii, cjj[j], cij[j], b1, v1, b2, v2);
         collinear |= pair_collinear(v1, v2);
@@ -379,31 +381,54 @@ __global__ void __launch_bounds__(kSelThreads) prune_select_kernel(const PruneAr
     cut_bin = s_cut[0];
     cut_take = s_cut[1];
   }
-  // emit in ascending q: bins above the cut, then the first cut_take of the cut bin
+  // Emit in ascending q: bins above the cut, then the first cut_take of the cut bin. Each warp
+  // owns a contiguous range of partners: it counts its selections, one block barrier gives
+  // the warps' offsets, then it writes its range in order with ballots (no further barrier).
   int* out = a.rowsel + static_cast<int64_t>(p) * u;
-  int written = 0, taken_cut = 0;
-  for (int base = 0; base < u; base += kSelThreads) {
-    const int q = base + threadIdx.x;
-    bool sel = false, in_cut = false;
-    if (q < u && eligible(q)) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int kWarps = kSelThreads / 32;
+  const int span = ((u + kWarps - 1) / kWarps + 31) & ~31;
+  const int q_lo = warp * span, q_hi = min(u, q_lo + span);
+  auto classify = [&](int q, bool& above, bool& in_cut) {
+    above = in_cut = false;
+    if (q < q_hi && eligible(q)) {
       if (cut_bin < 0) {
-        sel = true;
+        above = true;
       } else {
         const int b = key_bin(kn[a.act[q]]);
-        sel = b > cut_bin;
+        above = b > cut_bin;
         in_cut = (b == cut_bin);
       }
     }
-    if (cut_bin >= 0) {
-      int rk;
-      const int nc = block_prefix(in_cut, s_warp, rk);
-      if (in_cut && taken_cut + rk < cut_take) sel = true;
-      taken_cut += nc;
-    }
-    int pos;
-    const int ns = block_prefix(sel, s_warp, pos);
-    if (sel) out[written + pos] = q;
-    written += ns;
+  };
+  int n_above = 0, n_cut = 0;
+  for (int base = q_lo; base < q_hi; base += 32) {
+    bool ab, ic;
+    classify(base + lane, ab, ic);
+    n_above += __popc(__ballot_sync(0xffffffffu, ab));
+    n_cut += __popc(__ballot_sync(0xffffffffu, ic));
+  }
+  __shared__ int s_above[kWarps], s_cut_n[kWarps];
+  if (lane == 0) s_above[warp] = n_above, s_cut_n[warp] = n_cut;
+  __syncthreads();
+  int cut_seen = 0, out_before = 0, written = 0, cut_before = 0;
+  for (int w = 0; w < kWarps; ++w) {  // warp w takes the cut-bin entries ranked [cut_seen, ...)
+    const int take_w = max(0, min(s_cut_n[w], cut_take - cut_seen));
+    if (w < warp) out_before += s_above[w] + take_w, cut_before += s_cut_n[w];
+    written += s_above[w] + take_w;
+    cut_seen += s_cut_n[w];
+  }
+  int pos = out_before, cut_rank = cut_before;
+  for (int base = q_lo; base < q_hi; base += 32) {
+    bool ab, ic;
+    classify(base + lane, ab, ic);
+    const unsigned lt = (1u << lane) - 1u;
+    const unsigned bc = __ballot_sync(0xffffffffu, ic);
+    const bool sel = ab || (ic && cut_rank + __popc(bc & lt) < cut_take);
+    const unsigned bs = __ballot_sync(0xffffffffu, sel);
+    if (sel) out[pos + __popc(bs & lt)] = base + lane;
+    pos += __popc(bs);
+    cut_rank += __popc(bc);
   }
   if (threadIdx.x == 0) a.off[p] = written;
 }
@@ -665,7 +690,8 @@ __device__ __forceinline__ void finalize_chunk(const PruneArgs& a, const double*
   double l1 = 0.0, p1 = 0.0, l2 = 0.0, p2 = 0.0;
   const double2* src = reinterpret_cast<const double2*>(part + static_cast<int64_t>(kk) * 4);
   const int64_t stride = static_cast<int64_t>(a.batch) * 2;  // double2 per segment
-  for (int s = 0; s < a.nseg; ++s) {
+#pragma unroll 8
+  for (int s = 0; s < a.nseg; ++s) {  // loads run ahead; the adds stay in ascending order
     const double2 v1 = __ldcg(src);  // written by other SMs: bypass L1
     const double2 v2 = __ldcg(src + 1);
     l1 += v1.x;

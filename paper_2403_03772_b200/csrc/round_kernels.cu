@@ -260,7 +260,9 @@ __global__ void update_gram_kernel(double* C, int64_t ldc, const int* act_nxt, i
   const int m = rs->chosen_col;
   const int r = act_nxt[a], s = act_nxt[b];
   const double cmm = C[static_cast<int64_t>(m) * ldc + m];
-  const double prod = C[static_cast<int64_t>(r) * ldc + m] * C[static_cast<int64_t>(s) * ldc + m];
+  // C_sm read from row m (C is bit-symmetric): contiguous over s, where column m would be a
+  // strided gather; the product commutes, so C stays bit-symmetric
+  const double prod = C[static_cast<int64_t>(r) * ldc + m] * C[static_cast<int64_t>(m) * ldc + s];
   const double v = C[static_cast<int64_t>(r) * ldc + s] - prod / cmm;
   C[static_cast<int64_t>(r) * ldc + s] = v;
 }
