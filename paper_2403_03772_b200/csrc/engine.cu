@@ -184,10 +184,11 @@ struct plg_ctx {
   bool prune = true;
   int prune_R = 3;
   int prune_T = 1;
-  std::vector<double> prune_fracs{0.03, 0.1, 0.3};
+  std::vector<double> prune_fracs{0.05, 0.25};
   bool prune_tile_seg = false;  // PLG_PRUNE_TILESEG=1: the exhaustive rounds' segmentation (bit-identity tests)
   int emulate_world = 1;        // PLG_EMULATE_WORLD=W (tests): a single rank runs the W-rank shard schedule
   double prune_beta = 1.1;      // PLG_PRUNE_BETA > 0: hybrid refinement (deficit cut when smaller than the step)
+  int64_t prune_sub = 0;        // PLG_PRUNE_SUB: samples of round 0's prediction pass (0: exhaustive round 0)
   DevBuf<double> Md, KN, pk, L, ppart, pres;
   DevBuf<int> st0, st1, rowsel, off, pwork, pdone, crow, cand;
   DevBuf<unsigned long long> kstar, evals;
@@ -271,6 +272,7 @@ void parse_prune_env(plg_ctx* ctx) {
   if (const char* v = std::getenv("PLG_PRUNE_TILESEG")) ctx->prune_tile_seg = !strcmp(v, "1");
   if (const char* v = std::getenv("PLG_EMULATE_WORLD")) ctx->emulate_world = std::max(1, std::atoi(v));
   if (const char* v = std::getenv("PLG_PRUNE_BETA")) ctx->prune_beta = std::atof(v);
+  if (const char* v = std::getenv("PLG_PRUNE_SUB")) ctx->prune_sub = std::max<int64_t>(0, std::atoll(v));
 }
 
 int ctx_init(plg_ctx* ctx, int device, plg_status* st) {
@@ -411,8 +413,8 @@ int search_round(plg_ctx* c, int64_t n, int64_t ldw, int ldc, int u, const int* 
 // search_round, evaluating only the pairs needed to prove the argmin. Needs KN from an
 // earlier round of the same run.
 int search_round_pruned(plg_ctx* c, int64_t n, int64_t ldw, int d, int u, const int* act_cur, int round,
-                        plg_status* st) {
-  round_entropies(c, n, ldw, d, u, act_cur, round, true);
+                        plg_status* st, bool h_from_resid = true) {
+  round_entropies(c, n, ldw, d, u, act_cur, round, h_from_resid);
   const SegPlan sp = c->prune_tile_seg ? seg_plan(u, n) : prune_seg_plan(n);
   PLG_CUDA(cudaMemsetAsync(c->Md.p, 0xff, static_cast<size_t>(u) * u * sizeof(double), c->stream));
   plg::PruneArgs a{};
@@ -702,7 +704,15 @@ int causal_order_impl(plg_ctx* c, const double* dX, int64_t ldx, int64_t n, int 
     const int u = d - r;
     int* act_cur = (r & 1) ? c->act1.p : c->act0.p;
     int* act_nxt = (r & 1) ? c->act0.p : c->act1.p;
-    if (prune && r > 0 && u > plg::kSmallU) {
+    if (prune && r == 0 && c->prune_sub > 0 && n >= 2 * c->prune_sub) {
+      // Round 0 has no earlier round to predict from: an exhaustive round over the first
+      // prune_sub samples (its M are estimates, used only as predictions, KN) and then an
+      // exact pruned round over all n samples.
+      const int64_t before = c->pairs_done;
+      if (int rc = search_round(c, c->prune_sub, ldw, d, u, act_cur, r, st, c->KN.p, false)) return rc;
+      c->pairs_done = before + (c->pairs_done - before) * c->prune_sub / n;  // in full-n pair units
+      if (int rc = search_round_pruned(c, n, ldw, d, u, act_cur, r, st, false)) return rc;
+    } else if (prune && r > 0 && u > plg::kSmallU) {
       if (int rc = search_round_pruned(c, n, ldw, d, u, act_cur, r, st)) return rc;
     } else if (int rc = search_round(c, n, ldw, d, u, act_cur, r, st, (prune && r == 0) ? c->KN.p : nullptr,
                                      r > 0)) {

@@ -248,27 +248,46 @@ __device__ __forceinline__ int block_prefix(bool pred, int* s_warp, int& excl) {
 // on exponent bins of the predicted value (2^k granularity) with fixed-point weights, so it
 // is deterministic; inside the boundary bin partners are taken in ascending position.
 __global__ void __launch_bounds__(kSelThreads) prune_select_kernel(const PruneArgs a, int stage, int m,
-                                                                   double beta) {
+                                                                   double beta, int cache_keys) {
   __shared__ int hist[kBins];
   __shared__ unsigned long long wt[kBins];
   __shared__ int s_warp[kSelThreads / 32];
   __shared__ int s_cut[2];  // boundary bin, entries of it to take
   __shared__ double s_red[kSelThreads / 32];
+  extern __shared__ double s_key[];  // cache_keys: per partner, its prediction or -1 (not eligible)
   const int p = blockIdx.x;
   const int u = a.u;
   const int st = a.state_in[p];
   const double thr = (stage == kStageProbe) ? 0.0 : kstar_threshold(a);
   const double* md = a.Md + static_cast<int64_t>(p) * u;
-  // Refinement / full stages: the row's partial k over its evaluated partners (a lower bound
-  // of its k whatever the summation order; fixed block shape, so deterministic).
+  const double* kn = a.KN + static_cast<int64_t>(a.act[p]) * a.d;
+  const bool refine = (stage != kStageProbe);
+  // One pass over the row (refinement / full stages): the partial k over the evaluated
+  // partners (a lower bound of k whatever the summation order; fixed block shape, so
+  // deterministic) and, when cached, every unevaluated partner's prediction. Loads are
+  // issued 8 per thread at a time (the gather kn[act[q]] depends on act[q]).
   double Lp = 0.0;
-  if (stage != kStageProbe && st == 1) {
+  if (refine && st == 1) {
     double acc = 0.0;
-    for (int q = threadIdx.x; q < u; q += kSelThreads) {
-      const double mi = md[q];
-      if (q != p && is_eval(mi)) {
-        const double c = (mi < 0.0) ? mi : 0.0;
-        acc = __dadd_rn(acc, __dmul_rn(c, c));
+    constexpr int kB = 8;
+    for (int q0 = threadIdx.x; q0 < u; q0 += kB * kSelThreads) {
+      double mi[kB];
+      int vq[kB];
+#pragma unroll
+      for (int j = 0; j < kB; ++j) {
+        const int q = q0 + j * kSelThreads;
+        mi[j] = q < u ? md[q] : 0.0;
+        vq[j] = (cache_keys && q < u) ? a.act[q] : 0;
+      }
+#pragma unroll
+      for (int j = 0; j < kB; ++j) {
+        const int q = q0 + j * kSelThreads;
+        if (q >= u) continue;
+        if (q != p && is_eval(mi[j])) {
+          const double c = (mi[j] < 0.0) ? mi[j] : 0.0;
+          acc = __dadd_rn(acc, __dmul_rn(c, c));
+        }
+        if (cache_keys) s_key[q] = (q == p || is_eval(mi[j])) ? -1.0 : kn[vq[j]];
       }
     }
 #pragma unroll
@@ -278,7 +297,7 @@ __global__ void __launch_bounds__(kSelThreads) prune_select_kernel(const PruneAr
     for (int w = 0; w < kSelThreads / 32; ++w) Lp += s_red[w];
   }
   bool active = false, full = false;
-  if (stage == kStageProbe) {
+  if (!refine) {
     active = true;
     full = (st == 2);
   } else {
@@ -286,19 +305,21 @@ __global__ void __launch_bounds__(kSelThreads) prune_select_kernel(const PruneAr
     full = (stage == kStageFull);
   }
   if (threadIdx.x == 0) {
-    a.state_out[p] = (st == 1 && stage != kStageProbe && !active) ? 0 : st;
-    if (stage != kStageProbe) a.L[p] = Lp;
+    a.state_out[p] = (st == 1 && refine && !active) ? 0 : st;
+    if (refine) a.L[p] = Lp;
     if (!active) a.off[p] = 0;
   }
   if (!active) return;
-  const double* kn = a.KN + static_cast<int64_t>(a.act[p]) * a.d;
+  const bool cached = cache_keys && refine;
   // A pair of two full rows is listed twice in the full stage (both rows are still alive,
   // rare); its two evaluations have identical bits and the same writes.
   auto eligible = [&](int q) -> bool {
+    if (cached) return s_key[q] >= 0.0;
     if (q == p || is_eval(md[q])) return false;
     if (stage == kStageProbe) return full ? !(a.state_in[q] == 2 && q < p) : a.state_in[q] != 2;
     return true;
   };
+  auto key_of = [&](int q) -> double { return cached ? s_key[q] : kn[a.act[q]]; };
   // Modes: count (beta <= 0): the m strongest; deficit (m <= 0): strongest until their
   // predicted sum reaches beta x deficit, else all; hybrid (both): the deficit cut when it
   // needs fewer than m partners, else the m strongest.
@@ -313,7 +334,7 @@ __global__ void __launch_bounds__(kSelThreads) prune_select_kernel(const PruneAr
     for (int q0 = 0; q0 < u; q0 += kSelThreads) {  // warp-aggregated bin increments
       const int q = q0 + threadIdx.x;
       const bool e = q < u && eligible(q);
-      const double v = e ? kn[a.act[q]] : 0.0;
+      const double v = e ? key_of(q) : 0.0;
       const int b = e ? key_bin(v) : -1;
       const unsigned grp = __match_any_sync(0xffffffffu, b);
       const int leader = __ffs(grp) - 1;
@@ -395,7 +416,7 @@ __global__ void __launch_bounds__(kSelThreads) prune_select_kernel(const PruneAr
       if (cut_bin < 0) {
         above = true;
       } else {
-        const int b = key_bin(kn[a.act[q]]);
+        const int b = key_bin(key_of(q));
         above = b > cut_bin;
         in_cut = (b == cut_bin);
       }
@@ -856,7 +877,16 @@ void launch_prune_top(const PruneArgs& a, int R, cudaStream_t s) {
 
 void launch_prune_select(const PruneArgs& a, int stage, int m, double beta, cudaStream_t s) {
   if (stage == kStageProbe) prune_probe_select_kernel<<<(a.u + 7) / 8, 256, 0, s>>>(a, m < kMaxT ? m : kMaxT);
-  else prune_select_kernel<<<a.u, kSelThreads, 0, s>>>(a, stage, m, beta);
+  else {
+    // the row's predictions cached in shared memory (u <= 24 576; larger rows re-read them)
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(prune_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 24576 * 8);
+      attr = true;
+    }
+    const int cache = a.u <= 24576 ? 1 : 0;
+    prune_select_kernel<<<a.u, kSelThreads, cache ? a.u * sizeof(double) : 0, s>>>(a, stage, m, beta, cache);
+  }
 }
 
 void launch_prune_scan(const PruneArgs& a, cudaStream_t s) { prune_scan_kernel<<<1, 1024, 0, s>>>(a); }
