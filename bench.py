@@ -43,6 +43,16 @@ LIBDEVICE_OPS_PER_EDE = 70  # SURVEY.md §8d algorithmic basis (libdevice exp/lo
 FP64_PEAK_TFLOPS = 33.85  # measured DFMA microbenchmark on this pool's B200 (tools/probe/fp64_peak.cu)
 
 
+def _hbm_peak():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except (OSError, ValueError, KeyError):
+        return 7700.0  # B200_PROFILING.md fallback
+
+
+HBM_PEAK_GBS = _hbm_peak()
+
+
 def pair_evals(d: int) -> int:
     return (d + 1) * d * (d - 1) // 3
 
@@ -235,6 +245,7 @@ def run_ours(args, world, rank, local):
     barrier(world)
 
     dev_ms, pair_ms, launches, pair_launches, pairs_done = [], [], 0, 0, 0
+    resid_ms, resid_bytes = 0.0, 0
     with ClockSampler(local) as clocks:
         barrier(world)
         t0 = time.perf_counter()
@@ -246,6 +257,8 @@ def run_ours(args, world, rank, local):
             launches += st["launches"]
             pair_launches += st["pair_launches"]
             pairs_done += st["pairs_evaluated"]
+            resid_ms += st["resid_ms"]
+            resid_bytes += st["resid_bytes"]
         barrier(world)
         wall = time.perf_counter() - t0
     clk = clocks.summary()
@@ -310,7 +323,18 @@ def run_ours(args, world, rank, local):
                               f"per step); peak = measured DFMA rate (no FP64 figure in MEASURED_PEAKS.json)",
                      "libdevice_basis_frac": (LIBDEVICE_OPS_PER_EDE * 2 * ede / (pair_s * world) / 1e12)
                      / FP64_PEAK_TFLOPS if pair_s > 0 else None,
-                     "pair_share_of_step": pair_s / (dev_s / args.steps)},
+                     "pair_share_of_step": pair_s / (dev_s / args.steps),
+                     "residualize": {
+                         "bound": "hbm", "kernel": "resid_ent_kernel (residualisation + next round's column "
+                                                   "entropies, fused)",
+                         "unit": "GB/s", "achieved": resid_bytes / (resid_ms / 1e3) / 1e9 if resid_ms > 0 else None,
+                         "peak": HBM_PEAK_GBS,
+                         "frac": (resid_bytes / (resid_ms / 1e3) / 1e9) / HBM_PEAK_GBS if resid_ms > 0 else None,
+                         "bytes_per_step": resid_bytes / args.steps,
+                         "share_of_step": resid_ms / 1e3 / dev_s,
+                         "note": "algorithmic bytes (2(u-1)+1) n 8 per round (read + write of the u-1 "
+                                 "remaining columns, one read of the root); the same pass evaluates "
+                                 "(u-1) n EDE of column entropies, so the kernel is not purely HBM-bound"}},
         "e2e": {"value": P * args.steps / e2e_s, "unit": "pair-evals/s",
                 "h2d_bytes_per_step": int(st_e2e["h2d_bytes"]), "d2h_bytes_per_step": int(st_e2e["d2h_bytes"]),
                 "wall_s_per_step": e2e_s / args.steps},

@@ -63,6 +63,9 @@ typedef struct plg_stats {
   int32_t world;
   int64_t h2d_bytes;
   int64_t d2h_bytes;
+  double resid_ms;      /* device time of the residualisation launches (fused with the next
+                           round's column entropies) */
+  int64_t resid_bytes;  /* their algorithmic HBM bytes: (2 (u - 1) + 1) n 8 per round */
 } plg_stats;
 
 typedef struct plg_ctx plg_ctx;

@@ -193,7 +193,9 @@ struct plg_ctx {
   DevBuf<int> st0, st1, rowsel, off, pwork, pdone, crow, cand;
   DevBuf<unsigned long long> kstar, evals;
 
-  size_t ev_pairs = 0;  // pair-kernel timing intervals recorded by this call (ev[3 + 2 i], ev[4 + 2 i])
+  size_t ev_pairs = 0;  // timing intervals recorded by this call (ev[3 + 2 i], ev[4 + 2 i])
+  std::vector<char> ev_kind;  // per interval: 0 pair evaluation, 1 residualisation
+  int64_t resid_bytes = 0;    // algorithmic HBM bytes of the residualisations of this call
 
   cudaError_t events(size_t count) {
     while (ev.size() < count) {
@@ -209,10 +211,12 @@ struct plg_ctx {
 namespace {
 
 // CUDA-event interval around one pair-evaluation launch (plg_stats.pair_ms / pair_launches).
-size_t pair_timer_begin(plg_ctx* c) {
+size_t pair_timer_begin(plg_ctx* c, char kind = 0) {
   if (!c->timing) return 0;
   const size_t i = 3 + 2 * c->ev_pairs;
   if (c->events(i + 2) != cudaSuccess) return 0;
+  if (c->ev_kind.size() <= c->ev_pairs) c->ev_kind.resize(c->ev_pairs + 1);
+  c->ev_kind[c->ev_pairs] = kind;
   cudaEventRecord(c->ev[i], c->stream);
   return i;
 }
@@ -563,7 +567,7 @@ int reserve_run(plg_ctx* c, int64_t n, int ncols, int64_t ldw, plg_status* st) {
   PLG_CUDA(c->msd.reserve(2 * static_cast<size_t>(ncols)));
   PLG_CUDA(c->idx.reserve(ncols));
   PLG_CUDA(c->nz.reserve(ncols));
-  PLG_CUDA(c->events(3 + 2 * static_cast<size_t>(std::max(ncols, 1)) * (3 + c->prune_fracs.size())));
+  PLG_CUDA(c->events(3 + 2 * static_cast<size_t>(std::max(ncols, 1)) * (4 + c->prune_fracs.size())));
   return 0;
 }
 
@@ -646,12 +650,21 @@ void finish_stats(plg_ctx* c, int64_t n, int d, int rounds, bool host_in) {
     cudaEventElapsedTime(&ms, c->ev[0], c->ev[2]);
     s.h2d_ms = ms;
   }
-  double pair_ms = 0.0;
+  double pair_ms = 0.0, resid_ms = 0.0;
+  int64_t pl = 0;
   for (size_t i = 0; i < c->ev_pairs; ++i) {
-    if (cudaEventElapsedTime(&ms, c->ev[3 + 2 * i], c->ev[4 + 2 * i]) == cudaSuccess) pair_ms += ms;
+    if (cudaEventElapsedTime(&ms, c->ev[3 + 2 * i], c->ev[4 + 2 * i]) != cudaSuccess) continue;
+    if (c->ev_kind[i] == 1) {
+      resid_ms += ms;
+    } else {
+      pair_ms += ms;
+      ++pl;
+    }
   }
   s.pair_ms = pair_ms;
-  s.pair_launches = static_cast<int64_t>(c->ev_pairs);
+  s.pair_launches = pl;
+  s.resid_ms = resid_ms;
+  s.resid_bytes = c->resid_bytes;
 }
 
 // Analysis hook: copy the round's full entropy table to the host as a dense u x u matrix
@@ -726,8 +739,12 @@ int causal_order_impl(plg_ctx* c, const double* dX, int64_t ldx, int64_t n, int 
     if (u - 1 >= 2 || (u - 1 == 1 && max_rounds >= 0)) {
       // the next round's build_cache check only exists when it has >= 2 candidates
       plg::launch_update_gram(c->C.p, d, act_nxt, u - 1, c->rs.p, c->err.p, c->stream);
+      const size_t tr = pair_timer_begin(c, 1);
       plg::launch_resid_ent(c->W.p, ldw, n, c->C.p, d, act_nxt, u - 1, c->rs.p, c->nz.p, r + 1, c->err.p,
                             c->hpart.p, c->g_exp, c->g_log, c->stream);
+      pair_timer_end(c, tr);
+      // read w_r, write w_r for the u - 1 remaining columns, read w_m once
+      c->resid_bytes += (2 * static_cast<int64_t>(u - 1) + 1) * n * static_cast<int64_t>(sizeof(double));
       c->launches += 2;
     }
   }
@@ -760,6 +777,7 @@ int begin_call(plg_ctx* c, plg_status* st) {
   PLG_CUDA(cudaSetDevice(c->device));
   c->launches = 0;
   c->ev_pairs = 0;
+  c->resid_bytes = 0;
   c->last = plg_stats{};
   if (c->timing) {
     PLG_CUDA(c->events(3));

@@ -551,6 +551,8 @@ PYBIND11_MODULE(_core, m) {
         d["world"] = s.world;
         d["h2d_bytes"] = s.h2d_bytes;
         d["d2h_bytes"] = s.d2h_bytes;
+        d["resid_ms"] = s.resid_ms;
+        d["resid_bytes"] = s.resid_bytes;
         return d;
       });
 }

@@ -426,9 +426,13 @@ __global__ void __launch_bounds__(kResidThreads)
     const int64_t t0 = c * chunk, t1 = lmin(n, t0 + chunk);  // samples; chunk is even
     EdeAcc acc;
     bool any = false;
-    for (int64_t t = t0 + 2 * lane; t < t1; t += 64) {
-      const double2 x = wr[t >> 1];
-      const double2 y = wm[t >> 1];
+    // loads of the next step issued before this step's element math (latency-bound otherwise)
+    int64_t t = t0 + 2 * lane;
+    double2 xn = make_double2(0.0, 0.0), yn = xn;
+    if (t < t1) xn = wr[t >> 1], yn = wm[t >> 1];
+    for (; t < t1; t += 64) {
+      const double2 x = xn, y = yn;
+      if (t + 64 < t1) xn = wr[(t + 64) >> 1], yn = wm[(t + 64) >> 1];
       const double2 o = make_double2(__dsub_rn(x.x, __dmul_rn(beta, y.x)), __dsub_rn(x.y, __dmul_rn(beta, y.y)));
       wr[t >> 1] = o;
       any |= (o.x != 0.0) | (o.y != 0.0);
