@@ -646,17 +646,25 @@ __device__ __forceinline__ void eval_segment(const double* wi, const double* wj,
   auto ld = [](const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); };
   int64_t t = t0;
   if (kVar == 0) {
-    if (t + 3 < t1) {
-      double2 xa = ld(wi + t), xb = ld(wi + t + 2), ya = ld(wj + t), yb = ld(wj + t + 2);
+    // pointer increments and a 32-bit step count keep the address arithmetic out of the
+    // register-starved loop (index arithmetic was rematerialised every step)
+    const int nstep = static_cast<int>((t1 - t) >> 2);
+    if (nstep > 0) {
+      const double2* pi = reinterpret_cast<const double2*>(wi + t);
+      const double2* pj = reinterpret_cast<const double2*>(wj + t);
+      double2 xa = __ldg(pi), xb = __ldg(pi + 1), ya = __ldg(pj), yb = __ldg(pj + 1);
 #pragma unroll 1
-      for (; t + 3 < t1; t += 4) {
+      for (int i = 1; i <= nstep; ++i) {
         const double2 cxa = xa, cxb = xb, cya = ya, cyb = yb;
-        if (t + 7 < t1) xa = ld(wi + t + 4), xb = ld(wi + t + 6), ya = ld(wj + t + 4), yb = ld(wj + t + 6);
+        pi += 2;
+        pj += 2;
+        if (i < nstep) xa = __ldg(pi), xb = __ldg(pi + 1), ya = __ldg(pj), yb = __ldg(pj + 1);
         ede2<kClampA>(cxa.x, cya.x, s1, bs1, s2, bs2, acc1, acc2, tp);
         ede2<kClampA>(cxa.y, cya.y, s1, bs1, s2, bs2, acc1, acc2, tp);
         ede2<kClampA>(cxb.x, cyb.x, s1, bs1, s2, bs2, acc1, acc2, tp);
         ede2<kClampA>(cxb.y, cyb.y, s1, bs1, s2, bs2, acc1, acc2, tp);
       }
+      t += 4 * static_cast<int64_t>(nstep);
     }
   } else if (kVar == 1) {
     if (t + 5 < t1) {
