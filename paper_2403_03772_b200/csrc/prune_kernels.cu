@@ -666,32 +666,42 @@ __device__ __forceinline__ void eval_segment(const double* wi, const double* wj,
       }
       t += 4 * static_cast<int64_t>(nstep);
     }
-  } else if (kVar == 1) {
-    if (t + 5 < t1) {
-      double2 x0 = ld(wi + t), y0 = ld(wj + t), x1 = ld(wi + t + 2), y1 = ld(wj + t + 2);
+  } else if (kVar == 1) {  // 2 samples per step, loads 2 steps ahead
+    const int nstep = static_cast<int>((t1 - t) >> 1);
+    if (nstep > 0) {
+      const double2* pi = reinterpret_cast<const double2*>(wi + t);
+      const double2* pj = reinterpret_cast<const double2*>(wj + t);
+      double2 x0 = __ldg(pi), y0 = __ldg(pj), x1 = x0, y1 = y0;
+      if (nstep > 1) x1 = __ldg(pi + 1), y1 = __ldg(pj + 1);
 #pragma unroll 1
-      for (; t + 1 < t1; t += 2) {
+      for (int i = 2; i < nstep + 2; ++i) {
         const double2 cx = x0, cy = y0;
         x0 = x1, y0 = y1;
-        if (t + 5 < t1) x1 = ld(wi + t + 4), y1 = ld(wj + t + 4);
+        if (i < nstep) x1 = __ldg(pi + i), y1 = __ldg(pj + i);
         ede2<kClampA>(cx.x, cy.x, s1, bs1, s2, bs2, acc1, acc2, tp);
         ede2<kClampA>(cx.y, cy.y, s1, bs1, s2, bs2, acc1, acc2, tp);
       }
+      t += 2 * static_cast<int64_t>(nstep);
     }
-  } else {
-    if (t + 7 < t1) {
-      double2 xa = ld(wi + t), xb = ld(wi + t + 2), ya = ld(wj + t), yb = ld(wj + t + 2);
-      double2 xc = ld(wi + t + 4), xd = ld(wi + t + 6), yc = ld(wj + t + 4), yd = ld(wj + t + 6);
+  } else {  // 4 samples per step, loads 2 steps ahead
+    const int nstep = static_cast<int>((t1 - t) >> 2);
+    if (nstep > 0) {
+      const double2* pi = reinterpret_cast<const double2*>(wi + t);
+      const double2* pj = reinterpret_cast<const double2*>(wj + t);
+      double2 xa = __ldg(pi), xb = __ldg(pi + 1), ya = __ldg(pj), yb = __ldg(pj + 1);
+      double2 xc = xa, xd = xb, yc = ya, yd = yb;
+      if (nstep > 1) xc = __ldg(pi + 2), xd = __ldg(pi + 3), yc = __ldg(pj + 2), yd = __ldg(pj + 3);
 #pragma unroll 1
-      for (; t + 3 < t1; t += 4) {
+      for (int i = 2; i < nstep + 2; ++i) {
         const double2 cxa = xa, cxb = xb, cya = ya, cyb = yb;
         xa = xc, xb = xd, ya = yc, yb = yd;
-        if (t + 11 < t1) xc = ld(wi + t + 8), xd = ld(wi + t + 10), yc = ld(wj + t + 8), yd = ld(wj + t + 10);
+        if (i < nstep) xc = __ldg(pi + 2 * i), xd = __ldg(pi + 2 * i + 1), yc = __ldg(pj + 2 * i), yd = __ldg(pj + 2 * i + 1);
         ede2<kClampA>(cxa.x, cya.x, s1, bs1, s2, bs2, acc1, acc2, tp);
         ede2<kClampA>(cxa.y, cya.y, s1, bs1, s2, bs2, acc1, acc2, tp);
         ede2<kClampA>(cxb.x, cyb.x, s1, bs1, s2, bs2, acc1, acc2, tp);
         ede2<kClampA>(cxb.y, cyb.y, s1, bs1, s2, bs2, acc1, acc2, tp);
       }
+      t += 4 * static_cast<int64_t>(nstep);
     }
   }
   for (; t < t1; ++t) ede2<kClampA>(wi[t], wj[t], s1, bs1, s2, bs2, acc1, acc2, tp);
