@@ -91,3 +91,40 @@ def test_pruned_rounds_sharded_schedule(world):
     r = _run(300, 4000, 7, "laplace", tileseg=True, emulate_world=world)
     assert r["prune"]["order"] == r["full"]["order"]
     assert r["prune"]["k"] == r["full"]["k"]
+
+
+_ERR_CHILD = r"""
+import json, sys
+sys.path.insert(0, %r)
+import numpy as np
+import paper_2403_03772_b200 as plg
+rng = np.random.default_rng(%d)
+d, n, kind = %d, %d, %r
+X = np.asfortranarray(rng.laplace(size=(n, d)))
+if kind == "dup":          # an exact duplicate: the round after one of them is chosen raises
+    X[:, d - 3] = X[:, 5]
+elif kind == "affine":     # exact affine copy: same standardised column
+    X[:, d - 7] = 2.5 * X[:, 11] - 1.0
+eng = plg.Engine(0)
+out = {}
+for mode in ("prune", "full"):
+    eng.set_prune(mode == "prune")
+    try:
+        out[mode] = {"order": eng.causal_order(X)}
+    except plg.Error as e:
+        out[mode] = {"code": e.code, "row": e.row, "col": e.col}
+print(json.dumps(out))
+"""
+
+
+@pytest.mark.parametrize("seed,d,n,kind", [(1, 150, 500, "dup"), (2, 140, 301, "affine"), (3, 130, 257, "none"),
+                                           (4, 131, 130, "none")])
+def test_pruned_rounds_edge_cases_match_exhaustive(seed, d, n, kind):
+    # boundary sizes (one or two pruned rounds, n below one segment, odd n) and the
+    # collinearity errors raised mid-run: same order, or the same error, as the exhaustive path
+    out = subprocess.run([sys.executable, "-c", _ERR_CHILD % (ROOT, seed, d, n, kind)], capture_output=True,
+                         text=True, check=True, timeout=600)
+    r = json.loads(out.stdout.strip().splitlines()[-1])
+    assert r["prune"] == r["full"], r
+    if kind != "none":
+        assert r["prune"].get("code") == "ZeroVariance", r
