@@ -713,7 +713,15 @@ int causal_order_impl(plg_ctx* c, const double* dX, int64_t ldx, int64_t n, int 
   c->pairs_done = 0;
   if (prune)
     if (int rc = reserve_prune(c, n, d, st)) return rc;
+  // PLG_ROUND_TIMES=<path> (analysis): per-round device time written after the call
+  static const char* round_times = std::getenv("PLG_ROUND_TIMES");
+  std::vector<cudaEvent_t> rev;
+  if (round_times && c->timing) {
+    rev.resize(static_cast<size_t>(rounds) + 1);
+    for (auto& e : rev) cudaEventCreate(&e);
+  }
   for (int r = 0; r < rounds; ++r) {
+    if (!rev.empty()) cudaEventRecord(rev[r], c->stream);
     const int u = d - r;
     int* act_cur = (r & 1) ? c->act1.p : c->act0.p;
     int* act_nxt = (r & 1) ? c->act0.p : c->act1.p;
@@ -748,6 +756,7 @@ int causal_order_impl(plg_ctx* c, const double* dX, int64_t ldx, int64_t n, int 
       c->launches += 2;
     }
   }
+  if (!rev.empty()) cudaEventRecord(rev[rounds], c->stream);
   if (c->timing) cudaEventRecord(c->ev[1], c->stream);
   unsigned long long key = 0, pruned_pairs = 0, per_stage[1 + plg::kMaxPruneStages] = {};
   PLG_CUDA(cudaMemcpyAsync(&key, c->err.p, sizeof(key), cudaMemcpyDeviceToHost, c->stream));
@@ -759,6 +768,17 @@ int causal_order_impl(plg_ctx* c, const double* dX, int64_t ldx, int64_t n, int 
   PLG_CUDA(cudaStreamSynchronize(c->stream));
   PLG_CUDA(cudaGetLastError());
   finish_stats(c, n, d, rounds, host_in);
+  if (!rev.empty()) {
+    if (FILE* f = std::fopen(round_times, "w")) {
+      for (int r = 0; r < rounds; ++r) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, rev[r], rev[r + 1]);
+        std::fprintf(f, "%d %d %.4f\n", r, d - r, ms);
+      }
+      std::fclose(f);
+    }
+    for (auto& e : rev) cudaEventDestroy(e);
+  }
   pruned_pairs = per_stage[0];
   c->last.pairs_evaluated = c->pairs_done + static_cast<int64_t>(pruned_pairs);
   if (prune && std::getenv("PLG_PRUNE_DEBUG")) {
