@@ -190,7 +190,7 @@ struct plg_ctx {
   double prune_beta = 1.1;      // PLG_PRUNE_BETA > 0: hybrid refinement (deficit cut when smaller than the step)
   int64_t prune_sub = 0;        // PLG_PRUNE_SUB: samples of round 0's prediction pass (0: exhaustive round 0)
   DevBuf<double> Md, KN, pk, L, ppart, pres;
-  DevBuf<int> st0, st1, rowsel, off, pwork, pdone, crow, cand;
+  DevBuf<int> st0, st1, rowsel, off, pwork, pdone, crow, cand, alive;
   DevBuf<unsigned long long> kstar, evals;
 
   size_t ev_pairs = 0;  // timing intervals recorded by this call (ev[3 + 2 i], ev[4 + 2 i])
@@ -440,6 +440,7 @@ int search_round_pruned(plg_ctx* c, int64_t n, int64_t ldw, int d, int u, const 
   a.off = c->off.p;
   a.crow = c->crow.p;
   a.cand = c->cand.p;
+  a.alive = c->alive.p;
   a.part = c->ppart.p;
   a.work = c->pwork.p;
   a.done = c->pdone.p;
@@ -593,6 +594,8 @@ int reserve_prune(plg_ctx* c, int64_t n, int d, plg_status* st) {
   PLG_CUDA(c->pdone.reserve(kPruneBatch / 32));
   PLG_CUDA(c->crow.reserve(max_list / 32 + 2));
   PLG_CUDA(c->cand.reserve(static_cast<size_t>(d) * 8));
+  PLG_CUDA(c->alive.reserve(static_cast<size_t>(d) + 1));
+  PLG_CUDA(cudaMemsetAsync(c->alive.p, 0, sizeof(int), c->stream));
   if (c->world > 1 || c->emulate_world > 1) PLG_CUDA(c->pres.reserve(max_list + 64));
   PLG_CUDA(cudaMemsetAsync(c->pdone.p, 0, (kPruneBatch / 32) * sizeof(int), c->stream));
   PLG_CUDA(cudaMemsetAsync(c->evals.p, 0, (1 + plg::kMaxPruneStages) * sizeof(unsigned long long), c->stream));

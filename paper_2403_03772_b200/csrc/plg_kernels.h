@@ -157,6 +157,7 @@ struct PruneArgs {
   int* rowsel;                  // [u * u] selected partner positions of each row, ascending
   int* off;                     // [u + 1] per-row counts -> exclusive offsets, off[u] = total
   int* crow;                    // [list / 32 + 1] row of each 32-entry chunk's first entry
+  int* alive;                   // [1 + u] count, then the stage's surviving rows (any order)
   double* part;                 // [nseg][batch][4] segment partial sums
   int* work;                    // per-batch item counters (zeroed by the scan kernel)
   int* done;                    // [batch / 32] per-chunk finished-segment counters (self-resetting)

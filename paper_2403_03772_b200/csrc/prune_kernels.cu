@@ -75,10 +75,14 @@ __device__ __forceinline__ void insert_key(unsigned long long (&bk)[K], int (&bq
 
 // ---- predict: pk[p] = sum_q KN(p, q); the row's kPredK strongest predicted partners (the
 // probe stage's suspects come from them); collinearity of every pair; state = alive ----
-__global__ void __launch_bounds__(256) prune_predict_kernel(const PruneArgs a) {
-  const int p = blockIdx.x * 8 + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (p >= a.u) return;
+constexpr int kPredThreads = 128;  // 4 warps per row: enough loads in flight at ~2000 rows
+__global__ void __launch_bounds__(kPredThreads) prune_predict_kernel(const PruneArgs a) {
+  __shared__ double s_acc[kPredThreads / 32];
+  __shared__ unsigned long long s_bk[kPredThreads / 32][kPredK];
+  __shared__ int s_bq[kPredThreads / 32][kPredK];
+  __shared__ int s_col[kPredThreads / 32];
+  const int p = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int vp = a.act[p];
   const double* kn = a.KN + static_cast<int64_t>(vp) * a.d;
   const double* crow = a.C + static_cast<int64_t>(vp) * a.ldc;
@@ -89,12 +93,12 @@ __global__ void __launch_bounds__(256) prune_predict_kernel(const PruneArgs a) {
   int bq[kPredK];
 #pragma unroll
   for (int i = 0; i < kPredK; ++i) bk[i] = 0ull, bq[i] = -1;
-  for (int q0 = lane; q0 < a.u; q0 += 128) {
+  for (int q0 = threadIdx.x; q0 < a.u; q0 += 4 * kPredThreads) {
     int vq[4];
     double kv[4], cjj[4], cij[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {  // independent loads first
-      const int q = q0 + 32 * j;
+      const int q = q0 + kPredThreads * j;
       vq[j] = q < a.u ? a.act[q] : vp;
     }
 #pragma unroll
@@ -105,7 +109,7 @@ __global__ void __launch_bounds__(256) prune_predict_kernel(const PruneArgs a) {
     }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const int q = q0 + 32 * j;
+      const int q = q0 + kPredThreads * j;
       if (q >= a.u) continue;
       acc += (q == p) ? 0.0 : kv[j];
       if (q != p) insert_key<kPredK>(bk, bq, static_cast<unsigned long long>(__double_as_longlong(kv[j])), q);
@@ -120,10 +124,10 @@ __global__ void __launch_bounds__(256) prune_predict_kernel(const PruneArgs a) {
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (__any_sync(0xffffffffu, collinear) && lane == 0) atomicMin(a.err, err_key(a.round, kErrPairCollinear, -1));
-  int* cand = a.cand + static_cast<int64_t>(p) * kPredK;
+  const bool wcol = __any_sync(0xffffffffu, collinear);
+  // the warp's best kPredK (merge of the lanes' sorted lists)
 #pragma unroll
-  for (int r = 0; r < kPredK; ++r) {  // warp merge of the lanes' sorted lists
+  for (int r = 0; r < kPredK; ++r) {
     unsigned long long k = bk[0];
     int q = bq[0];
 #pragma unroll
@@ -132,15 +136,40 @@ __global__ void __launch_bounds__(256) prune_predict_kernel(const PruneArgs a) {
       const int oq = __shfl_xor_sync(0xffffffffu, q, o);
       if (key_better(ok, oq, k, q)) k = ok, q = oq;
     }
-    if (lane == 0) cand[r] = q;
+    if (lane == 0) s_bk[warp][r] = k, s_bq[warp][r] = q;
     if (q >= 0 && bq[0] == q) {
 #pragma unroll
       for (int i = 0; i + 1 < kPredK; ++i) bk[i] = bk[i + 1], bq[i] = bq[i + 1];
       bk[kPredK - 1] = 0ull, bq[kPredK - 1] = -1;
     }
   }
+  if (lane == 0) s_acc[warp] = acc, s_col[warp] = wcol;
+  __syncthreads();
+  if (warp != 0) return;
+  // row totals in a fixed order; the row's best kPredK from the warps' lists
+  unsigned long long k = 0ull;
+  int q = -1;
+  if (lane < (kPredThreads / 32) * kPredK) k = s_bk[lane / kPredK][lane % kPredK], q = s_bq[lane / kPredK][lane % kPredK];
+  int* cand = a.cand + static_cast<int64_t>(p) * kPredK;
+#pragma unroll
+  for (int r = 0; r < kPredK; ++r) {
+    unsigned long long bkk = k;
+    int bqq = q;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long ok = __shfl_xor_sync(0xffffffffu, bkk, o);
+      const int oq = __shfl_xor_sync(0xffffffffu, bqq, o);
+      if (key_better(ok, oq, bkk, bqq)) bkk = ok, bqq = oq;
+    }
+    if (lane == 0) cand[r] = bqq;
+    if (bqq >= 0 && q == bqq) k = 0ull, q = -1;
+  }
   if (lane == 0) {
-    a.pk[p] = acc;
+    double tot = 0.0;
+    bool col = false;
+    for (int w = 0; w < kPredThreads / 32; ++w) tot += s_acc[w], col |= (s_col[w] != 0);
+    if (col) atomicMin(a.err, err_key(a.round, kErrPairCollinear, -1));
+    a.pk[p] = tot;
     a.state_out[p] = 1;
     a.L[p] = 0.0;
   }
@@ -247,28 +276,67 @@ __device__ __forceinline__ int block_prefix(bool pred, int* s_warp, int& excl) {
 // remaining partner (the row is a contender and needs its exact k anyway). Selection works
 // on exponent bins of the predicted value (2^k granularity) with fixed-point weights, so it
 // is deterministic; inside the boundary bin partners are taken in ascending position.
+// Refinement / full stages, step 1 (CTA of 128 threads per row): the row's partial k over
+// its evaluated partners (a lower bound of k whatever the summation order; fixed block
+// shape, so deterministic), the prune decision, and the compact list of surviving rows
+// (its order is irrelevant: each row's selection depends on that row only).
+constexpr int kRowThreads = 128;
+__global__ void __launch_bounds__(kRowThreads) prune_rowl_kernel(const PruneArgs a) {
+  __shared__ double s_red[kRowThreads / 32];
+  const int p = blockIdx.x;
+  const int u = a.u;
+  const int st = a.state_in[p];
+  if (st != 1) {
+    if (threadIdx.x == 0) a.state_out[p] = st, a.off[p] = 0;
+    return;
+  }
+  const double* md = a.Md + static_cast<int64_t>(p) * u;
+  double acc = 0.0;
+#pragma unroll 4
+  for (int q = threadIdx.x; q < u; q += kRowThreads) {
+    const double mi = md[q];
+    if (q != p && is_eval(mi)) {
+      const double c = (mi < 0.0) ? mi : 0.0;
+      acc = __dadd_rn(acc, __dmul_rn(c, c));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  double Lp = 0.0;
+  for (int w = 0; w < kRowThreads / 32; ++w) Lp += s_red[w];
+  const bool alive = Lp <= kstar_threshold(a);
+  a.L[p] = Lp;
+  a.state_out[p] = alive ? 1 : 0;
+  a.off[p] = 0;  // the selection overwrites it for surviving rows
+  if (alive) a.alive[1 + atomicAdd(a.alive, 1)] = p;
+}
+
+// Step 2 (CTA per surviving row, from the compact list; probe fallback: CTA per row).
 __global__ void __launch_bounds__(kSelThreads) prune_select_kernel(const PruneArgs a, int stage, int m,
                                                                    double beta, int cache_keys) {
   __shared__ int hist[kBins];
   __shared__ unsigned long long wt[kBins];
   __shared__ int s_warp[kSelThreads / 32];
   __shared__ int s_cut[2];  // boundary bin, entries of it to take
-  __shared__ double s_red[kSelThreads / 32];
   extern __shared__ double s_key[];  // cache_keys: per partner, its prediction or -1 (not eligible)
-  const int p = blockIdx.x;
   const int u = a.u;
+  const bool refine = (stage != kStageProbe);
+  if (refine && static_cast<int>(blockIdx.x) >= *a.alive) return;
+  const int p = refine ? a.alive[1 + blockIdx.x] : static_cast<int>(blockIdx.x);
   const int st = a.state_in[p];
-  const double thr = (stage == kStageProbe) ? 0.0 : kstar_threshold(a);
+  const double thr = refine ? kstar_threshold(a) : 0.0;
+  const double Lp = refine ? a.L[p] : 0.0;
   const double* md = a.Md + static_cast<int64_t>(p) * u;
   const double* kn = a.KN + static_cast<int64_t>(a.act[p]) * a.d;
-  const bool refine = (stage != kStageProbe);
-  // One pass over the row (refinement / full stages): the partial k over the evaluated
-  // partners (a lower bound of k whatever the summation order; fixed block shape, so
-  // deterministic) and, when cached, every unevaluated partner's prediction. Loads are
-  // issued 8 per thread at a time (the gather kn[act[q]] depends on act[q]).
-  double Lp = 0.0;
-  if (refine && st == 1) {
-    double acc = 0.0;
+  const bool full = refine ? (stage == kStageFull) : (st == 2);
+  if (!refine && threadIdx.x == 0) a.state_out[p] = st;
+  // The row's predictions for its unevaluated partners, cached in shared memory (loads 8 per
+  // thread at a time: the gather kn[act[q]] depends on act[q]).
+  const bool cached = cache_keys && refine;
+  if (cached) {
     constexpr int kB = 8;
     for (int q0 = threadIdx.x; q0 < u; q0 += kB * kSelThreads) {
       double mi[kB];
@@ -277,40 +345,16 @@ __global__ void __launch_bounds__(kSelThreads) prune_select_kernel(const PruneAr
       for (int j = 0; j < kB; ++j) {
         const int q = q0 + j * kSelThreads;
         mi[j] = q < u ? md[q] : 0.0;
-        vq[j] = (cache_keys && q < u) ? a.act[q] : 0;
+        vq[j] = q < u ? a.act[q] : 0;
       }
 #pragma unroll
       for (int j = 0; j < kB; ++j) {
         const int q = q0 + j * kSelThreads;
-        if (q >= u) continue;
-        if (q != p && is_eval(mi[j])) {
-          const double c = (mi[j] < 0.0) ? mi[j] : 0.0;
-          acc = __dadd_rn(acc, __dmul_rn(c, c));
-        }
-        if (cache_keys) s_key[q] = (q == p || is_eval(mi[j])) ? -1.0 : kn[vq[j]];
+        if (q < u) s_key[q] = (q == p || is_eval(mi[j])) ? -1.0 : kn[vq[j]];
       }
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = acc;
     __syncthreads();
-    for (int w = 0; w < kSelThreads / 32; ++w) Lp += s_red[w];
   }
-  bool active = false, full = false;
-  if (!refine) {
-    active = true;
-    full = (st == 2);
-  } else {
-    active = (st == 1 && Lp <= thr);
-    full = (stage == kStageFull);
-  }
-  if (threadIdx.x == 0) {
-    a.state_out[p] = (st == 1 && refine && !active) ? 0 : st;
-    if (refine) a.L[p] = Lp;
-    if (!active) a.off[p] = 0;
-  }
-  if (!active) return;
-  const bool cached = cache_keys && refine;
   // A pair of two full rows is listed twice in the full stage (both rows are still alive,
   // rare); its two evaluations have identical bits and the same writes.
   auto eligible = [&](int q) -> bool {
@@ -609,6 +653,7 @@ __global__ void __launch_bounds__(1024) prune_scan_kernel(const PruneArgs a) {
     atomicAdd(a.evals + 1 + a.stage_idx, static_cast<unsigned long long>(s_carry));
   }
   for (int b = threadIdx.x; b <= s_carry / a.batch; b += blockDim.x) a.work[b] = 0;  // fetch counters
+  if (threadIdx.x == 0) *a.alive = 0;  // the next stage's surviving-row list starts empty
   __syncthreads();  // every offset visible to the block
   const int total = s_carry;
   for (int p = threadIdx.x; p < a.u; p += blockDim.x) {  // chunk -> row of its first entry
@@ -886,7 +931,7 @@ void launch_pairs_cfg(const PruneArgs& a, cudaStream_t s) {
 }  // namespace
 
 void launch_prune_predict(const PruneArgs& a, cudaStream_t s) {
-  prune_predict_kernel<<<(a.u + 7) / 8, 256, 0, s>>>(a);
+  prune_predict_kernel<<<a.u, kPredThreads, 0, s>>>(a);
 }
 
 void launch_prune_top(const PruneArgs& a, int R, cudaStream_t s) {
@@ -896,6 +941,7 @@ void launch_prune_top(const PruneArgs& a, int R, cudaStream_t s) {
 void launch_prune_select(const PruneArgs& a, int stage, int m, double beta, cudaStream_t s) {
   if (stage == kStageProbe) prune_probe_select_kernel<<<(a.u + 7) / 8, 256, 0, s>>>(a, m < kMaxT ? m : kMaxT);
   else {
+    prune_rowl_kernel<<<a.u, kRowThreads, 0, s>>>(a);
     // the row's predictions cached in shared memory (u <= 24 576; larger rows re-read them)
     static bool attr = false;
     if (!attr) {
