@@ -592,6 +592,272 @@ int orc_causal_order(const double* X, int64_t n, int32_t d, int64_t ld, int32_t 
   return rc ? rc : ok(st);
 }
 
+/* ------------------------------------------------------------ exact pruned order */
+/* The product's pruned rounds (prune_kernels.cu) restated on the CPU, used to produce full
+ * golden orders for the largest configs (C3, C5) in minutes instead of days. Each round
+ * evaluates pair_mi only for the pairs a branch and bound on k needs: R = 3 rows with the
+ * lowest predicted k get full rows (k* = min of their exact k), every other row its T = 2
+ * strongest predicted partners, then rows whose partial k is still <= k* (1 + 1e-9) their
+ * strongest partners up to 5% and 25% of the row, then the survivors full rows. A row's
+ * partial k is a sum of a subset of its non-negative terms, so pruned rows cannot win; the
+ * winner's k is summed exactly as candidate_score (q ascending) from the same pair_mi
+ * values, so order and winning k equal the fast/faithful modes' (tested bit for bit).
+ * Predictions: the last evaluated min(0, mi)^2 of each variable pair (round 0 evaluates
+ * every pair). Error paths are not reproduced (golden generation on valid data only). */
+typedef struct {
+  const round_cache* cache;
+  double* mi_full;
+  const int32_t* pp;
+  const int32_t* qq;
+  int64_t lo, hi;
+  int rc;
+  orc_status st;
+} list_job;
+
+static void* run_list(void* arg) {
+  list_job* job = (list_job*)arg;
+  const round_cache* c = job->cache;
+  double* ri_j = (double*)malloc(sizeof(double) * (size_t)c->n);
+  double* rj_i = (double*)malloc(sizeof(double) * (size_t)c->n);
+  job->rc = 0;
+  for (int64_t k = job->lo; k < job->hi && !job->rc; ++k) {
+    const int32_t p = job->pp[k], q = job->qq[k];
+    double mi;
+    int rc = pair_mi(c, p, q, ri_j, rj_i, &mi, &job->st);
+    if (rc) {
+      job->rc = rc;
+      break;
+    }
+    job->mi_full[(int64_t)p * c->u + q] = mi;
+    job->mi_full[(int64_t)q * c->u + p] = -mi;
+  }
+  free(ri_j);
+  free(rj_i);
+  return NULL;
+}
+
+typedef struct {
+  int32_t* pp;
+  int32_t* qq;
+  int64_t n, cap;
+  uint8_t* queued; /* u x u */
+} pair_list;
+
+static void list_add(pair_list* L, int32_t u, int32_t p, int32_t q, const double* mi_full) {
+  const int32_t a = p < q ? p : q, b = p < q ? q : p;
+  if (a == b || L->queued[(int64_t)a * u + b] || mi_full[(int64_t)a * u + b] == mi_full[(int64_t)a * u + b])
+    return;
+  L->queued[(int64_t)a * u + b] = 1;
+  if (L->n == L->cap) {
+    L->cap = L->cap ? 2 * L->cap : 1024;
+    L->pp = (int32_t*)realloc(L->pp, sizeof(int32_t) * (size_t)L->cap);
+    L->qq = (int32_t*)realloc(L->qq, sizeof(int32_t) * (size_t)L->cap);
+  }
+  L->pp[L->n] = a;
+  L->qq[L->n] = b;
+  ++L->n;
+}
+
+static int eval_list(const round_cache* c, double* mi_full, pair_list* L, int32_t nthreads, int64_t* evaluated,
+                     orc_status* st) {
+  if (L->n == 0) return 0;
+  list_job* jobs = (list_job*)calloc((size_t)nthreads, sizeof(list_job));
+  for (int32_t t = 0; t < nthreads; ++t) {
+    jobs[t].cache = c;
+    jobs[t].mi_full = mi_full;
+    jobs[t].pp = L->pp;
+    jobs[t].qq = L->qq;
+    jobs[t].lo = L->n * t / nthreads;
+    jobs[t].hi = L->n * (t + 1) / nthreads;
+  }
+  run_threads(jobs, sizeof(list_job), nthreads, run_list);
+  int rc = 0;
+  for (int32_t t = 0; t < nthreads && !rc; ++t)
+    if (jobs[t].rc) {
+      rc = jobs[t].rc;
+      if (st) *st = jobs[t].st;
+    }
+  free(jobs);
+  for (int64_t k = 0; k < L->n; ++k) L->queued[(int64_t)L->pp[k] * c->u + L->qq[k]] = 0;
+  *evaluated += L->n;
+  L->n = 0;
+  return rc;
+}
+
+/* k of position p over its evaluated partners, q ascending (candidate_score's order) */
+static double partial_k(const double* mi_full, int32_t u, int32_t p) {
+  double k = 0.0;
+  for (int32_t q = 0; q < u; ++q) {
+    if (q == p) continue;
+    const double mi = mi_full[(int64_t)p * u + q];
+    if (mi != mi) continue;
+    const double cl = clip0(mi);
+    k += cl * cl;
+  }
+  return k;
+}
+
+static const double* g_key_row; /* qsort context: predictions of the row being selected */
+static int cmp_key_desc(const void* a, const void* b) {
+  const int32_t qa = *(const int32_t*)a, qb = *(const int32_t*)b;
+  const double ka = g_key_row[qa], kb = g_key_row[qb];
+  if (ka != kb) return ka > kb ? -1 : 1;
+  return (qa > qb) - (qa < qb);
+}
+
+int orc_causal_order_pruned(const double* X, int64_t n, int32_t d, int64_t ld, int32_t workers,
+                            int32_t* order_out, double* winner_k, int64_t* pairs_evaluated, orc_status* st) {
+  int rc = orc_validate(X, n, d, ld, st);
+  if (rc) return rc;
+  if (workers < 1) workers = 1;
+  const int32_t R = 3, T = 2;
+  const double fracs[2] = {0.05, 0.25};
+  double* working = (double*)malloc(sizeof(double) * (size_t)n * (size_t)d);
+  for (int32_t j = 0; j < d; ++j)
+    memcpy(working + (int64_t)j * n, X + (int64_t)j * ld, sizeof(double) * (size_t)n);
+  int32_t* u = (int32_t*)malloc(sizeof(int32_t) * (size_t)d);
+  int32_t* rem = (int32_t*)malloc(sizeof(int32_t) * (size_t)d);
+  double* res = (double*)malloc(sizeof(double) * (size_t)n * (size_t)(d > 1 ? d - 1 : 1));
+  double* KN = (double*)calloc((size_t)d * (size_t)d, sizeof(double));
+  double* mi_full = (double*)malloc(sizeof(double) * (size_t)d * (size_t)d);
+  double* kex = (double*)malloc(sizeof(double) * (size_t)d);
+  double* key = (double*)malloc(sizeof(double) * (size_t)d);
+  int32_t* state = (int32_t*)malloc(sizeof(int32_t) * (size_t)d);
+  int32_t* cand = (int32_t*)malloc(sizeof(int32_t) * (size_t)d);
+  pair_list L = {NULL, NULL, 0, 0, (uint8_t*)calloc((size_t)d * (size_t)d, 1)};
+  int64_t evaluated = 0;
+  for (int32_t p = 0; p < d; ++p) u[p] = p;
+  int32_t nu = d, pos = 0, round = 0;
+  rc = 0;
+  while (nu > 1) {
+    round_cache cache;
+    memset(&cache, 0, sizeof(cache));
+    rc = build_cache(working, n, n, u, nu, &cache, st);
+    if (rc) {
+      free_cache(&cache);
+      break;
+    }
+    const int32_t nthreads = workers;
+    for (int64_t i = 0; i < (int64_t)nu * nu; ++i) mi_full[i] = NAN;
+    const int exhaustive = (round == 0 || nu <= 8);
+    int32_t best = -1;
+    if (exhaustive) {
+      for (int32_t p = 0; p < nu; ++p)
+        for (int32_t q = p + 1; q < nu; ++q) list_add(&L, nu, p, q, mi_full);
+      rc = eval_list(&cache, mi_full, &L, nthreads, &evaluated, st);
+      for (int32_t p = 0; p < nu; ++p) {
+        kex[p] = partial_k(mi_full, nu, p);
+        state[p] = 1;
+      }
+    } else {
+      double* pk = key; /* predicted k per position */
+      for (int32_t p = 0; p < nu; ++p) {
+        double a = 0.0;
+        for (int32_t q = 0; q < nu; ++q)
+          if (q != p) a += KN[(int64_t)u[p] * d + u[q]];
+        pk[p] = a;
+        state[p] = 1;
+      }
+      for (int32_t r = 0; r < R && r < nu; ++r) { /* top: lowest predicted k, lowest position */
+        int32_t b = -1;
+        for (int32_t p = 0; p < nu; ++p)
+          if (state[p] == 1 && (b < 0 || pk[p] < pk[b])) b = p;
+        state[b] = 2;
+      }
+      for (int32_t p = 0; p < nu; ++p) {
+        if (state[p] == 2) {
+          for (int32_t q = 0; q < nu; ++q) list_add(&L, nu, p, q, mi_full);
+        } else {
+          int32_t nc = 0;
+          for (int32_t q = 0; q < nu; ++q)
+            if (q != p && state[q] != 2) cand[nc++] = q;
+          for (int32_t q = 0; q < nu; ++q) key[q] = KN[(int64_t)u[p] * d + u[q]];
+          g_key_row = key;
+          qsort(cand, (size_t)nc, sizeof(int32_t), cmp_key_desc);
+          for (int32_t i = 0; i < T && i < nc; ++i) list_add(&L, nu, p, cand[i], mi_full);
+        }
+      }
+      if (!rc) rc = eval_list(&cache, mi_full, &L, nthreads, &evaluated, st);
+      double kstar = INFINITY;
+      for (int32_t p = 0; p < nu; ++p)
+        if (state[p] == 2) {
+          kex[p] = partial_k(mi_full, nu, p);
+          if (kex[p] < kstar) kstar = kex[p];
+        }
+      const double thr = kstar * (1.0 + 1e-9);
+      double prev = 0.0;
+      for (int32_t stage = 0; stage <= 2 && !rc; ++stage) {
+        for (int32_t p = 0; p < nu; ++p) {
+          if (state[p] != 1) continue;
+          if (partial_k(mi_full, nu, p) > thr) {
+            state[p] = 0;
+            continue;
+          }
+          if (stage == 2) { /* full row */
+            for (int32_t q = 0; q < nu; ++q) list_add(&L, nu, p, q, mi_full);
+            continue;
+          }
+          const int32_t m = (int32_t)((fracs[stage] - prev) * nu) > 0 ? (int32_t)((fracs[stage] - prev) * nu) : 1;
+          int32_t nc = 0;
+          for (int32_t q = 0; q < nu; ++q) {
+            const double mi = mi_full[(int64_t)p * nu + q];
+            if (q != p && mi != mi) cand[nc++] = q;
+          }
+          for (int32_t q = 0; q < nu; ++q) key[q] = KN[(int64_t)u[p] * d + u[q]];
+          g_key_row = key;
+          qsort(cand, (size_t)nc, sizeof(int32_t), cmp_key_desc);
+          for (int32_t i = 0; i < m && i < nc; ++i) list_add(&L, nu, p, cand[i], mi_full);
+        }
+        if (stage < 2) prev = fracs[stage];
+        rc = eval_list(&cache, mi_full, &L, nthreads, &evaluated, st);
+      }
+      for (int32_t p = 0; p < nu; ++p)
+        if (state[p] == 1) kex[p] = partial_k(mi_full, nu, p);
+    }
+    free_cache(&cache);
+    if (rc) break;
+    for (int32_t p = 0; p < nu; ++p) /* ordering.cpp:154-160: lowest position on ties */
+      if (state[p] >= 1 && (best < 0 || kex[p] < kex[best])) best = p;
+    for (int32_t p = 0; p < nu; ++p) /* knowledge: evaluated pairs */
+      for (int32_t q = 0; q < nu; ++q) {
+        const double mi = mi_full[(int64_t)p * nu + q];
+        if (q != p && mi == mi) {
+          const double cl = clip0(mi);
+          KN[(int64_t)u[p] * d + u[q]] = cl * cl;
+        }
+      }
+    if (winner_k) winner_k[round] = kex[best];
+    const int32_t chosen = u[best];
+    int32_t nr = 0;
+    for (int32_t p = 0; p < nu; ++p)
+      if (u[p] != chosen) rem[nr++] = u[p];
+    rc = orc_regress_out(working, n, d, n, chosen, rem, nr, res, st);
+    if (rc) break;
+    for (int32_t p = 0; p < nr; ++p)
+      memcpy(working + (int64_t)rem[p] * n, res + (int64_t)p * n, sizeof(double) * (size_t)n);
+    order_out[pos++] = chosen;
+    memcpy(u, rem, sizeof(int32_t) * (size_t)nr);
+    nu = nr;
+    ++round;
+  }
+  if (!rc && nu == 1) order_out[pos++] = u[0];
+  if (pairs_evaluated) *pairs_evaluated = evaluated;
+  free(working);
+  free(u);
+  free(rem);
+  free(res);
+  free(KN);
+  free(mi_full);
+  free(kex);
+  free(key);
+  free(state);
+  free(cand);
+  free(L.pp);
+  free(L.qq);
+  free(L.queued);
+  return rc ? rc : ok(st);
+}
+
 /* ------------------------------------------------------------------ weights */
 
 /* Column-pivoted Householder QR of A (m x p, column-major, lda = m), in place, in the

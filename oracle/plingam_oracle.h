@@ -91,6 +91,13 @@ int orc_causal_order(const double* X, int64_t n, int32_t d, int64_t ld, int32_t 
                      int32_t workers, int32_t fast, int32_t max_rounds, int32_t* order_out,
                      double* round_scores, orc_status* st);
 
+/* Full order by exact pruned rounds (the product's branch and bound on k, restated): same
+ * order and winning k as orc_causal_order (tested), a few % of the pair evaluations.
+ * winner_k (optional): d - 1 doubles, the k of each round's chosen variable. Golden
+ * generation on valid data; error paths are not reproduced. */
+int orc_causal_order_pruned(const double* X, int64_t n, int32_t d, int64_t ld, int32_t workers,
+                            int32_t* order_out, double* winner_k, int64_t* pairs_evaluated, orc_status* st);
+
 /* ---- adjacency weights (proj/src/direct_lingam.cpp:46-70) ----
  * Per-target least squares on centred data via column-pivoted Householder QR
  * (Eigen::ColPivHouseholderQR); B is d x d column-major, B[target + d*pred].

@@ -209,6 +209,20 @@ def causal_order(X, parallel: bool = False, workers: int = 1, fast: bool = False
     return (out, scores[:rounds]) if return_scores else out
 
 
+def causal_order_pruned(X, workers: int = 1):
+    """Exact pruned rounds (orc_causal_order_pruned): (order, winning k per round, pairs)."""
+    X = _mat(X)
+    n, d = X.shape
+    order = np.full(max(d, 1), -1, dtype=np.int32)
+    wk = np.zeros(max(d - 1, 1), dtype=np.float64)
+    pairs = ctypes.c_int64(0)
+    st = _Status()
+    _check(lib().orc_causal_order_pruned(_dp(X), ctypes.c_int64(n), ctypes.c_int32(d), ctypes.c_int64(max(n, 1)),
+                                         ctypes.c_int32(workers), _ip(order), _dp(wk), ctypes.byref(pairs),
+                                         ctypes.byref(st)), st)
+    return [int(v) for v in order[:d]], wk[: max(d - 1, 0)], pairs.value
+
+
 def fit_weights(X, order):
     X = _mat(X)
     n, d = X.shape
