@@ -5,7 +5,8 @@ across machines of this image); the expected outputs come from the CPU oracle
 (oracle/plingam_oracle.c, the restated reference). Each fixture stores the SHA-256 of
 the input matrix so a GPU test can prove it fed the oracle's exact input.
 
-    python tests/golden/make_golden.py [--c3]
+    python tests/golden/make_golden.py [c1 c2 c4]
+    python tests/golden/make_golden.py --full c3 c5   # full orders by the oracle's exact pruned rounds
 """
 
 import argparse
@@ -24,7 +25,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
 import oracle_lib  # noqa: E402
 import paper_2403_03772_b200 as plg  # noqa: E402
 
-WORKERS = os.cpu_count() or 1
+WORKERS = int(os.environ.get("GOLDEN_WORKERS", os.cpu_count() or 1))
 
 
 def digest(X: np.ndarray) -> str:
@@ -65,7 +66,14 @@ def c4_residuals():
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("configs", nargs="*", default=["c1", "c2"], help="c1 c2 c4 (c3: hours on 8 cores)")
+    ap.add_argument("--full", action="store_true",
+                    help="whole order + winning k per round via orc_causal_order_pruned (C3: ~15 min, "
+                         "C5: ~1.5 h on 8 cores)")
     args = ap.parse_args()
+    if args.full:
+        for name in args.configs:
+            make_full(name)
+        return
     if "c1" in args.configs:
         make_c1()
     for name in [c for c in args.configs if c != "c1"]:
@@ -111,6 +119,24 @@ def make_config(name):
                        "used_pinv": pinv,
                        "oracle_seconds": el, "oracle_workers": WORKERS}, f)
         print(name, "done", el, flush=True)
+
+
+def make_full(name):
+    """The oracle's exact pruned rounds (bit-identical order and winning k to its faithful
+    mode, tests/test_oracle_kats.py) over the whole order of a large config."""
+    X = config_input(name)
+    t0 = time.time()
+    order, wk, pairs = oracle_lib.causal_order_pruned(X, workers=WORKERS)
+    el = time.time() - t0
+    n, d = X.shape
+    with open(os.path.join(HERE, f"{name}_order_full.json"), "w") as f:
+        json.dump({"config": name, "n": int(n), "d": int(d), "sha256": digest(X), "order": order,
+                   "winner_k": [float(v).hex() for v in wk],
+                   "oracle": "orc_causal_order_pruned (exact branch and bound over the faithful "
+                             "pair statistics; same order and winning k as orc_causal_order)",
+                   "pairs_evaluated": int(pairs), "pairs_exhaustive": int(d * (d - 1) * (d + 1) // 6),
+                   "oracle_seconds": el, "oracle_workers": WORKERS}, f)
+    print(name, "full done", el, pairs, flush=True)
 
 
 if __name__ == "__main__":

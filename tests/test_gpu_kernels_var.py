@@ -134,3 +134,26 @@ def test_c5_sampled_rounds(engine, oracle):
 
     X = bench.make_input("c5")
     _sampled_rounds(engine, oracle, X, (1500, 1990))
+
+
+@pytest.mark.parametrize("name", ["c3", "c5"])
+def test_full_order_golden(engine, name):
+    """BASELINE configs[2] / configs[4], whole causal order against the CPU oracle: the
+    golden is the oracle's exact pruned run (orc_causal_order_pruned, bit-identical order
+    and winning k to its faithful mode, tests/test_oracle_kats.py). The GPU order must be
+    identical, every round's winning k within the score bar (1e-9 relative)."""
+    import bench
+
+    path = os.path.join(GOLDEN, f"{name}_order_full.json")
+    if not os.path.exists(path):
+        pytest.skip(f"{name} full golden not generated")
+    with open(path) as f:
+        fx = json.load(f)
+    X = np.asfortranarray(bench.make_input(name))
+    assert hashlib.sha256(X.tobytes(order="F")).hexdigest() == fx["sha256"]
+    order = engine.causal_order(X)
+    assert order == fx["order"]
+    k_gpu = np.asarray(engine.round_k())
+    k_ref = np.array([float.fromhex(v) for v in fx["winner_k"]])
+    assert k_gpu.shape == k_ref.shape
+    assert np.all(np.abs(k_gpu - k_ref) <= 1e-9 * np.abs(k_ref) + 1e-15), np.max(np.abs(k_gpu - k_ref) / np.abs(k_ref))

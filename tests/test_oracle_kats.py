@@ -412,3 +412,16 @@ def test_weights_pinv_fallback(oracle):  # test_direct_lingam.cpp:96-113
     Xc = X - X.mean(axis=0)
     ref = np.linalg.pinv(Xc[:, :3]) @ Xc[:, 3]
     assert np.allclose(B[3, :3], ref, atol=1e-8)
+
+
+@pytest.mark.parametrize("d,n,seed,kind", [(40, 1500, 11, "laplace"), (90, 1200, 12, "t3"), (70, 900, 13, "uniform")])
+def test_pruned_oracle_matches_faithful(plg, oracle, d, n, seed, kind):
+    """orc_causal_order_pruned (used for the full C3/C5 goldens) returns the faithful
+    oracle's order and the bit-identical winning k of every round."""
+    dag = plg.gen_sparse_dag(d, avg_parents=2.0, seed=seed)
+    X = plg.sample_lingam(dag, n, seed=seed, kind=kind)
+    order, scores = oracle.causal_order(X, parallel=True, workers=4, fast=True, return_scores=True)
+    order_p, wk, pairs = oracle.causal_order_pruned(X, workers=4)
+    assert order_p == order
+    assert np.array_equal(wk, np.array([-scores[r][order[r]] for r in range(d - 1)]))
+    assert 0 < pairs < d * (d - 1) * (d + 1) // 6
