@@ -163,6 +163,10 @@ struct plg_ctx {
   int rank = 0;
   int world = 1;
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;       // pruned rounds: predictions overlap the residualisation
+  cudaEvent_t ev_gram = nullptr;     // main stream: the round's Gram update is done
+  cudaEvent_t ev_side = nullptr;     // side stream: predictions + probe selection are done
+  bool gram_ready = false;           // ev_gram recorded by the previous round of this call
   ncclComm_t comm = nullptr;
   bool timing = true;
 
@@ -284,6 +288,9 @@ int ctx_init(plg_ctx* ctx, int device, plg_status* st) {
   parse_prune_env(ctx);
   PLG_CUDA(cudaSetDevice(device));
   PLG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+  PLG_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+  PLG_CUDA(cudaEventCreateWithFlags(&ctx->ev_gram, cudaEventDisableTiming));
+  PLG_CUDA(cudaEventCreateWithFlags(&ctx->ev_side, cudaEventDisableTiming));
   if (int rc = make_tables(ctx, st)) return rc;
   PLG_CUDA(ctx->err.reserve(1));
   PLG_CUDA(ctx->errs.reserve(64));
@@ -418,9 +425,16 @@ int search_round(plg_ctx* c, int64_t n, int64_t ldw, int ldc, int u, const int* 
 // earlier round of the same run.
 int search_round_pruned(plg_ctx* c, int64_t n, int64_t ldw, int d, int u, const int* act_cur, int round,
                         plg_status* st, bool h_from_resid = true) {
+  // The predictions, the top rows and the probe selection need the Gram update, the active
+  // list and KN but not W: after the previous round's Gram update they run on the side
+  // stream while the main stream residualises W and forms H (resid_ent + hfin).
+  const bool overlap = c->gram_ready && h_from_resid;
+  cudaStream_t ps = overlap ? c->side : c->stream;
+  if (overlap) PLG_CUDA(cudaStreamWaitEvent(c->side, c->ev_gram, 0));
+  c->gram_ready = false;
   round_entropies(c, n, ldw, d, u, act_cur, round, h_from_resid);
   const SegPlan sp = c->prune_tile_seg ? seg_plan(u, n) : prune_seg_plan(n);
-  PLG_CUDA(cudaMemsetAsync(c->Md.p, 0xff, static_cast<size_t>(u) * u * sizeof(double), c->stream));
+  PLG_CUDA(cudaMemsetAsync(c->Md.p, 0xff, static_cast<size_t>(u) * u * sizeof(double), ps));
   plg::PruneArgs a{};
   a.W = c->W.p;
   a.ldw = ldw;
@@ -462,8 +476,8 @@ int search_round_pruned(plg_ctx* c, int64_t n, int64_t ldw, int d, int u, const 
   int* sb = c->st1.p;
   a.state_in = sa;
   a.state_out = sa;
-  plg::launch_prune_predict(a, c->stream);
-  plg::launch_prune_top(a, c->prune_R, c->stream);
+  plg::launch_prune_predict(a, ps);
+  plg::launch_prune_top(a, c->prune_R, ps);
   c->launches += 2;
   int stage_idx = 0;
   const int shards = c->world > 1 ? c->world : c->emulate_world;
@@ -474,9 +488,14 @@ int search_round_pruned(plg_ctx* c, int64_t n, int64_t ldw, int d, int u, const 
     a.stage_idx = std::min(stage_idx++, plg::kMaxPruneStages - 1);
     a.state_in = sa;
     a.state_out = sb;
-    plg::launch_prune_select(a, kind, m, beta, c->stream);
-    plg::launch_prune_scan(a, c->stream);
+    cudaStream_t ss = (kind == plg::kStageProbe) ? ps : c->stream;
+    plg::launch_prune_select(a, kind, m, beta, ss);
+    plg::launch_prune_scan(a, ss);
     c->launches += 2;
+    if (ss != c->stream) {  // join: the probe's pairs need W and H from the main stream
+      PLG_CUDA(cudaEventRecord(c->ev_side, ss));
+      PLG_CUDA(cudaStreamWaitEvent(c->stream, c->ev_side, 0));
+    }
     if (shards == 1) {
       const size_t tm = pair_timer_begin(c);
       plg::launch_prune_pairs(a, c->stream);
@@ -750,6 +769,10 @@ int causal_order_impl(plg_ctx* c, const double* dX, int64_t ldx, int64_t n, int 
     if (u - 1 >= 2 || (u - 1 == 1 && max_rounds >= 0)) {
       // the next round's build_cache check only exists when it has >= 2 candidates
       plg::launch_update_gram(c->C.p, d, act_nxt, u - 1, c->rs.p, c->err.p, c->stream);
+      if (prune) {
+        PLG_CUDA(cudaEventRecord(c->ev_gram, c->stream));
+        c->gram_ready = true;
+      }
       const size_t tr = pair_timer_begin(c, 1);
       plg::launch_resid_ent(c->W.p, ldw, n, c->C.p, d, act_nxt, u - 1, c->rs.p, c->nz.p, r + 1, c->err.p,
                             c->hpart.p, c->g_exp, c->g_log, c->stream);
@@ -913,6 +936,9 @@ void plg_ctx_destroy(plg_ctx* c) {
   c->errs.release();
   if (c->g_exp) cudaFree(c->g_exp);
   if (c->g_log) cudaFree(c->g_log);
+  if (c->side) cudaStreamDestroy(c->side);
+  if (c->ev_gram) cudaEventDestroy(c->ev_gram);
+  if (c->ev_side) cudaEventDestroy(c->ev_side);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
