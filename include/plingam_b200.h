@@ -122,6 +122,14 @@ int plg_regress_out(plg_ctx* ctx, const double* X, int64_t n, int32_t d, int64_t
 int plg_fit_weights(plg_ctx* ctx, const double* X, int64_t n, int32_t d, int64_t ld,
                     const int32_t* order, double* B_out, int32_t* used_pinv, plg_status* st);
 
+/* VarLiNGAM front-end (var_lingam.cpp:7-53, estimate_var): least-squares VAR(lag) with
+ * intercept of the T x d series ts. coef_out (optional): (1 + lag d) x d column-major, row 0
+ * the intercepts, row 1 + (tau - 1) d + j the coefficient of x_j(t - tau); resid_out
+ * (optional): (T - lag) x d residuals. Device: scaled normal equations, blocked Cholesky,
+ * one refinement step. Errors: OutOfRange (lag < 1), DimensionMismatch, NonFinite,
+ * InsufficientRows (T < lag + 2d or fewer rows than coefficients), SingularDesign. */
+int plg_estimate_var(plg_ctx* ctx, const double* ts, int64_t T, int32_t d, int64_t ld, int32_t lag,
+                     double* coef_out, double* resid_out, plg_status* st);
 /* The element functions of plingam::kernels (include/plingam/kernels.hpp:25-70), exposed
  * by the reference's Python module (bindings/pymodule.cpp:79-96):
  *   standardize (kernels.cpp:92-104; bit-identical: left-to-right sums),

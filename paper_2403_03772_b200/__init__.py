@@ -9,6 +9,7 @@ There is no CPU fallback: if the compiled extension is missing the import fails,
 without a CUDA device every call raises ``Error`` with ``code == "DeviceError"``.
 """
 
+from ._core import _estimate_var_qr  # noqa: F401  (test reference: the reference's host QR)
 from ._core import (  # noqa: F401  (re-export, as the reference package does)
     Engine,
     Error,

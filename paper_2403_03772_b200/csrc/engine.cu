@@ -1325,6 +1325,65 @@ void pinv_solve_sym(std::vector<double> A, int q, const double* b, double* x) {
 
 }  // namespace
 
+extern "C" int plg_estimate_var(plg_ctx* c, const double* ts, int64_t T, int32_t d, int64_t ld, int32_t lag,
+                                double* coef_out, double* resid_out, plg_status* st) {
+  // var_lingam.cpp:7-53 on the device (var_kernels.cu): errors in the reference's order.
+  if (!c) return set_status(st, PLG_OutOfRange, -1, -1, "null context");
+  if (lag < 1) return set_status(st, PLG_OutOfRange, -1, -1, "estimate_var: lag must be >= 1");
+  if (d < 1) return set_status(st, PLG_DimensionMismatch, -1, -1, "estimate_var: need at least 1 variable");
+  if (ld < T) return set_status(st, PLG_DimensionMismatch, -1, -1, "leading dimension smaller than T");
+  const int64_t n_rows = T - lag;
+  const int64_t n_cols = 1 + static_cast<int64_t>(lag) * d;
+  if (int rc = begin_call(c, st)) return rc;
+  if (int rc = upload_x(c, ts, T, d, ld, st)) return rc;
+  // non-finite scan first (the reference checks the whole series before the row count)
+  if (T < lag + 2 * static_cast<int64_t>(d) || n_rows < n_cols) {
+    std::vector<double> h(static_cast<size_t>(T) * d);
+    PLG_CUDA(cudaMemcpyAsync(h.data(), c->Xd.p, h.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    PLG_CUDA(cudaStreamSynchronize(c->stream));
+    for (double v : h)
+      if (!std::isfinite(v)) return set_status(st, PLG_NonFinite, -1, -1, "estimate_var: non-finite entries in series");
+    return set_status(st, PLG_InsufficientRows, -1, -1, "estimate_var: series too short for lag %d", lag);
+  }
+  const int ncol = static_cast<int>(n_cols + d);
+  const int64_t lda = round_up(n_rows, 16);
+  const size_t nn = static_cast<size_t>(n_cols) * n_cols;
+  PLG_CUDA(c->W.reserve(static_cast<size_t>(ncol) * lda));
+  PLG_CUDA(c->C.reserve(static_cast<size_t>(ncol) * ncol));
+  PLG_CUDA(c->gscr.reserve(static_cast<size_t>(plg::gram_scratch_doubles(ncol, n_rows))));
+  PLG_CUDA(c->part.reserve(2 * nn + 2 * static_cast<size_t>(n_cols) * d + n_cols + static_cast<size_t>(n_rows) * d));
+  PLG_CUDA(c->stat.reserve(2));
+  double* S = c->part.p;
+  double* S0 = S + nn;
+  double* R = S0 + nn;
+  double* B = R + static_cast<size_t>(n_cols) * d;
+  double* D = B + static_cast<size_t>(n_cols) * d;
+  double* E = D + n_cols;
+  const int32_t init[2] = {static_cast<int32_t>(n_cols), 0};
+  PLG_CUDA(cudaMemcpyAsync(c->stat.p, init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
+  plg::launch_build_var_design(c->Xd.p, T, n_rows, d, lag, c->W.p, lda, c->stat.p + 1, c->stream);
+  plg::launch_gram(c->W.p, lda, n_rows, ncol, c->C.p, ncol, c->gscr.p, c->stream);
+  plg::launch_var_scale(c->C.p, ncol, static_cast<int>(n_cols), d, S, S0, R, D, c->stream);
+  plg::launch_cholesky(S, static_cast<int>(n_cols), 1e-14, c->stat.p, c->stream);
+  plg::launch_var_solve(S, S0, R, D, static_cast<int>(n_cols), d, B, c->stat.p, c->stream);
+  plg::launch_var_resid(c->W.p, lda, n_rows, static_cast<int>(n_cols), d, B, E, n_rows, c->stream);
+  c->launches += 6;
+  int32_t flags[2] = {0, 0};
+  PLG_CUDA(cudaMemcpyAsync(flags, c->stat.p, sizeof(flags), cudaMemcpyDeviceToHost, c->stream));
+  PLG_CUDA(cudaStreamSynchronize(c->stream));
+  if (flags[1]) return set_status(st, PLG_NonFinite, -1, -1, "estimate_var: non-finite entries in series");
+  if (flags[0] < n_cols) return set_status(st, PLG_SingularDesign, -1, -1, "estimate_var: rank-deficient design matrix");
+  if (coef_out)
+    PLG_CUDA(cudaMemcpyAsync(coef_out, B, static_cast<size_t>(n_cols) * d * sizeof(double), cudaMemcpyDeviceToHost,
+                             c->stream));
+  if (resid_out)
+    PLG_CUDA(cudaMemcpyAsync(resid_out, E, static_cast<size_t>(n_rows) * d * sizeof(double), cudaMemcpyDeviceToHost,
+                             c->stream));
+  PLG_CUDA(cudaStreamSynchronize(c->stream));
+  PLG_CUDA(cudaGetLastError());
+  return ok(st);
+}
+
 extern "C" int plg_fit_weights(plg_ctx* c, const double* X, int64_t n, int32_t d, int64_t ld,
                                const int32_t* order, double* B_out, int32_t* used_pinv,
                                plg_status* st) {

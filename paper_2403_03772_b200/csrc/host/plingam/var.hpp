@@ -14,11 +14,14 @@ struct VarEstimate {
   DataMatrix residuals;                    // (T - k) x d
 };
 
-// Least-squares VAR(k) with intercept (estimated, then discarded) by one column-pivoted
-// Householder QR of the stacked design [1, x(t-1), ..., x(t-k)] (var_lingam.cpp:7-53).
+// Least-squares VAR(k) with intercept (estimated, then discarded) of the stacked design
+// [1, x(t-1), ..., x(t-k)] (var_lingam.cpp:7-53), on the B200 (plg_estimate_var).
 // `ts` rows are time points. Throws OutOfRange (lag < 1), DimensionMismatch, NonFinite,
 // InsufficientRows and SingularDesign.
 VarEstimate estimate_var(const DataMatrix& ts, int lag);
+// The same estimate by the reference's method (column-pivoted Householder QR on the host):
+// the parity reference of estimate_var's device path, used by the tests.
+VarEstimate estimate_var_qr(const DataMatrix& ts, int lag);
 
 struct VarModel {
   WeightedDag b0;

@@ -306,6 +306,16 @@ PYBIND11_MODULE(_core, m) {
       },
       py::arg("X"), py::arg("lag") = 1);
   m.def(
+      "_estimate_var_qr",  // test reference: the reference's host QR (not the product path)
+      [](const FArray& X, int lag) {
+        DataMatrix ts = to_data(X);
+        VarEstimate est = estimate_var_qr(ts, lag);
+        std::vector<py::array_t<double>> ms;
+        for (const auto& M : est.m_raw) ms.push_back(colmajor_array(M, ts.dims(), ts.dims()));
+        return py::make_tuple(ms, colmajor_array(est.residuals.values, est.residuals.rows, est.residuals.cols));
+      },
+      py::arg("X"), py::arg("lag") = 1);
+  m.def(
       "fit_var_lingam",
       [](const FArray& X, int lag, bool parallel, int workers) {
         DataMatrix ts = to_data(X);

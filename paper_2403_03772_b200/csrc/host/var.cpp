@@ -1,8 +1,12 @@
-// var.cpp — VarLiNGAM front-end on the host.
-// estimate_var restates proj/src/var_lingam.cpp:7-53 (stacked design, one column-pivoted
-// Householder QR for all d equations, rank check, M_tau blocks, residuals Y - Z coeffs);
+// var.cpp — VarLiNGAM front-end.
+// estimate_var: proj/src/var_lingam.cpp:7-53 on the B200 (plg_estimate_var: stacked design,
+// scaled normal equations by the engine's FP64 Cholesky, residuals on the device).
+// estimate_var_qr: the same estimate by one column-pivoted Householder QR on the host, the
+// reference's own method, kept as the parity reference of the device path (tests only).
 // fit_varlingam restates :55-70 with the causal order and weights from the B200 engine.
 #include "plingam/var.hpp"
+
+#include "../../../include/plingam_b200.h"
 
 #include <algorithm>
 #include <cmath>
@@ -85,6 +89,29 @@ int colpiv_qr(std::vector<double>& A, int64_t m, int p, std::vector<double>& tau
 }  // namespace
 
 VarEstimate estimate_var(const DataMatrix& ts, int lag) {
+  const int64_t T = ts.samples();
+  const int64_t d = ts.dims();
+  const int64_t n_rows = T - lag, n_cols = 1 + static_cast<int64_t>(lag) * d;
+  std::vector<double> coef(static_cast<size_t>(std::max<int64_t>(n_cols, 1) * std::max<int64_t>(d, 1)));
+  std::vector<double> res(static_cast<size_t>(std::max<int64_t>(n_rows, 1) * std::max<int64_t>(d, 1)));
+  plg_status st{};
+  gpu::check(plg_estimate_var(gpu::context(), ts.values.data(), T, static_cast<int32_t>(d), std::max<int64_t>(T, 1),
+                              lag, coef.data(), res.data(), &st),
+             &st);
+  VarEstimate est;
+  for (int tau_i = 1; tau_i <= lag; ++tau_i) {  // M_tau(i, j) = coef(1 + (tau-1) d + j, i)
+    std::vector<double> M(static_cast<size_t>(d * d));
+    for (int64_t i = 0; i < d; ++i)
+      for (int64_t j = 0; j < d; ++j)
+        M[static_cast<size_t>(j * d + i)] = coef[static_cast<size_t>(i * n_cols + 1 + (tau_i - 1) * d + j)];
+    est.m_raw.push_back(std::move(M));
+  }
+  res.resize(static_cast<size_t>(n_rows * d));
+  est.residuals = DataMatrix(std::move(res), n_rows, d, ts.var_names);
+  return est;
+}
+
+VarEstimate estimate_var_qr(const DataMatrix& ts, int lag) {
   if (lag < 1) throw Error(ErrorCode::OutOfRange, "estimate_var: lag must be >= 1");
   const int64_t T = ts.samples();
   const int64_t d = ts.dims();

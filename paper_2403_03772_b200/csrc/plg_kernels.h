@@ -220,6 +220,16 @@ void launch_cholesky(double* S, int n, double tol, int* fail, cudaStream_t s);
 void launch_regress_rows(const double* L, int n, const int* order, const double* msd, int limit, double* beta,
                          double* B, int64_t ldb, cudaStream_t s);
 
+// VarLiNGAM front-end (var_kernels.cu): stacked design, normal equations, residuals.
+void launch_build_var_design(const double* ts, int64_t ldt, int64_t n_rows, int d, int lag, double* A, int64_t lda,
+                             int* nonfinite, cudaStream_t s);
+void launch_var_scale(const double* G, int64_t ldg, int n_cols, int d, double* S, double* S0, double* R, double* D,
+                      cudaStream_t s);
+void launch_var_solve(const double* L, const double* S0, const double* R, const double* D, int n_cols, int d,
+                      double* B, const int* fail, cudaStream_t s);
+void launch_var_resid(const double* A, int64_t lda, int64_t n_rows, int n_cols, int d, const double* B, double* E,
+                      int64_t lde, cudaStream_t s);
+
 // entropy_approx(u * scale) of one vector (kernels.cpp:123-148).
 void launch_entropy_vec(const double* u, int64_t n, double scale, double* out, const double* g_exp,
                         const double2* g_log, cudaStream_t s);

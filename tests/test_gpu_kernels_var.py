@@ -93,13 +93,52 @@ def test_c4_golden_order(plg):
     b0 = plg.gen_sparse_dag(d, avg_parents=2.0, seed=1, wmin=0.1, wmax=0.5)
     b1 = np.diag(plg.uniform_vector(d, 1, 0.2, 0.5))
     X = plg.sample_svar(b0, [np.asfortranarray(b1)], T=2500, burn_in=500, seed=1, noise=(0.0, 1.0), kind="laplace")
-    _, res = plg.estimate_var(X, 1)
+    _, res = plg._estimate_var_qr(X, 1)  # the golden's input: the reference's QR residuals
     assert hashlib.sha256(np.asfortranarray(res).tobytes(order="F")).hexdigest() == fx["sha256"]
+    _, res_gpu = plg.estimate_var(X, 1)  # the device path (normal equations) feeds fit_var_lingam
+    assert np.max(np.abs(res_gpu - res)) <= 1e-10 * np.max(np.abs(res))
     model = plg.fit_var_lingam(X, lag=1)
     assert model.b0.order == fx["order"]
     for t, row in fx["B_rows"].items():
         ref = np.asarray(row)
         assert np.all(np.abs(model.b0.weights[int(t)] - ref) <= 1e-6 * np.maximum(1.0, np.abs(ref)))
+
+
+def _svar(plg, d, T, seed, lag_diag=0.4, burn=200, kind="uniform", lags=1):
+    dag = plg.gen_sparse_dag(d, avg_parents=1.0, seed=seed, wmin=0.1, wmax=0.4)
+    Ms = [np.asfortranarray(np.eye(d) * (lag_diag / lags)) for _ in range(lags)]
+    return plg.sample_svar(dag, Ms, T=T, burn_in=burn, seed=seed, kind=kind)
+
+
+@pytest.mark.parametrize("d,T,lag,seed", [(6, 3000, 1, 3), (6, 3000, 2, 4), (40, 2000, 1, 5), (120, 1500, 3, 6)])
+def test_estimate_var_device_matches_qr(plg, d, T, lag, seed):
+    """estimate_var on the device (scaled normal equations + Cholesky + refinement) against
+    the reference's method (column-pivoted QR, host restatement) and numpy lstsq."""
+    X = _svar(plg, d, T, seed, kind="laplace", lags=lag)
+    ms, res = plg.estimate_var(X, lag)
+    ms_q, res_q = plg._estimate_var_qr(X, lag)
+    scale = np.max(np.abs(res_q))
+    assert res.shape == res_q.shape and len(ms) == len(ms_q) == lag
+    assert np.max(np.abs(res - res_q)) <= 1e-10 * scale
+    for a, b in zip(ms, ms_q):
+        assert np.max(np.abs(a - b)) <= 1e-10 * max(1.0, np.max(np.abs(b)))
+    Z = np.hstack([np.ones((T - lag, 1))] + [X[lag - t:T - t] for t in range(1, lag + 1)])
+    B = np.linalg.lstsq(Z, X[lag:], rcond=None)[0]
+    assert np.max(np.abs(res - (X[lag:] - Z @ B))) <= 1e-10 * scale
+
+
+def test_estimate_var_device_errors(plg):  # test_var_lingam.cpp:61-80, same codes as the host QR
+    rng = np.random.default_rng(31)
+    bad = rng.uniform(size=(100, 3))
+    bad[4, 1] = np.inf
+    for X, lag, code in ((np.full((100, 2), 3.5), 1, "SingularDesign"), (rng.uniform(size=(5, 3)), 1, "InsufficientRows"),
+                         (rng.uniform(size=(100, 3)), 0, "OutOfRange"), (bad, 1, "NonFinite")):
+        with pytest.raises(plg.Error) as e:
+            plg.estimate_var(X, lag)
+        assert e.value.code == code
+        with pytest.raises(plg.Error) as e2:
+            plg._estimate_var_qr(X, lag)
+        assert e2.value.code == code
 
 
 def _sampled_rounds(engine, oracle, X, rounds):

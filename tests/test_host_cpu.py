@@ -180,25 +180,26 @@ def _svar(plg, d, T, seed, lag_diag=0.4, burn=200, kind="uniform", b0=None):
 
 
 def test_estimate_var_matches_lstsq(plg):
+    # the host QR restatement (the reference's method; parity reference of the device path)
     X = _svar(plg, 6, 3000, 3)
-    ms, res = plg.estimate_var(X, 1)
+    ms, res = plg._estimate_var_qr(X, 1)
     Z = np.hstack([np.ones((X.shape[0] - 1, 1)), X[:-1]])
     B = np.linalg.lstsq(Z, X[1:], rcond=None)[0]
     assert np.allclose(ms[0], B[1:].T, atol=1e-12)
     assert np.allclose(res, X[1:] - Z @ B, atol=1e-12)
-    ms2, res2 = plg.estimate_var(X, 2)
+    ms2, res2 = plg._estimate_var_qr(X, 2)
     assert len(ms2) == 2 and res2.shape == (X.shape[0] - 2, 6)
 
 
 def test_estimate_var_reference_contracts(plg):  # test_var_lingam.cpp:39-97
     rng = np.random.default_rng(11)
-    ms, res = plg.estimate_var(rng.uniform(size=(10000, 3)), 1)
+    ms, res = plg._estimate_var_qr(rng.uniform(size=(10000, 3)), 1)
     assert np.all(np.abs(ms[0]) < 0.05) and res.shape[0] == 9999
     ar = _svar(plg, 2, 10000, 21, lag_diag=0.5, b0=plg.gen_two_level_dag(2, seed=0, edge_prob=1e-12))
     # (a 2-variable empty DAG; the AR(1) coefficient of each variable is recovered)
-    assert abs(plg.estimate_var(ar, 1)[0][0][0, 0] - 0.5) <= 0.05
+    assert abs(plg._estimate_var_qr(ar, 1)[0][0][0, 0] - 0.5) <= 0.05
     X = _svar(plg, 3, 4000, 41)
-    _, res = plg.estimate_var(X, 1)
+    _, res = plg._estimate_var_qr(X, 1)
     for eq in range(3):
         for reg in range(3):
             lagged = X[:-1, reg]
@@ -208,19 +209,19 @@ def test_estimate_var_reference_contracts(plg):  # test_var_lingam.cpp:39-97
 
 def test_estimate_var_errors(plg):  # test_var_lingam.cpp:61-80
     with pytest.raises(plg.Error) as e:
-        plg.estimate_var(np.full((100, 2), 3.5), 1)
+        plg._estimate_var_qr(np.full((100, 2), 3.5), 1)
     assert e.value.code == "SingularDesign"
     rng = np.random.default_rng(31)
     with pytest.raises(plg.Error) as e:
-        plg.estimate_var(rng.uniform(size=(5, 3)), 1)
+        plg._estimate_var_qr(rng.uniform(size=(5, 3)), 1)
     assert e.value.code == "InsufficientRows"
     with pytest.raises(plg.Error) as e:
-        plg.estimate_var(rng.uniform(size=(100, 3)), 0)
+        plg._estimate_var_qr(rng.uniform(size=(100, 3)), 0)
     assert e.value.code == "OutOfRange"
     bad = rng.uniform(size=(100, 3))
     bad[4, 1] = np.inf
     with pytest.raises(plg.Error) as e:
-        plg.estimate_var(bad, 1)
+        plg._estimate_var_qr(bad, 1)
     assert e.value.code == "NonFinite"
 
 
