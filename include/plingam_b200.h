@@ -130,6 +130,10 @@ int plg_fit_weights(plg_ctx* ctx, const double* X, int64_t n, int32_t d, int64_t
  * InsufficientRows (T < lag + 2d or fewer rows than coefficients), SingularDesign. */
 int plg_estimate_var(plg_ctx* ctx, const double* ts, int64_t T, int32_t d, int64_t ld, int32_t lag,
                      double* coef_out, double* resid_out, plg_status* st);
+/* VarLiNGAM lag weights (var_lingam.cpp:55-70): out[t] = (I - B0) M[t] for t < lag, all d x d
+ * column-major (M and out hold lag matrices back to back). */
+int plg_var_lagged_weights(plg_ctx* ctx, const double* B0, const double* M, int32_t d, int32_t lag, double* out,
+                           plg_status* st);
 /* The element functions of plingam::kernels (include/plingam/kernels.hpp:25-70), exposed
  * by the reference's Python module (bindings/pymodule.cpp:79-96):
  *   standardize (kernels.cpp:92-104; bit-identical: left-to-right sums),

@@ -1384,6 +1384,29 @@ extern "C" int plg_estimate_var(plg_ctx* c, const double* ts, int64_t T, int32_t
   return ok(st);
 }
 
+extern "C" int plg_var_lagged_weights(plg_ctx* c, const double* B0, const double* M, int32_t d, int32_t lag,
+                                      double* out, plg_status* st) {
+  // var_lingam.cpp:55-70: B_tau = (I - B0) M_tau = M_tau - B0 M_tau for every lag, one FP64
+  // GEMM launch per lag (var_resid_kernel with Z = B0, Y = B = M_tau).
+  if (!c) return set_status(st, PLG_OutOfRange, -1, -1, "null context");
+  if (d < 1 || lag < 1) return set_status(st, PLG_OutOfRange, -1, -1, "var weights: need d >= 1 and lag >= 1");
+  if (int rc = begin_call(c, st)) return rc;
+  const size_t dd = static_cast<size_t>(d) * d;
+  PLG_CUDA(c->part.reserve(3 * dd));
+  double* A = c->part.p;  // [B0 | M_tau], d x 2d column-major
+  double* E = A + 2 * dd;
+  PLG_CUDA(cudaMemcpyAsync(A, B0, dd * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  for (int t = 0; t < lag; ++t) {
+    PLG_CUDA(cudaMemcpyAsync(A + dd, M + t * dd, dd * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    plg::launch_var_resid(A, d, d, d, d, A + dd, E, d, c->stream);
+    ++c->launches;
+    PLG_CUDA(cudaMemcpyAsync(out + t * dd, E, dd * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    PLG_CUDA(cudaStreamSynchronize(c->stream));
+  }
+  PLG_CUDA(cudaGetLastError());
+  return ok(st);
+}
+
 extern "C" int plg_fit_weights(plg_ctx* c, const double* X, int64_t n, int32_t d, int64_t ld,
                                const int32_t* order, double* B_out, int32_t* used_pinv,
                                plg_status* st) {

@@ -184,19 +184,16 @@ VarModel fit_varlingam(const DataMatrix& ts, int lag, const DirectLingamConfig& 
   model.b0 = DirectLingam(cfg).fit(est.residuals);
   model.m_raw = std::move(est.m_raw);
   const int d = model.b0.d;
-  for (const auto& M : model.m_raw) {  // (I - B0) * M
-    std::vector<double> out(static_cast<size_t>(d) * d, 0.0);
-    for (int j = 0; j < d; ++j)
-      for (int i = 0; i < d; ++i) {
-        double s = 0.0;
-        for (int k = 0; k < d; ++k) {
-          const double a = (i == k ? 1.0 : 0.0) - model.b0(i, k);
-          s += a * M[static_cast<size_t>(j) * d + k];
-        }
-        out[static_cast<size_t>(j) * d + i] = s;
-      }
-    model.b_lagged.push_back(std::move(out));
-  }
+  // (I - B0) * M_tau on the device (plg_var_lagged_weights)
+  const size_t dd = static_cast<size_t>(d) * d;
+  std::vector<double> ms(dd * model.m_raw.size()), out(dd * model.m_raw.size());
+  for (size_t t = 0; t < model.m_raw.size(); ++t) std::copy(model.m_raw[t].begin(), model.m_raw[t].end(), ms.begin() + t * dd);
+  plg_status st{};
+  gpu::check(plg_var_lagged_weights(gpu::context(), model.b0.weights.data(), ms.data(), d,
+                                    static_cast<int32_t>(model.m_raw.size()), out.data(), &st),
+             &st);
+  for (size_t t = 0; t < model.m_raw.size(); ++t)
+    model.b_lagged.emplace_back(out.begin() + t * dd, out.begin() + (t + 1) * dd);
   return model;
 }
 
