@@ -466,6 +466,11 @@ int search_round_pruned(plg_ctx* c, int64_t n, int64_t ldw, int d, int u, const 
     return v ? std::atoi(v) : 0;
   }();
   a.seg_major = seg_major;
+  static const double top_ratio = [] {
+    const char* v = std::getenv("PLG_TOP_RATIO");
+    return v ? std::atof(v) : 0.0;
+  }();
+  a.top_ratio = top_ratio;
   a.g_exp = c->g_exp;
   a.g_log = c->g_log;
   a.err = c->err.p;

@@ -239,7 +239,11 @@ __global__ void __launch_bounds__(kTopThreads) prune_top_kernel(const PruneArgs 
   __shared__ int fp[kMaxR];
   warp_merge_best(bv, bp, R, fv, fp);
   __syncwarp();
-  if (lane < R && fp[lane] >= 0) a.state_out[fp[lane]] = 2;
+  // a clear favourite (its predicted k below top_ratio x the runner-up's) gets the full row
+  // alone; otherwise the R best do (k* must be tight for pruning to bite)
+  int r_eff = R;
+  if (a.top_ratio > 0.0 && R >= 2 && fp[1] >= 0 && fv[0] < a.top_ratio * fv[1]) r_eff = 1;
+  if (lane < r_eff && fp[lane] >= 0) a.state_out[fp[lane]] = 2;
 }
 
 // ---- select: each row's partners for one stage, ascending, into rowsel[p * u + i] ----
