@@ -193,6 +193,7 @@ struct plg_ctx {
   int emulate_world = 1;        // PLG_EMULATE_WORLD=W (tests): a single rank runs the W-rank shard schedule
   double prune_beta = 1.1;      // PLG_PRUNE_BETA > 0: hybrid refinement (deficit cut when smaller than the step)
   int64_t prune_sub = 0;        // PLG_PRUNE_SUB: samples of round 0's prediction pass (0: exhaustive round 0)
+  int prune_min_u = plg::kSmallU;  // PLG_PRUNE_MIN_U: rounds with more candidates are pruned
   DevBuf<double> Md, KN, pk, L, ppart, pres;
   DevBuf<int> st0, st1, rowsel, off, pwork, pdone, crow, cand, alive;
   DevBuf<unsigned long long> kstar, evals;
@@ -281,6 +282,7 @@ void parse_prune_env(plg_ctx* ctx) {
   if (const char* v = std::getenv("PLG_EMULATE_WORLD")) ctx->emulate_world = std::max(1, std::atoi(v));
   if (const char* v = std::getenv("PLG_PRUNE_BETA")) ctx->prune_beta = std::atof(v);
   if (const char* v = std::getenv("PLG_PRUNE_SUB")) ctx->prune_sub = std::max<int64_t>(0, std::atoll(v));
+  if (const char* v = std::getenv("PLG_PRUNE_MIN_U")) ctx->prune_min_u = std::max(8, std::atoi(v));
 }
 
 int ctx_init(plg_ctx* ctx, int device, plg_status* st) {
@@ -601,7 +603,7 @@ int reserve_prune(plg_ctx* c, int64_t n, int d, plg_status* st) {
   const size_t dd = static_cast<size_t>(d) * d;
   size_t nseg = static_cast<size_t>(prune_seg_plan(n).nseg);
   if (c->prune_tile_seg)
-    for (int u = d; u > plg::kSmallU; --u) nseg = std::max(nseg, static_cast<size_t>(seg_plan(u, n).nseg));
+    for (int u = d; u > c->prune_min_u; --u) nseg = std::max(nseg, static_cast<size_t>(seg_plan(u, n).nseg));
   PLG_CUDA(c->Md.reserve(dd));
   PLG_CUDA(c->KN.reserve(dd));
   PLG_CUDA(c->rowsel.reserve(dd));
@@ -736,7 +738,7 @@ int causal_order_impl(plg_ctx* c, const double* dX, int64_t ldx, int64_t n, int 
   const int rounds = (max_rounds < 0) ? d - 1 : std::min(max_rounds, d - 1);
   // Exact pruning needs a previous exhaustive round's knowledge and pays off above the
   // replicated small-round size.
-  const bool prune = c->prune && !c->hook && d > plg::kSmallU + 1 && rounds > 1;
+  const bool prune = c->prune && !c->hook && d > c->prune_min_u + 1 && rounds > 1;
   c->pairs_done = 0;
   if (prune)
     if (int rc = reserve_prune(c, n, d, st)) return rc;
@@ -760,7 +762,7 @@ int causal_order_impl(plg_ctx* c, const double* dX, int64_t ldx, int64_t n, int 
       if (int rc = search_round(c, c->prune_sub, ldw, d, u, act_cur, r, st, c->KN.p, false)) return rc;
       c->pairs_done = before + (c->pairs_done - before) * c->prune_sub / n;  // in full-n pair units
       if (int rc = search_round_pruned(c, n, ldw, d, u, act_cur, r, st, false)) return rc;
-    } else if (prune && r > 0 && u > plg::kSmallU) {
+    } else if (prune && r > 0 && u > c->prune_min_u) {
       if (int rc = search_round_pruned(c, n, ldw, d, u, act_cur, r, st)) return rc;
     } else if (int rc = search_round(c, n, ldw, d, u, act_cur, r, st, (prune && r == 0) ? c->KN.p : nullptr,
                                      r > 0)) {
