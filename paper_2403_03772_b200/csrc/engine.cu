@@ -168,6 +168,7 @@ struct plg_ctx {
   cudaEvent_t ev_side = nullptr;     // side stream: predictions + probe selection are done
   bool gram_ready = false;           // ev_gram recorded by the previous round of this call
   ncclComm_t comm = nullptr;
+  bool force_nccl = false;  // PLG_NCCL_SELFTEST=1 on a 1-rank dist context: every exchange through NCCL
   bool timing = true;
 
   double* g_exp = nullptr;
@@ -400,7 +401,7 @@ int search_round(plg_ctx* c, int64_t n, int64_t ldw, int ldc, int u, const int* 
     c->launches += 2;
   }
   pair_timer_end(c, tm);
-  const bool exchange = c->world > 1 && !rp.replicated;
+  const bool exchange = (c->world > 1 || c->force_nccl) && !rp.replicated;
   if (exchange) {
     // One grouped exchange per round: the entropy tiles (in place, rank slots of tpr tiles)
     // and every rank's error key.
@@ -503,7 +504,7 @@ int search_round_pruned(plg_ctx* c, int64_t n, int64_t ldw, int d, int u, const 
       PLG_CUDA(cudaEventRecord(c->ev_side, ss));
       PLG_CUDA(cudaStreamWaitEvent(c->stream, c->ev_side, 0));
     }
-    if (shards == 1) {
+    if (shards == 1 && !c->force_nccl) {
       const size_t tm = pair_timer_begin(c);
       plg::launch_prune_pairs(a, c->stream);
       pair_timer_end(c, tm);
@@ -518,11 +519,12 @@ int search_round_pruned(plg_ctx* c, int64_t n, int64_t ldw, int d, int u, const 
       int32_t cnt = 0, kb = 0, ke = 0;
       plg_plan_list_shard(total, 0, shards, &kb, &ke, &cnt);
       a.res = c->pres.p;
-      for (int r = (c->world > 1 ? c->rank : 0); r < (c->world > 1 ? c->rank + 1 : shards); ++r) {
+      const bool real = c->world > 1 || c->force_nccl;  // else: emulated ranks, one after the other
+      for (int r = (real ? c->rank : 0); r < (real ? c->rank + 1 : shards); ++r) {
         plg_plan_list_shard(total, r, shards, &kb, &ke, &cnt);
         a.k_begin = kb;
         a.k_end = ke;
-        if (r > (c->world > 1 ? c->rank : 0))  // emulated ranks share one set of fetch counters
+        if (r > (real ? c->rank : 0))  // emulated ranks share one set of fetch counters
           PLG_CUDA(cudaMemsetAsync(c->pwork.p, 0, (kPruneBatch > 0 ? (cnt / kPruneBatch + 2) : 2) * sizeof(int),
                                    c->stream));
         const size_t tm = pair_timer_begin(c);
@@ -530,7 +532,7 @@ int search_round_pruned(plg_ctx* c, int64_t n, int64_t ldw, int d, int u, const 
         pair_timer_end(c, tm);
         ++c->launches;
       }
-      if (c->world > 1 && cnt > 0) {
+      if ((c->world > 1 || c->force_nccl) && cnt > 0) {
         NcclApi& api = nccl();
         const ncclResult_t r = api.AllGather(c->pres.p + static_cast<size_t>(c->rank) * cnt, c->pres.p, cnt,
                                              ncclDouble, c->comm, c->stream);
@@ -622,7 +624,7 @@ int reserve_prune(plg_ctx* c, int64_t n, int d, plg_status* st) {
   PLG_CUDA(c->cand.reserve(static_cast<size_t>(d) * 8));
   PLG_CUDA(c->alive.reserve(static_cast<size_t>(d) + 1));
   PLG_CUDA(cudaMemsetAsync(c->alive.p, 0, sizeof(int), c->stream));
-  if (c->world > 1 || c->emulate_world > 1) PLG_CUDA(c->pres.reserve(max_list + 64));
+  if (c->world > 1 || c->emulate_world > 1 || c->force_nccl) PLG_CUDA(c->pres.reserve(max_list + 64));
   PLG_CUDA(cudaMemsetAsync(c->pdone.p, 0, (kPruneBatch / 32) * sizeof(int), c->stream));
   PLG_CUDA(cudaMemsetAsync(c->evals.p, 0, (1 + plg::kMaxPruneStages) * sizeof(unsigned long long), c->stream));
   return 0;
@@ -892,7 +894,9 @@ int plg_ctx_create_dist(int32_t device, int32_t rank, int32_t world, const void*
     return set_status(st, PLG_OutOfRange, -1, -1, "invalid rank %d / world %d (1..64 ranks)", rank, world);
   plg_ctx* c = new plg_ctx();
   int rc = ctx_init(c, device, st);
-  if (!rc && world > 1) {
+  const char* selftest = std::getenv("PLG_NCCL_SELFTEST");
+  c->force_nccl = world == 1 && selftest && !strcmp(selftest, "1");
+  if (!rc && (world > 1 || c->force_nccl)) {
     NcclApi& api = nccl();
     if (!api.loaded) {
       rc = set_status(st, PLG_NcclError, -1, -1, "libnccl.so.2 not loadable");

@@ -128,3 +128,30 @@ def test_pruned_rounds_edge_cases_match_exhaustive(seed, d, n, kind):
     assert r["prune"] == r["full"], r
     if kind != "none":
         assert r["prune"].get("code") == "ZeroVariance", r
+
+
+_NCCL_CHILD = r"""
+import json, sys
+sys.path.insert(0, %r)
+import paper_2403_03772_b200 as plg
+dag = plg.gen_sparse_dag(300, avg_parents=2.0, seed=7)
+X = plg.sample_lingam(dag, 4000, seed=7, kind="laplace")
+out = {}
+for mode in ("nccl", "local"):
+    eng = plg.Engine.distributed(0, 0, 1, plg.nccl_unique_id()) if mode == "nccl" else plg.Engine(0)
+    out[mode] = {"order": eng.causal_order(X), "k": [float(v).hex() for v in eng.round_k()]}
+print(json.dumps(out))
+"""
+
+
+def test_nccl_exchange_paths_on_one_rank():
+    # The NCCL call sites of both multi-GPU schedules (tile all-gather of the exhaustive
+    # round 0, slice all-gather + scatter of every pruned stage) run through a real NCCL
+    # communicator of one rank (PLG_NCCL_SELFTEST=1): same order and winning-k bits as a
+    # local context. Only one GPU is reachable from this build, so this is the NCCL path's
+    # hardware check; the slice arithmetic for W > 1 is covered by the emulated schedule.
+    env = dict(os.environ, PLG_NCCL_SELFTEST="1")
+    out = subprocess.run([sys.executable, "-c", _NCCL_CHILD % ROOT], env=env, capture_output=True, text=True,
+                         check=True, timeout=600)
+    r = json.loads(out.stdout.strip().splitlines()[-1])
+    assert r["nccl"] == r["local"]
