@@ -101,6 +101,9 @@ def test_package_fails_loudly_without_gpu(plg):
     with pytest.raises(plg.Error) as e:
         plg.causal_order(X)
     assert e.value.code == "DeviceError"
+    with pytest.raises(plg.Error) as e:  # the VarLiNGAM front-end has no CPU fallback either
+        plg.estimate_var(np.asfortranarray(np.random.default_rng(1).uniform(size=(200, 3))), 1)
+    assert e.value.code == "DeviceError"
 
 
 def test_host_validation_before_device(plg):
