@@ -154,7 +154,7 @@ SegPlan prune_seg_plan(int64_t n) {
   const int64_t seg_len = std::max<int64_t>(prune_seg_min(), round_up((n + 127) / 128, 4));
   return {static_cast<int>((n + seg_len - 1) / seg_len), static_cast<int>(seg_len)};
 }
-constexpr int kPruneBatch = 131072;  // pairs per batch of the list kernel (part-buffer capacity)
+constexpr int kPruneBatchDefault = 131072;  // pairs per batch of the list kernel (part-buffer capacity)
 
 }  // namespace
 
@@ -195,6 +195,7 @@ struct plg_ctx {
   double prune_beta = 1.1;      // PLG_PRUNE_BETA > 0: hybrid refinement (deficit cut when smaller than the step)
   int64_t prune_sub = 0;        // PLG_PRUNE_SUB: samples of round 0's prediction pass (0: exhaustive round 0)
   int prune_min_u = plg::kSmallU;  // PLG_PRUNE_MIN_U: rounds with more candidates are pruned
+  int prune_batch = kPruneBatchDefault;  // PLG_PRUNE_BATCH (tests: small batches exercise the grid barrier)
   DevBuf<double> Md, KN, pk, L, ppart, pres;
   DevBuf<int> st0, st1, rowsel, off, pwork, pdone, crow, cand, alive;
   DevBuf<unsigned long long> kstar, evals;
@@ -284,6 +285,7 @@ void parse_prune_env(plg_ctx* ctx) {
   if (const char* v = std::getenv("PLG_PRUNE_BETA")) ctx->prune_beta = std::atof(v);
   if (const char* v = std::getenv("PLG_PRUNE_SUB")) ctx->prune_sub = std::max<int64_t>(0, std::atoll(v));
   if (const char* v = std::getenv("PLG_PRUNE_MIN_U")) ctx->prune_min_u = std::max(8, std::atoi(v));
+  if (const char* v = std::getenv("PLG_PRUNE_BATCH")) ctx->prune_batch = std::max(64, std::atoi(v) / 32 * 32);
 }
 
 int ctx_init(plg_ctx* ctx, int device, plg_status* st) {
@@ -461,7 +463,7 @@ int search_round_pruned(plg_ctx* c, int64_t n, int64_t ldw, int d, int u, const 
   a.part = c->ppart.p;
   a.work = c->pwork.p;
   a.done = c->pdone.p;
-  a.batch = kPruneBatch;
+  a.batch = c->prune_batch;
   a.seg_len = sp.seg_len;
   a.nseg = sp.nseg;
   static const int seg_major = [] {
@@ -525,7 +527,7 @@ int search_round_pruned(plg_ctx* c, int64_t n, int64_t ldw, int d, int u, const 
         a.k_begin = kb;
         a.k_end = ke;
         if (r > (real ? c->rank : 0))  // emulated ranks share one set of fetch counters
-          PLG_CUDA(cudaMemsetAsync(c->pwork.p, 0, (kPruneBatch > 0 ? (cnt / kPruneBatch + 2) : 2) * sizeof(int),
+          PLG_CUDA(cudaMemsetAsync(c->pwork.p, 0, (cnt / c->prune_batch + 2) * sizeof(int),
                                    c->stream));
         const size_t tm = pair_timer_begin(c);
         plg::launch_prune_pairs(a, c->stream);
@@ -616,16 +618,16 @@ int reserve_prune(plg_ctx* c, int64_t n, int d, plg_status* st) {
   PLG_CUDA(c->st1.reserve(d));
   PLG_CUDA(c->kstar.reserve(1));
   PLG_CUDA(c->evals.reserve(1 + plg::kMaxPruneStages));
-  PLG_CUDA(c->ppart.reserve(nseg * kPruneBatch * 4));
+  PLG_CUDA(c->ppart.reserve(nseg * c->prune_batch * 4));
   const size_t max_list = dd + d;  // per-stage list bound: u (u - 1) entries + slack
-  PLG_CUDA(c->pwork.reserve(max_list / kPruneBatch + 2));
-  PLG_CUDA(c->pdone.reserve(kPruneBatch / 32));
+  PLG_CUDA(c->pwork.reserve(max_list / c->prune_batch + 2));
+  PLG_CUDA(c->pdone.reserve(c->prune_batch / 32));
   PLG_CUDA(c->crow.reserve(max_list / 32 + 2));
   PLG_CUDA(c->cand.reserve(static_cast<size_t>(d) * 8));
   PLG_CUDA(c->alive.reserve(static_cast<size_t>(d) + 1));
   PLG_CUDA(cudaMemsetAsync(c->alive.p, 0, sizeof(int), c->stream));
   if (c->world > 1 || c->emulate_world > 1 || c->force_nccl) PLG_CUDA(c->pres.reserve(max_list + 64));
-  PLG_CUDA(cudaMemsetAsync(c->pdone.p, 0, (kPruneBatch / 32) * sizeof(int), c->stream));
+  PLG_CUDA(cudaMemsetAsync(c->pdone.p, 0, (c->prune_batch / 32) * sizeof(int), c->stream));
   PLG_CUDA(cudaMemsetAsync(c->evals.p, 0, (1 + plg::kMaxPruneStages) * sizeof(unsigned long long), c->stream));
   return 0;
 }

@@ -46,9 +46,11 @@ print(json.dumps(out))
 """
 
 
-def _run(d, n, seed, kind, tileseg, emulate_world=1):
+def _run(d, n, seed, kind, tileseg, emulate_world=1, batch=None):
     env = dict(os.environ, PLG_PRUNE_TILESEG="1" if tileseg else "0", PLG_EMULATE_WORLD=str(emulate_world))
     env.pop("PLG_PRUNE", None)
+    if batch:
+        env["PLG_PRUNE_BATCH"] = str(batch)
     out = subprocess.run([sys.executable, "-c", _CHILD % (ROOT, d, n, seed, kind)], env=env,
                          capture_output=True, text=True, check=True, timeout=900)
     return json.loads(out.stdout.strip().splitlines()[-1])
@@ -155,3 +157,11 @@ def test_nccl_exchange_paths_on_one_rank():
                          check=True, timeout=600)
     r = json.loads(out.stdout.strip().splitlines()[-1])
     assert r["nccl"] == r["local"]
+
+
+def test_pruned_rounds_multi_batch_lists():
+    # lists longer than the part buffer run batch after batch with a grid barrier between
+    # them; a 256-pair batch makes every stage of this run multi-batch
+    r = _run(260, 3001, 11, "t3", tileseg=True, batch=256)
+    assert r["prune"]["order"] == r["full"]["order"]
+    assert r["prune"]["k"] == r["full"]["k"]
