@@ -756,6 +756,34 @@ __device__ __forceinline__ void eval_segment(const double* wi, const double* wj,
   for (; t < t1; ++t) ede2<kClampA>(wi[t], wj[t], s1, bs1, s2, bs2, acc1, acc2, tp);
 }
 
+// Variant 0's loop with the first step already loaded by the caller (kVar 4: the item's
+// first data loads are issued before the pair's scales are computed, so their latency
+// overlaps the Gram loads, divisions and square roots instead of following them).
+template <bool kClampA, typename Tab>
+__device__ __forceinline__ void eval_segment_pre(const double* wi, const double* wj, int64_t t0, int64_t t1, double s1,
+                                                 double bs1, double s2, double bs2, EdeAcc& acc1, EdeAcc& acc2,
+                                                 const Tab& tp, double2 xa, double2 xb, double2 ya, double2 yb) {
+  int64_t t = t0;
+  const int nstep = static_cast<int>((t1 - t) >> 2);
+  if (nstep > 0) {
+    const double2* pi = reinterpret_cast<const double2*>(wi + t);
+    const double2* pj = reinterpret_cast<const double2*>(wj + t);
+#pragma unroll 1
+    for (int i = 1; i <= nstep; ++i) {
+      const double2 cxa = xa, cxb = xb, cya = ya, cyb = yb;
+      pi += 2;
+      pj += 2;
+      if (i < nstep) xa = __ldg(pi), xb = __ldg(pi + 1), ya = __ldg(pj), yb = __ldg(pj + 1);
+      ede2<kClampA>(cxa.x, cya.x, s1, bs1, s2, bs2, acc1, acc2, tp);
+      ede2<kClampA>(cxa.y, cya.y, s1, bs1, s2, bs2, acc1, acc2, tp);
+      ede2<kClampA>(cxb.x, cyb.x, s1, bs1, s2, bs2, acc1, acc2, tp);
+      ede2<kClampA>(cxb.y, cyb.y, s1, bs1, s2, bs2, acc1, acc2, tp);
+    }
+    t += 4 * static_cast<int64_t>(nstep);
+  }
+  for (; t < t1; ++t) ede2<kClampA>(wi[t], wj[t], s1, bs1, s2, bs2, acc1, acc2, tp);
+}
+
 // M_pq and M_qp = -M_pq into the round's table; KN (the next rounds' predictions) gets
 // min(0, M)^2 in both directions.
 __device__ __forceinline__ void store_pair(const PruneArgs& a, int p, int q, double mpq) {
@@ -836,14 +864,26 @@ __global__ void __launch_bounds__(kListThreads, 2) prune_pairs_kernel(const Prun
         int p, q;
         list_entry(a, base + kk, p, q);
         const int ci = a.act[p], cj = a.act[q];
-        double s1, bs1, s2, bs2;
-        pair_scales(a.C, a.ldc, ci, cj, s1, bs1, s2, bs2);  // collinear pairs: zeros (flagged by predict)
         const double* wi = a.W + static_cast<int64_t>(ci) * a.ldw;
         const double* wj = a.W + static_cast<int64_t>(cj) * a.ldw;
         const int64_t t0 = static_cast<int64_t>(seg) * a.seg_len;  // multiple of 4: 32-byte aligned
         const int64_t t1 = lmin(a.n, t0 + a.seg_len);
         EdeAcc acc1, acc2;
-        eval_segment<kClampA, kVar>(wi, wj, t0, t1, s1, bs1, s2, bs2, acc1, acc2, tp);
+        if (kVar == 4) {
+          double2 xa = make_double2(0.0, 0.0), xb = xa, ya = xa, yb = xa;
+          if (t0 + 3 < t1) {
+            const double2* pi = reinterpret_cast<const double2*>(wi + t0);
+            const double2* pj = reinterpret_cast<const double2*>(wj + t0);
+            xa = __ldg(pi), xb = __ldg(pi + 1), ya = __ldg(pj), yb = __ldg(pj + 1);
+          }
+          double s1, bs1, s2, bs2;
+          pair_scales(a.C, a.ldc, ci, cj, s1, bs1, s2, bs2);  // collinear pairs: zeros (flagged by predict)
+          eval_segment_pre<kClampA>(wi, wj, t0, t1, s1, bs1, s2, bs2, acc1, acc2, tp, xa, xb, ya, yb);
+        } else {
+          double s1, bs1, s2, bs2;
+          pair_scales(a.C, a.ldc, ci, cj, s1, bs1, s2, bs2);  // collinear pairs: zeros (flagged by predict)
+          eval_segment<kClampA, kVar>(wi, wj, t0, t1, s1, bs1, s2, bs2, acc1, acc2, tp);
+        }
         double2* dst = reinterpret_cast<double2*>(a.part + (static_cast<int64_t>(seg) * a.batch + kk) * 4);
         __stcg(dst, make_double2(acc_lc(acc1), acc_pdf(acc1)));
         __stcg(dst + 1, make_double2(acc_lc(acc2), acc_pdf(acc2)));
@@ -962,12 +1002,13 @@ void launch_prune_scan(const PruneArgs& a, cudaStream_t s) { prune_scan_kernel<<
 void launch_prune_pairs(const PruneArgs& a, cudaStream_t s) {
   static const int var = [] {  // PLG_LIST_VAR: load-pipeline variant (tuning knob)
     const char* v = std::getenv("PLG_LIST_VAR");
-    return v ? std::atoi(v) : 0;
+    return v ? std::atoi(v) : 4;
   }();
-  if (a.n > 90000) launch_pairs_cfg<true, 0>(a, s);
+  if (a.n > 90000) launch_pairs_cfg<true, 4>(a, s);
   else if (var == 1) launch_pairs_cfg<false, 1>(a, s);
   else if (var == 2) launch_pairs_cfg<false, 2>(a, s);
-  else launch_pairs_cfg<false, 0>(a, s);
+  else if (var == 0) launch_pairs_cfg<false, 0>(a, s);
+  else launch_pairs_cfg<false, 4>(a, s);
 }
 
 void launch_prune_scatter(const PruneArgs& a, int total, cudaStream_t s) {
@@ -981,6 +1022,6 @@ void launch_prune_bound(const PruneArgs& a, int pass, cudaStream_t s) {
   prune_bound_kernel<<<(a.u + 7) / 8, 256, 0, s>>>(a, pass);
 }
 
-int prune_pairs_grid() { return pairs_grid_for<false, 0>(); }
+int prune_pairs_grid() { return pairs_grid_for<false, 4>(); }
 
 }  // namespace plg
