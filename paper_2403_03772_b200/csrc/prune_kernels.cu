@@ -1002,13 +1002,13 @@ void launch_prune_scan(const PruneArgs& a, cudaStream_t s) { prune_scan_kernel<<
 void launch_prune_pairs(const PruneArgs& a, cudaStream_t s) {
   static const int var = [] {  // PLG_LIST_VAR: load-pipeline variant (tuning knob)
     const char* v = std::getenv("PLG_LIST_VAR");
-    return v ? std::atoi(v) : 4;
+    return v ? std::atoi(v) : 0;
   }();
-  if (a.n > 90000) launch_pairs_cfg<true, 4>(a, s);
+  if (a.n > 90000) launch_pairs_cfg<true, 0>(a, s);
   else if (var == 1) launch_pairs_cfg<false, 1>(a, s);
   else if (var == 2) launch_pairs_cfg<false, 2>(a, s);
-  else if (var == 0) launch_pairs_cfg<false, 0>(a, s);
-  else launch_pairs_cfg<false, 4>(a, s);
+  else if (var == 4) launch_pairs_cfg<false, 4>(a, s);
+  else launch_pairs_cfg<false, 0>(a, s);
 }
 
 void launch_prune_scatter(const PruneArgs& a, int total, cudaStream_t s) {
@@ -1022,6 +1022,6 @@ void launch_prune_bound(const PruneArgs& a, int pass, cudaStream_t s) {
   prune_bound_kernel<<<(a.u + 7) / 8, 256, 0, s>>>(a, pass);
 }
 
-int prune_pairs_grid() { return pairs_grid_for<false, 4>(); }
+int prune_pairs_grid() { return pairs_grid_for<false, 0>(); }
 
 }  // namespace plg
