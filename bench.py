@@ -237,6 +237,7 @@ def run_ours(args, world, rank, local):
         torch.cuda.set_device(local)
         eng = plg.Engine(local)
     eng.set_prune(not args.no_prune)
+    eng.set_detail_timing(True)  # per-launch pair / residualisation time for the rooflines
     X = make_input(args.config)
     dX = torch.from_numpy(np.ascontiguousarray(X.T)).to(f"cuda:{local}")  # column j contiguous
     ptr = dX.data_ptr()
@@ -267,7 +268,8 @@ def run_ours(args, world, rank, local):
     P = pair_evals(d)
     value = P * args.steps / dev_s
 
-    # e2e: the public API with the matrix in pinned host memory
+    # e2e: the public API with the matrix in pinned host memory (no per-launch timing)
+    eng.set_detail_timing(False)
     pinned = torch.empty((d, n), dtype=torch.float64, pin_memory=True)
     pinned.copy_(torch.from_numpy(np.ascontiguousarray(X.T)))
     Xh = pinned.numpy().T  # F-contiguous (n, d) view, zero-copy into the binding

@@ -172,6 +172,10 @@ int plg_plan_list_shard(int32_t total, int32_t rank, int32_t world, int32_t* beg
 /* tile index -> (bi, bj), bi <= bj, row-major over the upper triangle */
 int plg_tile_decode(int32_t t, int32_t nb, int32_t* bi, int32_t* bj);
 
+/* Per-launch timing of the pair-evaluation and residualisation launches (plg_stats.pair_ms,
+ * resid_ms; default off). Off: only the call's total device time is measured, which saves
+ * the host ~10k event queries per large causal order. */
+int plg_set_detail_timing(plg_ctx* ctx, int32_t enable, plg_status* st);
 /* Stats of the last call on ctx. */
 int plg_last_stats(plg_ctx* ctx, plg_stats* out);
 

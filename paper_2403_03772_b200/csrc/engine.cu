@@ -170,6 +170,7 @@ struct plg_ctx {
   ncclComm_t comm = nullptr;
   bool force_nccl = false;  // PLG_NCCL_SELFTEST=1 on a 1-rank dist context: every exchange through NCCL
   bool timing = true;
+  bool detail_timing = false;  // per-launch pair / residualisation intervals (plg_set_detail_timing)
 
   double* g_exp = nullptr;
   double2* g_log = nullptr;
@@ -219,7 +220,7 @@ namespace {
 
 // CUDA-event interval around one pair-evaluation launch (plg_stats.pair_ms / pair_launches).
 size_t pair_timer_begin(plg_ctx* c, char kind = 0) {
-  if (!c->timing) return 0;
+  if (!c->timing || !c->detail_timing) return 0;
   const size_t i = 3 + 2 * c->ev_pairs;
   if (c->events(i + 2) != cudaSuccess) return 0;
   if (c->ev_kind.size() <= c->ev_pairs) c->ev_kind.resize(c->ev_pairs + 1);
@@ -1221,6 +1222,12 @@ int plg_last_round_k(plg_ctx* c, double* out, int32_t cap, int32_t* count, plg_s
   const int n = std::min(cap, c->last.rounds);
   *count = n;
   if (n > 0) PLG_CUDA(cudaMemcpy(out, c->rk.p, n * sizeof(double), cudaMemcpyDeviceToHost));
+  return ok(st);
+}
+
+int plg_set_detail_timing(plg_ctx* c, int32_t enable, plg_status* st) {
+  if (!c) return set_status(st, PLG_OutOfRange, -1, -1, "null context");
+  c->detail_timing = enable != 0;
   return ok(st);
 }
 

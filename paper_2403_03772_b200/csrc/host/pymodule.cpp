@@ -539,6 +539,13 @@ PYBIND11_MODULE(_core, m) {
              return k;
            })
       .def(
+          "set_detail_timing",
+          [](Engine& e, bool enable) {
+            plg_status st{};
+            gpu::check(plg_set_detail_timing(e.ctx, enable ? 1 : 0, &st), &st);
+          },
+          py::arg("enable"))
+      .def(
           "set_prune",
           [](Engine& e, bool enable) {
             plg_status st{};

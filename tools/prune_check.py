@@ -24,6 +24,7 @@ def main():
 
     X = np.asfortranarray(bench.make_input(args.config))
     eng = plg.Engine(0)
+    eng.set_detail_timing(True)
     res = {}
     for mode in ("prune", "full"):
         eng.set_prune(mode == "prune")

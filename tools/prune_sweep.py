@@ -15,6 +15,7 @@ sys.path.insert(0, %r)
 import numpy as np, bench, paper_2403_03772_b200 as plg
 X = np.asfortranarray(bench.make_input(%r))
 eng = plg.Engine(0)
+eng.set_detail_timing(True)
 o1 = eng.causal_order(X)
 o2 = eng.causal_order(X)
 s = eng.stats()
