@@ -495,6 +495,10 @@ int search_round_pruned(plg_ctx* c, int64_t n, int64_t ldw, int d, int u, const 
   a.k_begin = 0;
   a.k_end = -1;
   a.res = nullptr;
+  a.res_base = 0;
+  a.shard_world = 0;
+  a.shard_rank = 0;
+  a.shard_slot = 0;
   auto stage = [&](int kind, int m, double beta, int pass) -> int {
     a.stage_idx = std::min(stage_idx++, plg::kMaxPruneStages - 1);
     a.state_in = sa;
@@ -514,39 +518,56 @@ int search_round_pruned(plg_ctx* c, int64_t n, int64_t ldw, int d, int u, const 
       ++c->launches;
     } else {
       // Multi-rank: the list is identical on every rank (deterministic selection), so rank r
-      // evaluates the contiguous slice [r cnt, (r + 1) cnt) and one in-place all-gather of
-      // the M values gives every rank the whole stage; the scatter writes them into Md / KN.
-      int total = 0;
-      PLG_CUDA(cudaMemcpyAsync(&total, c->off.p + u, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-      PLG_CUDA(cudaStreamSynchronize(c->stream));
-      int32_t cnt = 0, kb = 0, ke = 0;
-      plg_plan_list_shard(total, 0, shards, &kb, &ke, &cnt);
-      a.res = c->pres.p;
+      // evaluates a contiguous slice and one in-place all-gather of the M values gives every
+      // rank the whole stage; the scatter writes them into Md / KN. Stages whose list length
+      // has a host-side bound (probe: (R + T) u; refinement: u m) plan the slices on the
+      // device and all-gather fixed slots of ceil(bound / ranks) entries, with no host
+      // synchronisation; the full stage reads the length first (plg_plan_list_shard).
       const bool real = c->world > 1 || c->force_nccl;  // else: emulated ranks, one after the other
+      int64_t bound = -1;
+      if (kind == plg::kStageProbe) bound = static_cast<int64_t>(c->prune_R + c->prune_T) * u;
+      else if (kind == plg::kStageRefine && m > 0) bound = static_cast<int64_t>(u) * m;
+      int32_t slot = 0, kb = 0, ke = 0, total = -1;
+      if (bound >= 0) {
+        slot = static_cast<int32_t>((bound + shards - 1) / shards);
+      } else {
+        PLG_CUDA(cudaMemcpyAsync(&total, c->off.p + u, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        PLG_CUDA(cudaStreamSynchronize(c->stream));
+        plg_plan_list_shard(total, 0, shards, &kb, &ke, &slot);
+      }
+      a.res = c->pres.p;
       for (int r = (real ? c->rank : 0); r < (real ? c->rank + 1 : shards); ++r) {
-        plg_plan_list_shard(total, r, shards, &kb, &ke, &cnt);
-        a.k_begin = kb;
-        a.k_end = ke;
+        if (bound >= 0) {
+          a.shard_world = shards;
+          a.shard_rank = r;
+          a.shard_slot = slot;
+          a.res_base = r * slot;
+        } else {
+          plg_plan_list_shard(total, r, shards, &kb, &ke, &slot);
+          a.k_begin = kb;
+          a.k_end = ke;
+          a.res_base = kb;  // = r * slot
+        }
         if (r > (real ? c->rank : 0))  // emulated ranks share one set of fetch counters
-          PLG_CUDA(cudaMemsetAsync(c->pwork.p, 0, (cnt / c->prune_batch + 2) * sizeof(int),
-                                   c->stream));
+          PLG_CUDA(cudaMemsetAsync(c->pwork.p, 0, (slot / c->prune_batch + 2) * sizeof(int), c->stream));
         const size_t tm = pair_timer_begin(c);
         plg::launch_prune_pairs(a, c->stream);
         pair_timer_end(c, tm);
         ++c->launches;
       }
-      if ((c->world > 1 || c->force_nccl) && cnt > 0) {
+      if (real && slot > 0) {
         NcclApi& api = nccl();
-        const ncclResult_t r = api.AllGather(c->pres.p + static_cast<size_t>(c->rank) * cnt, c->pres.p, cnt,
+        const ncclResult_t r = api.AllGather(c->pres.p + static_cast<size_t>(c->rank) * slot, c->pres.p, slot,
                                              ncclDouble, c->comm, c->stream);
         if (r != ncclSuccess)
           return set_status(st, PLG_NcclError, -1, -1, "ncclAllGather: %s", api.GetErrorString(r));
       }
-      plg::launch_prune_scatter(a, total, c->stream);
+      plg::launch_prune_scatter(a, shards, slot > 0 ? slot : 1, c->stream);
       ++c->launches;
       a.res = nullptr;
       a.k_begin = 0;
       a.k_end = -1;
+      a.shard_world = 0;
     }
     std::swap(sa, sb);
     a.state_in = sa;

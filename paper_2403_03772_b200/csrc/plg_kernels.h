@@ -175,7 +175,11 @@ struct PruneArgs {
   int stage_idx;
   int k_begin;                  // list entries this launch evaluates: [k_begin, k_end)
   int k_end;                    // (k_end < 0: the whole list from k_begin)
-  double* res;                  // multi-rank: M of every list entry by list index (all-gathered)
+  double* res;                  // multi-rank: M of the list entries, one slot per rank (all-gathered)
+  int res_base;                 // this launch's first entry goes to res[res_base] (host-planned slices)
+  int shard_world;              // > 0: slice of this rank planned on the device from the list length
+  int shard_rank;
+  int shard_slot;               // entries per rank slot in res
 };
 enum PruneStage : int { kStageProbe = 0, kStageRefine = 1, kStageFull = 2 };
 void launch_prune_predict(const PruneArgs& a, cudaStream_t s);
@@ -185,8 +189,9 @@ void launch_prune_top(const PruneArgs& a, int R, cudaStream_t s);
 void launch_prune_select(const PruneArgs& a, int stage, int m, double beta, cudaStream_t s);
 void launch_prune_scan(const PruneArgs& a, cudaStream_t s);
 void launch_prune_pairs(const PruneArgs& a, cudaStream_t s);
-// multi-rank: res[0..total) (all ranks' results, gathered) into Md / KN
-void launch_prune_scatter(const PruneArgs& a, int total, cudaStream_t s);
+// multi-rank: all ranks' results (res, `world` slots of `slot` entries; entry k of the list
+// sits at (k / cnt) slot + k % cnt with cnt = ceil(total / world)) into Md / KN
+void launch_prune_scatter(const PruneArgs& a, int world, int slot, cudaStream_t s);
 // pass 0: every row's partial k L[] and k* over the top rows; 1: alive rows' L[]; 2: exact k[]
 // of the top and alive rows (+inf for pruned rows)
 void launch_prune_bound(const PruneArgs& a, int pass, cudaStream_t s);

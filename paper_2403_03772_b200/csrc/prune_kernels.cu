@@ -798,7 +798,7 @@ __device__ __forceinline__ void store_pair(const PruneArgs& a, int p, int q, dou
 // Finalise one 32-pair chunk once all its sample segments are in: segments in ascending
 // order (finalize_kernel's order), both entropies, then M_pq and M_qp = -M_pq.
 __device__ __forceinline__ void finalize_chunk(const PruneArgs& a, const double* part, int base, int m, int chunk,
-                                               int lane) {
+                                               int lane, int kb) {
   const int kk = chunk * 32 + lane;
   if (kk >= m) return;
   int p, q;
@@ -822,7 +822,7 @@ __device__ __forceinline__ void finalize_chunk(const PruneArgs& a, const double*
   // ordering.cpp:93-94 (kreduce_kernel's expression); M_qp = -M_pq exactly
   const double mpq = (a.H[q] + e_pq) - (a.H[p] + e_qp);
   store_pair(a, p, q, mpq);
-  if (a.res) a.res[base + kk] = mpq;  // multi-rank: this rank's slot of the all-gathered results
+  if (a.res) a.res[a.res_base + (base + kk - kb)] = mpq;  // multi-rank: this rank's slot
 }
 
 // Work items (chunk of 32 list entries, sample segment) are fetched dynamically, chunk-major;
@@ -837,12 +837,20 @@ __global__ void __launch_bounds__(kListThreads, 2) prune_pairs_kernel(const Prun
   __syncthreads();
   cg::grid_group grid = cg::this_grid();
   const bool skip = (*a.err != kNoError);  // only skips work: every CTA still meets the barriers
-  // this launch's share of the list: [k_begin, k_end) (k_end < 0: to the end of the list)
-  const int total = (a.k_end >= 0 ? a.k_end : a.off[a.u]) - a.k_begin;
+  // this launch's share of the list: [kb, ke) — host-planned (k_end < 0: to the end of the
+  // list), or this rank's slice of ceil(total / shard_world) entries planned here
+  int kb = a.k_begin, ke = a.k_end >= 0 ? a.k_end : a.off[a.u];
+  if (a.shard_world > 0) {
+    const int tot = a.off[a.u];
+    const int cnt = (tot + a.shard_world - 1) / a.shard_world;
+    kb = min(tot, a.shard_rank * cnt);
+    ke = min(tot, (a.shard_rank + 1) * cnt);
+  }
+  const int total = ke - kb;
   const int nbatch = (total + a.batch - 1) / a.batch;
   for (int b = 0; b < nbatch; ++b) {
     if (b > 0) grid.sync();  // every chunk of batch b - 1 is finalised: the part slab is free
-    const int base = a.k_begin + b * a.batch;
+    const int base = kb + b * a.batch;
     const int m = min(a.batch, total - b * a.batch);
     const int chunks = (m + 31) / 32;
     const int items = chunks * a.nseg;
@@ -895,7 +903,7 @@ __global__ void __launch_bounds__(kListThreads, 2) prune_pairs_kernel(const Prun
       last = __shfl_sync(0xffffffffu, last, 0);
       if (last) {
         __threadfence();  // acquire the other segments' partials
-        finalize_chunk(a, a.part, base, m, chunk, lane);
+        finalize_chunk(a, a.part, base, m, chunk, lane, kb);
         if (lane == 0) a.done[chunk] = 0;  // ready for the next batch / launch
       }
     }
@@ -903,11 +911,13 @@ __global__ void __launch_bounds__(kListThreads, 2) prune_pairs_kernel(const Prun
 }
 
 // ---- scatter (multi-rank): every rank's results of the stage's list into Md / KN ----
-__global__ void prune_scatter_kernel(const PruneArgs a, int total) {
+__global__ void prune_scatter_kernel(const PruneArgs a, int world, int slot) {
+  const int total = a.off[a.u];
+  const int cnt = (total + world - 1) / world;
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < total; k += gridDim.x * blockDim.x) {
     int p, q;
     list_entry(a, k, p, q);
-    store_pair(a, p, q, a.res[k]);
+    store_pair(a, p, q, a.res[(k / cnt) * slot + (k % cnt)]);
   }
 }
 
@@ -1011,11 +1021,8 @@ void launch_prune_pairs(const PruneArgs& a, cudaStream_t s) {
   else launch_pairs_cfg<false, 0>(a, s);
 }
 
-void launch_prune_scatter(const PruneArgs& a, int total, cudaStream_t s) {
-  if (total <= 0) return;
-  int grid = (total + 255) / 256;
-  if (grid > 148 * 8) grid = 148 * 8;
-  prune_scatter_kernel<<<grid, 256, 0, s>>>(a, total);
+void launch_prune_scatter(const PruneArgs& a, int world, int slot, cudaStream_t s) {
+  prune_scatter_kernel<<<148 * 4, 256, 0, s>>>(a, world, slot);
 }
 
 void launch_prune_bound(const PruneArgs& a, int pass, cudaStream_t s) {
