@@ -172,35 +172,45 @@ def _shard(total, rank, world):
     return b.value, e.value, slot.value
 
 
-def _stage_worker(rank, world, port, total, u, out):
+def _stage_worker(rank, world, port, total, u, out, bound=None):
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     try:
         rng = np.random.default_rng(123)  # every rank builds the same list (deterministic selection)
         pairs = [(int(p), int(q)) for p, q in rng.integers(0, u, size=(total, 2)) if p != q][:total]
         total_eff = len(pairs)
-        b, e, slot = _shard(total_eff, rank, world)
+        if bound is None:  # host-planned slice (the full stage): plg_plan_list_shard
+            b, e, slot = _shard(total_eff, rank, world)
+            base = b
+        else:  # device-planned slice, fixed slot of ceil(bound / world) (probe / refinement)
+            cnt = (total_eff + world - 1) // world
+            b, e = min(total_eff, rank * cnt), min(total_eff, (rank + 1) * cnt)
+            slot = (bound + world - 1) // world
+            base = rank * slot
         res = torch.zeros(slot * world, dtype=torch.float64)
         for k in range(b, e):  # this rank's slice: "evaluate" entry k into its slot
             p, q = pairs[k]
-            res[k] = np.sin(1.0 + p * 0.37 + q * 0.011)  # any deterministic function of the pair
+            res[base + (k - b)] = np.sin(1.0 + p * 0.37 + q * 0.011)  # any deterministic function
         mine = res[rank * slot:(rank + 1) * slot].clone()
         gathered = [torch.zeros(slot, dtype=torch.float64) for _ in range(world)]
         dist.all_gather(gathered, mine)
-        full = torch.cat(gathered)[:total_eff].numpy()
+        full = torch.cat(gathered).numpy()
+        cnt = max(1, (total_eff + world - 1) // world)
         Md = np.full((u, u), np.nan)
-        for k, (p, q) in enumerate(pairs):  # prune_scatter_kernel: entry k -> M_pq, M_qp = -M_pq
-            Md[p, q], Md[q, p] = full[k], -full[k]
+        for k, (p, q) in enumerate(pairs):  # prune_scatter_kernel: entry k at (k / cnt) slot + k % cnt
+            v = full[(k // cnt) * slot + k % cnt]
+            Md[p, q], Md[q, p] = v, -v
         if rank == 0:
             np.save(out, Md)
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,total", [(2, 1000), (3, 1001), (3, 2), (2, 0)])
-def test_pruned_stage_shard_gather_scatter(tmp_path, world, total):
+@pytest.mark.parametrize("world,total,bound", [(2, 1000, None), (3, 1001, None), (3, 2, None), (2, 0, None),
+                                               (2, 700, 1200), (3, 1001, 1001), (3, 5, 64)])
+def test_pruned_stage_shard_gather_scatter(tmp_path, world, total, bound):
     u = 50
     out = str(tmp_path / "md.npy")
-    mp.spawn(_stage_worker, args=(world, _free_port(), total, u, out), nprocs=world, join=True)
+    mp.spawn(_stage_worker, args=(world, _free_port(), total, u, out, bound), nprocs=world, join=True)
     rng = np.random.default_rng(123)
     pairs = [(int(p), int(q)) for p, q in rng.integers(0, u, size=(total, 2)) if p != q][:total]
     ref = np.full((u, u), np.nan)
