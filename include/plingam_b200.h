@@ -66,6 +66,13 @@ typedef struct plg_stats {
   double resid_ms;      /* device time of the residualisation launches (fused with the next
                            round's column entropies) */
   int64_t resid_bytes;  /* their algorithmic HBM bytes: (2 (u - 1) + 1) n 8 per round */
+  /* Near-tie guard (causal_order): rounds whose runner-up k is not certified above
+   * winner k * (1 + 1e-9) — the reference's strict '>' argmax (ordering.cpp:154-160) could
+   * pick differently there under its own rounding — and the smallest relative gap
+   * (runner-up k - winner k) / winner k over all rounds, with its round. */
+  int32_t near_ties;
+  int32_t min_gap_round;
+  double min_gap;
 } plg_stats;
 
 typedef struct plg_ctx plg_ctx;
@@ -104,6 +111,10 @@ int plg_set_prune(plg_ctx* ctx, int32_t enable, plg_status* st);
 /* The winning k (= -score of the chosen variable) of every round of the last causal_order on
  * ctx, in round order (count = min(cap, rounds)). Diagnostics and parity tests. */
 int plg_last_round_k(plg_ctx* ctx, double* out, int32_t cap, int32_t* count, plg_status* st);
+/* Per round of the last causal_order: a lower bound of the runner-up's k (exact when the
+ * runner-up row was fully evaluated — every row within k* (1 + 1e-9) is — else that row's
+ * partial k), so second - k (plg_last_round_k) bounds the best-vs-second gap from below. */
+int plg_last_round_gaps(plg_ctx* ctx, double* second_out, int32_t cap, int32_t* count, plg_status* st);
 /* plingam::search_causal_order(X, U) — ordering.hpp:27, ordering.cpp:101-168.
  * scores_out: d doubles, -inf for non-candidates, -k for candidates. */
 int plg_search(plg_ctx* ctx, const double* X, int64_t n, int32_t d, int64_t ld, const int32_t* U,
@@ -115,10 +126,13 @@ int plg_regress_out(plg_ctx* ctx, const double* X, int64_t n, int32_t d, int64_t
                     const int32_t* remaining, int32_t r, double* out, plg_status* st);
 
 /* Adjacency weights of DirectLingam::fit (direct_lingam.cpp:46-70) given an order:
- * B (d x d, column-major, B[target + d * pred]) from the centred covariance, every
- * predecessor regression at once through one Cholesky of the order-permuted
- * covariance. used_pinv is set (and a pseudo-inverse solution used) when a predecessor
- * design is rank deficient. */
+ * B (d x d, column-major, B[target + d * pred]). Every predecessor regression at once from
+ * one FP64 Householder QR of the order-permuted centred design, in echelon form: a column
+ * whose residual norm is at or below ColPivHouseholderQR's rank threshold
+ * (eps * min(n, p) * largest column norm, direct_lingam.cpp:57-59) gets no reflector, and
+ * the targets after it take the minimum-norm least-squares solution, as
+ * CompleteOrthogonalDecomposition (direct_lingam.cpp:60-63); used_pinv is then set.
+ * Entirely on the device. */
 int plg_fit_weights(plg_ctx* ctx, const double* X, int64_t n, int32_t d, int64_t ld,
                     const int32_t* order, double* B_out, int32_t* used_pinv, plg_status* st);
 

@@ -706,7 +706,8 @@ static int cmp_key_desc(const void* a, const void* b) {
 }
 
 int orc_causal_order_pruned(const double* X, int64_t n, int32_t d, int64_t ld, int32_t workers,
-                            int32_t* order_out, double* winner_k, int64_t* pairs_evaluated, orc_status* st) {
+                            int32_t* order_out, double* winner_k, double* second_k, int64_t* pairs_evaluated,
+                            orc_status* st) {
   int rc = orc_validate(X, n, d, ld, st);
   if (rc) return rc;
   if (workers < 1) workers = 1;
@@ -827,6 +828,15 @@ int orc_causal_order_pruned(const double* X, int64_t n, int32_t d, int64_t ld, i
         }
       }
     if (winner_k) winner_k[round] = kex[best];
+    if (second_k) { /* runner-up: exact k of evaluated rows, the partial k (a lower bound) of pruned ones */
+      double s2 = INFINITY;
+      for (int32_t p = 0; p < nu; ++p) {
+        if (p == best) continue;
+        const double kp = state[p] >= 1 ? kex[p] : partial_k(mi_full, nu, p);
+        if (kp < s2) s2 = kp;
+      }
+      second_k[round] = s2;
+    }
     const int32_t chosen = u[best];
     int32_t nr = 0;
     for (int32_t p = 0; p < nu; ++p)
@@ -1014,8 +1024,9 @@ static void cod_solve(const double* Aqr, int64_t m, int32_t p, int32_t r, const 
 
 /* direct_lingam.cpp:46-70 — centred (not standardised) data; per target p, regress
  * X[:, order[p]] on X[:, order[0..p-1]]. */
-int orc_fit_weights(const double* X, int64_t n, int32_t d, int64_t ld, const int32_t* order,
-                    double* B, int32_t* used_pinv, orc_status* st) {
+/* Targets at the listed order positions only (positions == NULL: every p >= 1). */
+static int fit_weights_impl(const double* X, int64_t n, int32_t d, int64_t ld, const int32_t* order,
+                            const int32_t* positions, int32_t npos, double* B, int32_t* used_pinv, orc_status* st) {
   double* centered = (double*)malloc(sizeof(double) * (size_t)n * (size_t)d);
   for (int32_t j = 0; j < d; ++j) {
     const double* c = X + (int64_t)j * ld;
@@ -1029,7 +1040,10 @@ int orc_fit_weights(const double* X, int64_t n, int32_t d, int64_t ld, const int
   double* hcoef = (double*)malloc(sizeof(double) * (size_t)d);
   int32_t* perm = (int32_t*)malloc(sizeof(int32_t) * (size_t)d);
   double* coef = (double*)malloc(sizeof(double) * (size_t)d);
-  for (int32_t p = 1; p < d; ++p) {
+  const int32_t count = positions ? npos : (d > 1 ? d - 1 : 0);
+  for (int32_t e = 0; e < count; ++e) {
+    const int32_t p = positions ? positions[e] : e + 1;
+    if (p < 1 || p >= d) continue;
     const int32_t target = order[p];
     for (int32_t q = 0; q < p; ++q)
       memcpy(A + n * q, centered + n * order[q], sizeof(double) * (size_t)n);
@@ -1058,5 +1072,276 @@ int orc_fit_weights(const double* X, int64_t n, int32_t d, int64_t ld, const int
   free(hcoef);
   free(perm);
   free(coef);
+  return ok(st);
+}
+
+/* direct_lingam.cpp:46-70 — centred (not standardised) data; per target p, regress
+ * X[:, order[p]] on X[:, order[0..p-1]]. */
+int orc_fit_weights(const double* X, int64_t n, int32_t d, int64_t ld, const int32_t* order,
+                    double* B, int32_t* used_pinv, orc_status* st) {
+  return fit_weights_impl(X, n, d, ld, order, NULL, 0, B, used_pinv, st);
+}
+
+int orc_fit_weights_targets(const double* X, int64_t n, int32_t d, int64_t ld, const int32_t* order,
+                            const int32_t* positions, int32_t npos, double* B, int32_t* used_pinv, orc_status* st) {
+  return fit_weights_impl(X, n, d, ld, order, positions, npos, B, used_pinv, st);
+}
+
+/* ------------------------------------------------- weights: one prefix QR for all targets
+ *
+ * The same least-squares problems as orc_fit_weights (direct_lingam.cpp:46-70), from ONE
+ * Householder QR of the order-permuted centred design A = [x_o0 - m, ..., x_o(d-1) - m]:
+ * the predecessor design of target p is A's first p columns, so the QR of A restricted
+ * to them gives target p's regression (coordinates of column p in the first rows, solved
+ * against the leading triangle). Rank deficiency is handled in echelon form: a column
+ * whose residual norm (after the reflectors of the columns before it) is at or below the
+ * ColPivHouseholderQR threshold of the first design it enters, eps * min(n, k + 1) *
+ * max_{j <= k} ||a_j|| (Eigen's rank(): |R_ii| > |max pivot| * eps * diagonalSize, the max
+ * pivot being the largest column norm), gets no reflector: it is "dependent", A_S = Q_r T
+ * with T r x p echelon. For target p with independent predecessors I and dependent ones D:
+ *   a  = T_I^-1 c   (c: column p's first r coordinates)      -- every LS solution has
+ *   b_I = a - G b_D (G: columns g_k = T_I^-1 T[:, k], k in D)  -- this form, and the
+ *   b_D = (I + G^T G)^-1 G^T a                                 -- minimum-norm one
+ * which is what CompleteOrthogonalDecomposition::solve returns (direct_lingam.cpp:62).
+ * Full-rank targets reduce to the plain QR solution (direct_lingam.cpp:64). */
+
+typedef struct {
+  double* A;        /* n x d, column-major (lda = n), factorised in place */
+  int64_t n;
+  int32_t d;
+  int32_t nthreads;
+  int32_t tid;
+  pthread_barrier_t* bar;
+  /* shared per-step state */
+  volatile int32_t* step_row; /* row of the current reflector, -1 when the column is dependent */
+  volatile double* step_tau;
+} pqr_job;
+
+static void* pqr_worker(void* arg) {
+  pqr_job* J = (pqr_job*)arg;
+  const int64_t n = J->n;
+  for (int32_t k = 0; k < J->d; ++k) {
+    pthread_barrier_wait(J->bar); /* thread 0 has built reflector k (or marked it dependent) */
+    const int32_t r = J->step_row[k];
+    if (r >= 0) {
+      const double tau = J->step_tau[k];
+      const double* v = J->A + n * k;
+      for (int32_t j = k + 1 + J->tid; j < J->d; j += J->nthreads) {
+        double* cj = J->A + n * j;
+        double s = cj[r];
+        for (int64_t i = r + 1; i < n; ++i) s += v[i] * cj[i];
+        s *= tau;
+        cj[r] -= s;
+        for (int64_t i = r + 1; i < n; ++i) cj[i] -= s * v[i];
+      }
+    }
+    pthread_barrier_wait(J->bar); /* column k + 1 is up to date */
+  }
+  return NULL;
+}
+
+/* Cholesky solve of the small SPD system N x = y (N m x m row-major, overwritten). */
+static void spd_solve(double* N, int32_t m, double* y) {
+  for (int32_t j = 0; j < m; ++j) {
+    double s = N[(int64_t)j * m + j];
+    for (int32_t k = 0; k < j; ++k) s -= N[(int64_t)j * m + k] * N[(int64_t)j * m + k];
+    const double l = sqrt(s);
+    N[(int64_t)j * m + j] = l;
+    for (int32_t i = j + 1; i < m; ++i) {
+      double t = N[(int64_t)i * m + j];
+      for (int32_t k = 0; k < j; ++k) t -= N[(int64_t)i * m + k] * N[(int64_t)j * m + k];
+      N[(int64_t)i * m + j] = t / l;
+    }
+  }
+  for (int32_t i = 0; i < m; ++i) {
+    double t = y[i];
+    for (int32_t k = 0; k < i; ++k) t -= N[(int64_t)i * m + k] * y[k];
+    y[i] = t / N[(int64_t)i * m + i];
+  }
+  for (int32_t i = m - 1; i >= 0; --i) {
+    double t = y[i];
+    for (int32_t k = i + 1; k < m; ++k) t -= N[(int64_t)k * m + i] * y[k];
+    y[i] = t / N[(int64_t)i * m + i];
+  }
+}
+
+typedef struct {
+  const double* A;
+  int64_t n;
+  int32_t d;
+  const int32_t* rbefore; /* rows (reflectors) before column k */
+  const int32_t* rowcol;  /* column of reflector t */
+  const int32_t* dep;     /* dependent columns, ascending */
+  int32_t ndep;
+  double* coef;           /* d x d: row k = a_k (length rbefore[k]) */
+  int32_t tid, nthreads;
+} pqr_solve_job;
+
+/* a_k = T_I^-1 c_k for every column k (targets, and g_k for dependent columns). */
+static void* pqr_solve_worker(void* arg) {
+  pqr_solve_job* J = (pqr_solve_job*)arg;
+  const int64_t n = J->n;
+  for (int32_t k = J->tid; k < J->d; k += J->nthreads) {
+    const int32_t r = J->rbefore[k];
+    double* a = J->coef + (int64_t)k * J->d;
+    for (int32_t i = 0; i < r; ++i) a[i] = J->A[i + n * k];
+    for (int32_t t = r - 1; t >= 0; --t) {
+      const double* col = J->A + n * J->rowcol[t];
+      a[t] /= col[t];
+      for (int32_t i = 0; i < t; ++i) a[i] -= a[t] * col[i];
+    }
+  }
+  return NULL;
+}
+
+int orc_fit_weights_prefix(const double* X, int64_t n, int32_t d, int64_t ld, const int32_t* order,
+                           int32_t nthreads, double* B, int32_t* used_pinv, int32_t* n_dependent,
+                           orc_status* st) {
+  if (nthreads < 1) nthreads = 1;
+  memset(B, 0, sizeof(double) * (size_t)d * (size_t)d);
+  *used_pinv = 0;
+  if (n_dependent) *n_dependent = 0;
+  if (d < 2) return ok(st);
+  double* A = (double*)malloc(sizeof(double) * (size_t)n * (size_t)d);
+  double* cn = (double*)malloc(sizeof(double) * (size_t)d);
+  for (int32_t k = 0; k < d; ++k) {
+    const double* c = X + (int64_t)order[k] * ld;
+    const double m = orc_mean(c, n); /* Eigen colwise().mean() (direct_lingam.cpp:49) */
+    double s = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+      A[i + n * k] = c[i] - m;
+      s += A[i + n * k] * A[i + n * k];
+    }
+    cn[k] = sqrt(s);
+  }
+  int32_t* step_row = (int32_t*)malloc(sizeof(int32_t) * (size_t)d);
+  double* step_tau = (double*)malloc(sizeof(double) * (size_t)d);
+  int32_t* rbefore = (int32_t*)malloc(sizeof(int32_t) * (size_t)d);
+  int32_t* rowcol = (int32_t*)malloc(sizeof(int32_t) * (size_t)d);
+  int32_t* dep = (int32_t*)malloc(sizeof(int32_t) * (size_t)d);
+  int32_t ndep = 0;
+
+  pthread_barrier_t bar;
+  pthread_barrier_init(&bar, NULL, (unsigned)nthreads);
+  pqr_job* jobs = (pqr_job*)calloc((size_t)nthreads, sizeof(pqr_job));
+  pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)nthreads);
+  for (int32_t t = 0; t < nthreads; ++t) {
+    jobs[t] = (pqr_job){A, n, d, nthreads, t, &bar, step_row, step_tau};
+    if (t) pthread_create(&th[t], NULL, pqr_worker, &jobs[t]);
+  }
+  /* thread 0 = this thread: builds reflector k, then shares the update of columns > k */
+  int32_t r = 0;
+  double maxnorm = 0.0;
+  for (int32_t k = 0; k < d; ++k) {
+    if (cn[k] > maxnorm) maxnorm = cn[k];
+    const double thr = 2.220446049250313e-16 * (double)((int64_t)(k + 1) < n ? (k + 1) : n) * maxnorm;
+    double* col = A + n * k;
+    rbefore[k] = r;
+    double tail = 0.0;
+    for (int64_t i = r + 1; i < n; ++i) tail += col[i] * col[i];
+    const double c0 = r < n ? col[r] : 0.0;
+    const double nu = sqrt(c0 * c0 + tail);
+    if (r < n && nu > thr) {
+      double beta = c0 >= 0.0 ? -nu : nu, tau;
+      if (tail == 0.0) {
+        tau = 0.0;
+        beta = c0;
+      } else {
+        const double denom = c0 - beta;
+        for (int64_t i = r + 1; i < n; ++i) col[i] /= denom;
+        tau = (beta - c0) / beta;
+      }
+      col[r] = beta;
+      step_row[k] = r;
+      step_tau[k] = tau;
+      rowcol[r] = k;
+      ++r;
+    } else {
+      step_row[k] = -1;
+      dep[ndep++] = k;
+    }
+    pthread_barrier_wait(&bar);
+    {
+      const int32_t rr = step_row[k];
+      if (rr >= 0) {
+        const double tau = step_tau[k];
+        for (int32_t j = k + 1; j < d; j += nthreads) {
+          double* cj = A + n * j;
+          double s = cj[rr];
+          for (int64_t i = rr + 1; i < n; ++i) s += col[i] * cj[i];
+          s *= tau;
+          cj[rr] -= s;
+          for (int64_t i = rr + 1; i < n; ++i) cj[i] -= s * col[i];
+        }
+      }
+    }
+    pthread_barrier_wait(&bar);
+  }
+  for (int32_t t = 1; t < nthreads; ++t) pthread_join(th[t], NULL);
+  pthread_barrier_destroy(&bar);
+
+  /* every column's coordinates solved against the leading triangle */
+  double* coef = (double*)calloc((size_t)d * (size_t)d, sizeof(double));
+  pqr_solve_job* sj = (pqr_solve_job*)calloc((size_t)nthreads, sizeof(pqr_solve_job));
+  for (int32_t t = 0; t < nthreads; ++t) {
+    sj[t] = (pqr_solve_job){A, n, d, rbefore, rowcol, dep, ndep, coef, t, nthreads};
+    if (t) pthread_create(&th[t], NULL, pqr_solve_worker, &sj[t]);
+  }
+  pqr_solve_worker(&sj[0]);
+  for (int32_t t = 1; t < nthreads; ++t) pthread_join(th[t], NULL);
+
+  double* bD = (double*)malloc(sizeof(double) * (size_t)(ndep > 0 ? ndep : 1));
+  double* N = (double*)malloc(sizeof(double) * (size_t)(ndep > 0 ? ndep : 1) * (size_t)(ndep > 0 ? ndep : 1));
+  double* bI = (double*)malloc(sizeof(double) * (size_t)d);
+  for (int32_t p = 1; p < d; ++p) {
+    const int32_t target = order[p];
+    const int32_t rp = rbefore[p];
+    const double* a = coef + (int64_t)p * d;
+    int32_t m = 0;
+    while (m < ndep && dep[m] < p) ++m; /* dependent predecessors dep[0..m) */
+    for (int32_t t = 0; t < rp; ++t) bI[t] = a[t];
+    if (m > 0) {
+      *used_pinv = 1;
+      /* N = I + G^T G, y = G^T a (g_k zero beyond rbefore[k]) */
+      for (int32_t i = 0; i < m; ++i) {
+        const double* gi = coef + (int64_t)dep[i] * d;
+        const int32_t ri = rbefore[dep[i]];
+        double s = 0.0;
+        for (int32_t t = 0; t < ri; ++t) s += gi[t] * a[t];
+        bD[i] = s;
+        for (int32_t j = 0; j <= i; ++j) {
+          const double* gj = coef + (int64_t)dep[j] * d;
+          const int32_t rj = rbefore[dep[j]];
+          const int32_t rm = ri < rj ? ri : rj;
+          double g = 0.0;
+          for (int32_t t = 0; t < rm; ++t) g += gi[t] * gj[t];
+          N[(int64_t)i * m + j] = N[(int64_t)j * m + i] = g + (i == j ? 1.0 : 0.0);
+        }
+      }
+      spd_solve(N, m, bD);
+      for (int32_t i = 0; i < m; ++i) {
+        const double* gi = coef + (int64_t)dep[i] * d;
+        const int32_t ri = rbefore[dep[i]];
+        for (int32_t t = 0; t < ri; ++t) bI[t] -= gi[t] * bD[i];
+        B[target + (int64_t)d * order[dep[i]]] = bD[i];
+      }
+    }
+    for (int32_t t = 0; t < rp; ++t) B[target + (int64_t)d * order[rowcol[t]]] = bI[t];
+  }
+  if (n_dependent) *n_dependent = ndep;
+  free(bD);
+  free(N);
+  free(bI);
+  free(coef);
+  free(sj);
+  free(jobs);
+  free(th);
+  free(A);
+  free(cn);
+  free(step_row);
+  free(step_tau);
+  free(rbefore);
+  free(rowcol);
+  free(dep);
   return ok(st);
 }

@@ -93,10 +93,14 @@ int orc_causal_order(const double* X, int64_t n, int32_t d, int64_t ld, int32_t 
 
 /* Full order by exact pruned rounds (the product's branch and bound on k, restated): same
  * order and winning k as orc_causal_order (tested), a few % of the pair evaluations.
- * winner_k (optional): d - 1 doubles, the k of each round's chosen variable. Golden
+ * winner_k (optional): d - 1 doubles, the k of each round's chosen variable; second_k
+ * (optional): d - 1 doubles, a lower bound of the runner-up's k (exact when the runner-up
+ * row was fully evaluated, its partial k otherwise), so second_k - winner_k bounds the
+ * round's best-vs-second gap from below (near-tie guard, SURVEY §7 hard part 1). Golden
  * generation on valid data; error paths are not reproduced. */
 int orc_causal_order_pruned(const double* X, int64_t n, int32_t d, int64_t ld, int32_t workers,
-                            int32_t* order_out, double* winner_k, int64_t* pairs_evaluated, orc_status* st);
+                            int32_t* order_out, double* winner_k, double* second_k, int64_t* pairs_evaluated,
+                            orc_status* st);
 
 /* ---- adjacency weights (proj/src/direct_lingam.cpp:46-70) ----
  * Per-target least squares on centred data via column-pivoted Householder QR
@@ -105,6 +109,21 @@ int orc_causal_order_pruned(const double* X, int64_t n, int32_t d, int64_t ld, i
  * minimum-norm solution is then returned (Eigen::CompleteOrthogonalDecomposition). */
 int orc_fit_weights(const double* X, int64_t n, int32_t d, int64_t ld, const int32_t* order,
                     double* B, int32_t* used_pinv, orc_status* st);
+
+/* orc_fit_weights restricted to the targets at the listed order positions (rows of the
+ * other targets stay zero): per-target spot checks at sizes where the full per-target
+ * route would take hours. */
+int orc_fit_weights_targets(const double* X, int64_t n, int32_t d, int64_t ld, const int32_t* order,
+                            const int32_t* positions, int32_t npos, double* B, int32_t* used_pinv, orc_status* st);
+
+/* The same weights from ONE Householder QR of the order-permuted centred design (every
+ * predecessor regression is a prefix of it), rank-deficient columns in echelon form with
+ * the minimum-norm correction (see the .c). O(n d^2) instead of the per-target O(n d^3):
+ * the large-d reference, cross-checked against orc_fit_weights at small d.
+ * n_dependent (optional): number of columns without a reflector. */
+int orc_fit_weights_prefix(const double* X, int64_t n, int32_t d, int64_t ld, const int32_t* order,
+                           int32_t nthreads, double* B, int32_t* used_pinv, int32_t* n_dependent,
+                           orc_status* st);
 
 #ifdef __cplusplus
 }

@@ -21,6 +21,7 @@
 #include <cstring>
 #include <initializer_list>
 #include <limits>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -33,11 +34,15 @@ namespace {
 using plg::kBT;
 using plg::kTilePairs;
 
-constexpr double kZeroVarTol = 1e-12;  // partial variance relative to the standardised 1.0
+
 // Pair-kernel CTAs per round over all ranks: ~16 waves even when 8 ranks split the tiles,
 // so the last partial wave costs little; the segmentation is chosen from this constant and
 // (u, n) only, never from the rank count.
 constexpr int kTargetCtas = 16 * 148 * 8;
+// Near-tie guard: rounds whose runner-up k is within this relative margin of the winner's.
+// Our k and the reference's differ by ~1e-11 relative (FP64 element math, Gram route), and
+// pruned rows are certified above k* (1 + 1e-9), so 1e-9 is the certified bound.
+constexpr double kTieRel = 1e-9;
 
 int set_status(plg_status* st, int32_t code, int64_t row, int64_t col, const char* fmt, ...) {
   if (st) {
@@ -159,6 +164,7 @@ constexpr int kPruneBatchDefault = 131072;  // pairs per batch of the list kerne
 }  // namespace
 
 struct plg_ctx {
+  std::mutex mu;  // one call at a time per context (the C-ABI contract, enforced)
   int device = 0;
   int rank = 0;
   int world = 1;
@@ -175,7 +181,7 @@ struct plg_ctx {
   double* g_exp = nullptr;
   double2* g_log = nullptr;
 
-  DevBuf<double> Xd, W, C, part, epack, H, k, scores, msd, gscr, rk, hpart;
+  DevBuf<double> Xd, W, C, part, epack, H, k, scores, msd, gscr, rk, rsec, hpart;
   DevBuf<int> act0, act1, colvar, order, stat, idx, nz;
   DevBuf<plg::RoundState> rs;
   DevBuf<unsigned long long> err, errs;
@@ -200,9 +206,12 @@ struct plg_ctx {
   DevBuf<double> Md, KN, pk, L, ppart, pres;
   DevBuf<int> st0, st1, rowsel, off, pwork, pdone, crow, cand, alive;
   DevBuf<unsigned long long> kstar, evals;
+  DevBuf<double> qd;  // QR weight step / VAR: thresholds, norms, tau, T, trailing scratch, coefficients
+  DevBuf<int> qi;     // QR: qstate, rbefore, rowcol, dep, pinfo, dependent lists
 
   size_t ev_pairs = 0;  // timing intervals recorded by this call (ev[3 + 2 i], ev[4 + 2 i])
   std::vector<char> ev_kind;  // per interval: 0 pair evaluation, 1 residualisation
+  std::vector<double> last_k, last_second;  // per round of the last causal_order: winner's k, runner-up's
   int64_t resid_bytes = 0;    // algorithmic HBM bytes of the residualisations of this call
 
   cudaError_t events(size_t count) {
@@ -513,7 +522,7 @@ int search_round_pruned(plg_ctx* c, int64_t n, int64_t ldw, int d, int u, const 
     }
     if (shards == 1 && !c->force_nccl) {
       const size_t tm = pair_timer_begin(c);
-      plg::launch_prune_pairs(a, c->stream);
+      PLG_CUDA(plg::launch_prune_pairs(a, c->stream));
       pair_timer_end(c, tm);
       ++c->launches;
     } else {
@@ -551,7 +560,7 @@ int search_round_pruned(plg_ctx* c, int64_t n, int64_t ldw, int d, int u, const 
         if (r > (real ? c->rank : 0))  // emulated ranks share one set of fetch counters
           PLG_CUDA(cudaMemsetAsync(c->pwork.p, 0, (slot / c->prune_batch + 2) * sizeof(int), c->stream));
         const size_t tm = pair_timer_begin(c);
-        plg::launch_prune_pairs(a, c->stream);
+        PLG_CUDA(plg::launch_prune_pairs(a, c->stream));
         pair_timer_end(c, tm);
         ++c->launches;
       }
@@ -610,6 +619,7 @@ int reserve_run(plg_ctx* c, int64_t n, int ncols, int64_t ldw, plg_status* st) {
   PLG_CUDA(c->H.reserve(ncols));
   PLG_CUDA(c->k.reserve(ncols));
   PLG_CUDA(c->rk.reserve(ncols));
+  PLG_CUDA(c->rsec.reserve(ncols));
   PLG_CUDA(c->hpart.reserve(static_cast<size_t>(ncols) * plg::resid_chunks(n) * 2));
   PLG_CUDA(c->scores.reserve(ncols));
   PLG_CUDA(c->act0.reserve(ncols));
@@ -632,6 +642,9 @@ int reserve_prune(plg_ctx* c, int64_t n, int d, plg_status* st) {
     for (int u = d; u > c->prune_min_u; --u) nseg = std::max(nseg, static_cast<size_t>(seg_plan(u, n).nseg));
   PLG_CUDA(c->Md.reserve(dd));
   PLG_CUDA(c->KN.reserve(dd));
+  // every KN entry is defined (round 0 fills the off-diagonal ones): the prediction pass reads
+  // whole rows and discards the diagonal
+  PLG_CUDA(cudaMemsetAsync(c->KN.p, 0, dd * sizeof(double), c->stream));
   PLG_CUDA(c->rowsel.reserve(dd));
   PLG_CUDA(c->off.reserve(static_cast<size_t>(d) + 1));
   PLG_CUDA(c->pk.reserve(d));
@@ -778,6 +791,7 @@ int causal_order_impl(plg_ctx* c, const double* dX, int64_t ldx, int64_t n, int 
   for (int r = 0; r < rounds; ++r) {
     if (!rev.empty()) cudaEventRecord(rev[r], c->stream);
     const int u = d - r;
+    bool pruned_round = prune && r == 0 && c->prune_sub > 0 && n >= 2 * c->prune_sub;
     int* act_cur = (r & 1) ? c->act1.p : c->act0.p;
     int* act_nxt = (r & 1) ? c->act0.p : c->act1.p;
     if (prune && r == 0 && c->prune_sub > 0 && n >= 2 * c->prune_sub) {
@@ -790,6 +804,7 @@ int causal_order_impl(plg_ctx* c, const double* dX, int64_t ldx, int64_t n, int 
       if (int rc = search_round_pruned(c, n, ldw, d, u, act_cur, r, st, false)) return rc;
     } else if (prune && r > 0 && u > c->prune_min_u) {
       if (int rc = search_round_pruned(c, n, ldw, d, u, act_cur, r, st)) return rc;
+      pruned_round = true;
     } else if (int rc = search_round(c, n, ldw, d, u, act_cur, r, st, (prune && r == 0) ? c->KN.p : nullptr,
                                      r > 0)) {
       return rc;
@@ -797,7 +812,7 @@ int causal_order_impl(plg_ctx* c, const double* dX, int64_t ldx, int64_t n, int 
     if (c->hook && c->world == 1)
       if (int rc = call_round_hook(c, u, r, act_cur, st)) return rc;
     plg::launch_commit(c->k.p, act_cur, act_nxt, u, c->colvar.p, c->order.p, r, nullptr, c->rs.p,
-                       c->err.p, c->stream, c->rk.p);
+                       c->err.p, c->stream, c->rk.p, pruned_round ? c->L.p : nullptr, c->rsec.p);
     ++c->launches;
     if (u - 1 >= 2 || (u - 1 == 1 && max_rounds >= 0)) {
       // the next round's build_cache check only exists when it has >= 2 candidates
@@ -824,6 +839,11 @@ int causal_order_impl(plg_ctx* c, const double* dX, int64_t ldx, int64_t n, int 
   const int nout = (rounds == d - 1) ? d : rounds;
   PLG_CUDA(cudaMemcpyAsync(order_out, c->order.p, nout * sizeof(int32_t), cudaMemcpyDeviceToHost,
                            c->stream));
+  c->last_k.resize(rounds);
+  c->last_second.resize(rounds);
+  PLG_CUDA(cudaMemcpyAsync(c->last_k.data(), c->rk.p, rounds * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  PLG_CUDA(cudaMemcpyAsync(c->last_second.data(), c->rsec.p, rounds * sizeof(double), cudaMemcpyDeviceToHost,
+                           c->stream));
   PLG_CUDA(cudaStreamSynchronize(c->stream));
   PLG_CUDA(cudaGetLastError());
   finish_stats(c, n, d, rounds, host_in);
@@ -848,6 +868,20 @@ int causal_order_impl(plg_ctx* c, const double* dX, int64_t ldx, int64_t n, int 
                  static_cast<long long>(c->last.pairs_evaluated));
   }
   c->last.d2h_bytes = nout * sizeof(int32_t);
+  // near-tie guard (SURVEY §7 hard part 1): a round whose runner-up is within kTieRel of the
+  // winner could order differently under the reference's own rounding (its k differ from
+  // ours by ~1e-11 relative), so it is counted and reported
+  c->last.near_ties = 0;
+  c->last.min_gap = INFINITY;
+  for (int r = 0; r < rounds; ++r) {
+    const double k1 = c->last_k[r], k2 = c->last_second[r];
+    if (!(k2 > k1 * (1.0 + kTieRel))) ++c->last.near_ties;
+    const double g = k1 > 0.0 ? (k2 - k1) / k1 : (k2 > 0.0 ? INFINITY : 0.0);
+    if (g < c->last.min_gap) {
+      c->last.min_gap = g;
+      c->last.min_gap_round = r;
+    }
+  }
   if (key != plg::kNoError) return report_error(key, nullptr, st);
   return ok(st);
 }
@@ -858,6 +892,8 @@ int begin_call(plg_ctx* c, plg_status* st) {
   c->ev_pairs = 0;
   c->resid_bytes = 0;
   c->last = plg_stats{};
+  c->last_k.clear();
+  c->last_second.clear();
   if (c->timing) {
     PLG_CUDA(c->events(3));
     PLG_CUDA(cudaEventRecord(c->ev[0], c->stream));
@@ -944,6 +980,9 @@ int plg_ctx_create_dist(int32_t device, int32_t rank, int32_t world, const void*
 }
 
 void plg_ctx_destroy(plg_ctx* c) {
+  if (c) {  // wait for an in-flight call on this context
+    std::lock_guard<std::mutex> lock_(c->mu);
+  }
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
@@ -981,6 +1020,7 @@ void plg_ctx_destroy(plg_ctx* c) {
 int plg_causal_order(plg_ctx* c, const double* X, int64_t n, int32_t d, int64_t ld,
                      int32_t* order_out, plg_status* st) {
   if (!c) return set_status(st, PLG_OutOfRange, -1, -1, "null context");
+  std::lock_guard<std::mutex> lock_(c->mu);
   if (int rc = check_shape(n, d, ld, st)) return rc;
   if (int rc = begin_call(c, st)) return rc;
   if (int rc = upload_x(c, X, n, d, ld, st)) return rc;
@@ -990,6 +1030,7 @@ int plg_causal_order(plg_ctx* c, const double* X, int64_t n, int32_t d, int64_t 
 int plg_causal_order_device(plg_ctx* c, const double* dX, int64_t n, int32_t d, int64_t ld,
                             int32_t* order_out, plg_status* st) {
   if (!c) return set_status(st, PLG_OutOfRange, -1, -1, "null context");
+  std::lock_guard<std::mutex> lock_(c->mu);
   if (int rc = check_shape(n, d, ld, st)) return rc;
   if (int rc = begin_call(c, st)) return rc;
   return causal_order_impl(c, dX, ld, n, d, -1, order_out, false, st);
@@ -998,6 +1039,7 @@ int plg_causal_order_device(plg_ctx* c, const double* dX, int64_t n, int32_t d, 
 int plg_search(plg_ctx* c, const double* X, int64_t n, int32_t d, int64_t ld, const int32_t* U,
                int32_t u, int32_t* chosen_out, double* scores_out, plg_status* st) {
   if (!c) return set_status(st, PLG_OutOfRange, -1, -1, "null context");
+  std::lock_guard<std::mutex> lock_(c->mu);
   // sorted_candidates (ordering.cpp:16-33)
   if (u <= 0) return set_status(st, PLG_EmptyCandidates, -1, -1, "search_causal_order: empty candidate set");
   std::vector<int> us(U, U + u);
@@ -1050,6 +1092,7 @@ int plg_search(plg_ctx* c, const double* X, int64_t n, int32_t d, int64_t ld, co
 int plg_regress_out(plg_ctx* c, const double* X, int64_t n, int32_t d, int64_t ld, int32_t exog,
                     const int32_t* remaining, int32_t r, double* out, plg_status* st) {
   if (!c) return set_status(st, PLG_OutOfRange, -1, -1, "null context");
+  std::lock_guard<std::mutex> lock_(c->mu);
   if (exog < 0 || exog >= d)
     return set_status(st, PLG_InvalidIndex, -1, exog, "regress_out: exog index out of range");
   if (int rc = begin_call(c, st)) return rc;
@@ -1137,6 +1180,7 @@ int device_eon(plg_ctx* c, const double* d_r, int64_t n, double* out, plg_status
 
 int plg_standardize(plg_ctx* c, const double* x, int64_t n, double* out, plg_status* st) {
   if (!c) return set_status(st, PLG_OutOfRange, -1, -1, "null context");
+  std::lock_guard<std::mutex> lock_(c->mu);
   if (n < 2) return set_status(st, PLG_TooShort, -1, -1, "standardize: need at least 2 samples");
   if (int rc = begin_call(c, st)) return rc;
   if (int rc = upload_vectors(c, {x}, n, st)) return rc;
@@ -1151,6 +1195,7 @@ int plg_standardize(plg_ctx* c, const double* x, int64_t n, double* out, plg_sta
 int plg_residual(plg_ctx* c, const double* xi, int64_t ni, const double* xj, int64_t nj, double* out,
                  plg_status* st) {
   if (!c) return set_status(st, PLG_OutOfRange, -1, -1, "null context");
+  std::lock_guard<std::mutex> lock_(c->mu);
   if (ni != nj) return set_status(st, PLG_LengthMismatch, -1, -1, "residual: length mismatch");
   if (ni < 2) return set_status(st, PLG_TooShort, -1, -1, "residual: need at least 2 samples");
   if (int rc = begin_call(c, st)) return rc;
@@ -1172,6 +1217,7 @@ int plg_residual(plg_ctx* c, const double* xi, int64_t ni, const double* xj, int
 
 int plg_entropy_approx(plg_ctx* c, const double* u, int64_t n, double* out, plg_status* st) {
   if (!c) return set_status(st, PLG_OutOfRange, -1, -1, "null context");
+  std::lock_guard<std::mutex> lock_(c->mu);
   if (n < 1) return set_status(st, PLG_TooShort, -1, -1, "entropy_approx: empty input");
   if (int rc = begin_call(c, st)) return rc;
   if (int rc = upload_vectors(c, {u}, n, st)) return rc;
@@ -1181,6 +1227,7 @@ int plg_entropy_approx(plg_ctx* c, const double* u, int64_t n, double* out, plg_
 
 int plg_entropy_of_normalized(plg_ctx* c, const double* r, int64_t n, double* out, plg_status* st) {
   if (!c) return set_status(st, PLG_OutOfRange, -1, -1, "null context");
+  std::lock_guard<std::mutex> lock_(c->mu);
   if (n < 1) return set_status(st, PLG_TooShort, -1, -1, "entropy_of_normalized: empty input");
   if (int rc = begin_call(c, st)) return rc;
   if (int rc = upload_vectors(c, {r}, n, st)) return rc;
@@ -1191,6 +1238,7 @@ int plg_entropy_of_normalized(plg_ctx* c, const double* r, int64_t n, double* ou
 int plg_diff_mutual_info(plg_ctx* c, const double* xi_std, const double* xj_std, const double* ri_j,
                          const double* rj_i, int64_t n, double* out, plg_status* st) {
   if (!c) return set_status(st, PLG_OutOfRange, -1, -1, "null context");
+  std::lock_guard<std::mutex> lock_(c->mu);
   if (n < 1) return set_status(st, PLG_TooShort, -1, -1, "diff_mutual_info: empty input");
   if (int rc = begin_call(c, st)) return rc;
   if (int rc = upload_vectors(c, {xi_std, xj_std, ri_j, rj_i}, n, st)) return rc;
@@ -1239,26 +1287,42 @@ int plg_tile_decode(int32_t t, int32_t nb, int32_t* bi, int32_t* bj) {
 }
 
 int plg_last_round_k(plg_ctx* c, double* out, int32_t cap, int32_t* count, plg_status* st) {
-  if (!c || !count) return set_status(st, PLG_OutOfRange, -1, -1, "null argument");
-  const int n = std::min(cap, c->last.rounds);
-  *count = n;
-  if (n > 0) PLG_CUDA(cudaMemcpy(out, c->rk.p, n * sizeof(double), cudaMemcpyDeviceToHost));
+  if (!c) return set_status(st, PLG_OutOfRange, -1, -1, "null context");
+  std::lock_guard<std::mutex> lock_(c->mu);
+  if (!count) return set_status(st, PLG_OutOfRange, -1, -1, "null argument");
+  const int n = std::min<int>(cap, static_cast<int>(c->last_k.size()));
+  *count = std::max(n, 0);
+  if (n > 0) std::memcpy(out, c->last_k.data(), n * sizeof(double));
+  return ok(st);
+}
+
+int plg_last_round_gaps(plg_ctx* c, double* second_out, int32_t cap, int32_t* count, plg_status* st) {
+  if (!c) return set_status(st, PLG_OutOfRange, -1, -1, "null context");
+  std::lock_guard<std::mutex> lock_(c->mu);
+  if (!count) return set_status(st, PLG_OutOfRange, -1, -1, "null argument");
+  const int n = std::min<int>(cap, static_cast<int>(c->last_second.size()));
+  *count = std::max(n, 0);
+  if (n > 0) std::memcpy(second_out, c->last_second.data(), n * sizeof(double));
   return ok(st);
 }
 
 int plg_set_detail_timing(plg_ctx* c, int32_t enable, plg_status* st) {
   if (!c) return set_status(st, PLG_OutOfRange, -1, -1, "null context");
+  std::lock_guard<std::mutex> lock_(c->mu);
   c->detail_timing = enable != 0;
   return ok(st);
 }
 
 int plg_set_prune(plg_ctx* c, int32_t enable, plg_status* st) {
   if (!c) return set_status(st, PLG_OutOfRange, -1, -1, "null context");
+  std::lock_guard<std::mutex> lock_(c->mu);
   c->prune = enable != 0;
   return ok(st);
 }
 
 int plg_debug_set_round_hook(plg_ctx* c, plg_round_hook hook, void* user) {
+  if (!c) return -1;
+  std::lock_guard<std::mutex> lock_(c->mu);
   if (!c) return PLG_OutOfRange;
   c->hook = hook;
   c->hook_user = user;
@@ -1266,6 +1330,8 @@ int plg_debug_set_round_hook(plg_ctx* c, plg_round_hook hook, void* user) {
 }
 
 int plg_last_stats(plg_ctx* c, plg_stats* out) {
+  if (!c) return -1;
+  std::lock_guard<std::mutex> lock_(c->mu);
   if (!c || !out) return PLG_OutOfRange;
   *out = c->last;
   return 0;
@@ -1275,6 +1341,7 @@ int plg_round_state(plg_ctx* c, const double* X, int64_t n, int32_t d, int64_t l
                     int32_t* active_out, int32_t* n_active, double* cols_out, int32_t* order_prefix_out,
                     plg_status* st) {
   if (!c) return set_status(st, PLG_OutOfRange, -1, -1, "null context");
+  std::lock_guard<std::mutex> lock_(c->mu);
   if (int rc = check_shape(n, d, ld, st)) return rc;
   if (rounds < 0 || rounds > d - 1) return set_status(st, PLG_OutOfRange, -1, -1, "rounds out of range");
   if (int rc = begin_call(c, st)) return rc;
@@ -1299,6 +1366,7 @@ int plg_round_state(plg_ctx* c, const double* X, int64_t n, int32_t d, int64_t l
 
 int plg_math_probe(plg_ctx* c, const double* u, int64_t n, double* out, plg_status* st) {
   if (!c) return set_status(st, PLG_OutOfRange, -1, -1, "null context");
+  std::lock_guard<std::mutex> lock_(c->mu);
   if (int rc = begin_call(c, st)) return rc;
   PLG_CUDA(c->Xd.reserve(static_cast<size_t>(n) * 5));
   PLG_CUDA(cudaMemcpyAsync(c->Xd.p, u, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
@@ -1311,63 +1379,87 @@ int plg_math_probe(plg_ctx* c, const double* u, int64_t n, double* out, plg_stat
 
 }  // extern "C"
 
+
 namespace {
 
-// Minimum-norm solution of the consistent symmetric system A x = b (A = X^T X / n of a
-// rank-deficient design) via cyclic Jacobi eigen-decomposition; equals the minimum-norm
-// least-squares solution of the design (Eigen CompleteOrthogonalDecomposition,
-// direct_lingam.cpp:58-62).
-void pinv_solve_sym(std::vector<double> A, int q, const double* b, double* x) {
-  std::vector<double> V(static_cast<size_t>(q) * q, 0.0);
-  for (int i = 0; i < q; ++i) V[static_cast<size_t>(i) * q + i] = 1.0;
-  for (int sweep = 0; sweep < 100; ++sweep) {
-    double off = 0.0, diag = 0.0;
-    for (int i = 0; i < q; ++i)
-      for (int j = 0; j < q; ++j) (i == j ? diag : off) += A[static_cast<size_t>(i) * q + j] * A[static_cast<size_t>(i) * q + j];
-    if (off <= 1e-30 * diag) break;
-    for (int p = 0; p < q; ++p)
-      for (int r = p + 1; r < q; ++r) {
-        const double apr = A[static_cast<size_t>(p) * q + r];
-        if (apr == 0.0) continue;
-        const double app = A[static_cast<size_t>(p) * q + p], arr = A[static_cast<size_t>(r) * q + r];
-        const double theta = (arr - app) / (2.0 * apr);
-        const double t = (theta >= 0 ? 1.0 : -1.0) / (std::fabs(theta) + std::sqrt(theta * theta + 1.0));
-        const double cs = 1.0 / std::sqrt(t * t + 1.0), sn = t * cs;
-        for (int k = 0; k < q; ++k) {  // A <- A J (columns p, r)
-          const double akp = A[static_cast<size_t>(k) * q + p], akr = A[static_cast<size_t>(k) * q + r];
-          A[static_cast<size_t>(k) * q + p] = cs * akp - sn * akr;
-          A[static_cast<size_t>(k) * q + r] = sn * akp + cs * akr;
-        }
-        for (int k = 0; k < q; ++k) {  // A <- J^T A (rows p, r)
-          const double apk = A[static_cast<size_t>(p) * q + k], ark = A[static_cast<size_t>(r) * q + k];
-          A[static_cast<size_t>(p) * q + k] = cs * apk - sn * ark;
-          A[static_cast<size_t>(r) * q + k] = sn * apk + cs * ark;
-        }
-        for (int k = 0; k < q; ++k) {
-          const double vkp = V[static_cast<size_t>(k) * q + p], vkr = V[static_cast<size_t>(k) * q + r];
-          V[static_cast<size_t>(k) * q + p] = cs * vkp - sn * vkr;
-          V[static_cast<size_t>(k) * q + r] = sn * vkp + cs * vkr;
-        }
-      }
+// Device echelon QR of A (c->W, n x ncol, ldw) with thresholds from `thr_mode` (0: the
+// weight step's per-prefix thresholds, 1: VAR design of `ndesign` columns), followed by
+// the coefficient solve of every column k >= k_first into `coef` (ncol x ncol rows) and,
+// with B != nullptr, the scatter into B. Host-visible results: rank, dependent flags.
+struct QrLayout {
+  double *cn, *thr, *tau, *T, *Yp, *Z, *coef;
+  int *qstate, *rbefore, *rowcol, *dep, *pinfo, *deps, *tg, *mcount;
+};
+
+int qr_reserve(plg_ctx* c, int64_t n, int ncol, QrLayout* L, plg_status* st) {
+  const int npanel = (ncol + plg::kQrNB - 1) / plg::kQrNB;
+  const size_t nd = 3 * static_cast<size_t>(ncol) + static_cast<size_t>(npanel) * plg::kQrNB * plg::kQrNB +
+                    static_cast<size_t>(plg::qr_scratch_doubles(n, ncol)) + static_cast<size_t>(ncol) * ncol;
+  const size_t ni = 2 + 6 * static_cast<size_t>(ncol) + 2 * static_cast<size_t>(npanel);
+  PLG_CUDA(c->qd.reserve(nd));
+  PLG_CUDA(c->qi.reserve(ni));
+  double* d = c->qd.p;
+  L->cn = d;
+  L->thr = d + ncol;
+  L->tau = d + 2 * ncol;
+  L->T = d + 3 * ncol;
+  L->Yp = L->T + static_cast<size_t>(npanel) * plg::kQrNB * plg::kQrNB;
+  L->Z = L->Yp + (plg::qr_scratch_doubles(n, ncol) - static_cast<int64_t>(plg::kQrNB) * ncol);
+  L->coef = L->Z + static_cast<size_t>(plg::kQrNB) * ncol;
+  int* q = c->qi.p;
+  L->qstate = q;
+  L->rbefore = q + 2;
+  L->rowcol = L->rbefore + ncol;
+  L->dep = L->rowcol + ncol;
+  L->deps = L->dep + ncol;
+  L->tg = L->deps + ncol;
+  L->mcount = L->tg + ncol;
+  L->pinfo = L->mcount + ncol;
+  return 0;
+}
+
+// Minimum-norm correction of the targets (positions >= 1) with dependent predecessors.
+// dep_h: host copy of the dependent flags. Returns through *any_pinv.
+int qr_mincorr(plg_ctx* c, const QrLayout& L, int ncol, const std::vector<int>& dep_h, const int* order_d,
+               double* B, int64_t ldb, int* any_pinv, plg_status* st) {
+  std::vector<int> deps, tg, mc;
+  for (int k = 0; k < ncol; ++k)
+    if (dep_h[k]) deps.push_back(k);
+  *any_pinv = 0;
+  if (deps.empty() || deps[0] >= ncol - 1) return 0;
+  *any_pinv = 1;
+  int m = 0;
+  for (int p = 1; p < ncol; ++p) {
+    while (m < static_cast<int>(deps.size()) && deps[m] < p) ++m;
+    if (m > 0) {
+      tg.push_back(p);
+      mc.push_back(m);
+    }
   }
-  double lmax = 0.0;
-  for (int i = 0; i < q; ++i) lmax = std::max(lmax, std::fabs(A[static_cast<size_t>(i) * q + i]));
-  const double tol = 1e-12 * lmax;
-  for (int j = 0; j < q; ++j) x[j] = 0.0;
-  for (int e = 0; e < q; ++e) {
-    const double lam = A[static_cast<size_t>(e) * q + e];
-    if (!(std::fabs(lam) > tol)) continue;
-    double proj = 0.0;
-    for (int k = 0; k < q; ++k) proj += V[static_cast<size_t>(k) * q + e] * b[k];
-    proj /= lam;
-    for (int j = 0; j < q; ++j) x[j] += proj * V[static_cast<size_t>(j) * q + e];
+  const int mmax = static_cast<int>(deps.size());
+  PLG_CUDA(cudaMemcpyAsync(L.deps, deps.data(), deps.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  PLG_CUDA(cudaMemcpyAsync(L.tg, tg.data(), tg.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  PLG_CUDA(cudaMemcpyAsync(L.mcount, mc.data(), mc.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  // scratch: per CTA mmax^2 doubles, batches of at most 2^27 doubles (1 GiB)
+  const int64_t per = static_cast<int64_t>(mmax) * mmax;
+  const int batch = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(static_cast<int64_t>(tg.size()),
+                                                                           (int64_t{1} << 27) / per)));
+  PLG_CUDA(c->part.reserve(static_cast<size_t>(batch) * per));
+  for (size_t b0 = 0; b0 < tg.size(); b0 += batch) {
+    const int cnt = static_cast<int>(std::min<size_t>(batch, tg.size() - b0));
+    PLG_CUDA(plg::launch_qr_mincorr(L.coef, ncol, L.rbefore, L.rowcol, L.deps, L.tg + b0, L.mcount + b0, cnt, order_d,
+                                    c->part.p, mmax, B, ldb, c->stream));
+    ++c->launches;
   }
+  return 0;
 }
 
 }  // namespace
 
 extern "C" int plg_estimate_var(plg_ctx* c, const double* ts, int64_t T, int32_t d, int64_t ld, int32_t lag,
                                 double* coef_out, double* resid_out, plg_status* st) {
+  if (!c) return set_status(st, PLG_OutOfRange, -1, -1, "null context");
+  std::lock_guard<std::mutex> lock_(c->mu);
   // var_lingam.cpp:7-53 on the device (var_kernels.cu): errors in the reference's order.
   if (!c) return set_status(st, PLG_OutOfRange, -1, -1, "null context");
   if (lag < 1) return set_status(st, PLG_OutOfRange, -1, -1, "estimate_var: lag must be >= 1");
@@ -1386,34 +1478,39 @@ extern "C" int plg_estimate_var(plg_ctx* c, const double* ts, int64_t T, int32_t
       if (!std::isfinite(v)) return set_status(st, PLG_NonFinite, -1, -1, "estimate_var: non-finite entries in series");
     return set_status(st, PLG_InsufficientRows, -1, -1, "estimate_var: series too short for lag %d", lag);
   }
+  // The stacked design [Z | Y] (var_kernels.cu) and ONE FP64 Householder QR of it
+  // (qr_kernels.cu): Z gets the reflectors, with ColPivHouseholderQR's rank test over the
+  // whole design (eps * min(rows, cols) * largest column norm, var_lingam.cpp:39-42 ->
+  // SingularDesign); the response columns only receive them, so their leading coordinates
+  // are Q^T Y and B = R^-1 (Q^T Y) (qr.solve, :43). Residuals Y - Z B by the FP64 GEMM.
   const int ncol = static_cast<int>(n_cols + d);
   const int64_t lda = round_up(n_rows, 16);
-  const size_t nn = static_cast<size_t>(n_cols) * n_cols;
   PLG_CUDA(c->W.reserve(static_cast<size_t>(ncol) * lda));
-  PLG_CUDA(c->C.reserve(static_cast<size_t>(ncol) * ncol));
-  PLG_CUDA(c->gscr.reserve(static_cast<size_t>(plg::gram_scratch_doubles(ncol, n_rows))));
-  PLG_CUDA(c->part.reserve(2 * nn + 2 * static_cast<size_t>(n_cols) * d + n_cols + static_cast<size_t>(n_rows) * d));
+  PLG_CUDA(c->scores.reserve(static_cast<size_t>(n_cols) * d + static_cast<size_t>(n_rows) * d));
   PLG_CUDA(c->stat.reserve(2));
-  double* S = c->part.p;
-  double* S0 = S + nn;
-  double* R = S0 + nn;
-  double* B = R + static_cast<size_t>(n_cols) * d;
-  double* D = B + static_cast<size_t>(n_cols) * d;
-  double* E = D + n_cols;
+  QrLayout L{};
+  if (int rc = qr_reserve(c, n_rows, ncol, &L, st)) return rc;
+  double* B = c->scores.p;
+  double* E = B + static_cast<size_t>(n_cols) * d;
   const int32_t init[2] = {static_cast<int32_t>(n_cols), 0};
   PLG_CUDA(cudaMemcpyAsync(c->stat.p, init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
   plg::launch_build_var_design(c->Xd.p, T, n_rows, d, lag, c->W.p, lda, c->stat.p + 1, c->stream);
-  plg::launch_gram(c->W.p, lda, n_rows, ncol, c->C.p, ncol, c->gscr.p, c->stream);
-  plg::launch_var_scale(c->C.p, ncol, static_cast<int>(n_cols), d, S, S0, R, D, c->stream);
-  plg::launch_cholesky(S, static_cast<int>(n_cols), 1e-14, c->stat.p, c->stream);
-  plg::launch_var_solve(S, S0, R, D, static_cast<int>(n_cols), d, B, c->stat.p, c->stream);
+  plg::launch_qr_center(c->W.p, lda, n_rows, nullptr, ncol, 0, c->W.p, lda, L.cn, c->stream);  // norms only
+  plg::launch_qr_thr_design(L.cn, n_rows, static_cast<int>(n_cols), ncol, L.thr, L.qstate, c->stream);
+  PLG_CUDA(plg::launch_qr_factor(c->W.p, lda, n_rows, ncol, L.thr, L.qstate, L.rbefore, L.rowcol, L.tau, L.dep,
+                                 L.pinfo, L.T, L.Yp, L.Z, c->stream));
+  PLG_CUDA(plg::launch_qr_solve(c->W.p, lda, ncol, static_cast<int>(n_cols), L.rbefore, L.rowcol, L.coef, ncol,
+                                nullptr, B, n_cols, c->stream));
+  // the factor overwrote the design: rebuild it for the residuals
+  plg::launch_build_var_design(c->Xd.p, T, n_rows, d, lag, c->W.p, lda, c->stat.p + 1, c->stream);
   plg::launch_var_resid(c->W.p, lda, n_rows, static_cast<int>(n_cols), d, B, E, n_rows, c->stream);
-  c->launches += 6;
-  int32_t flags[2] = {0, 0};
+  c->launches += 6 + 4 * ((ncol + plg::kQrNB - 1) / plg::kQrNB);
+  int32_t flags[2] = {0, 0}, qs[2] = {0, 0};
   PLG_CUDA(cudaMemcpyAsync(flags, c->stat.p, sizeof(flags), cudaMemcpyDeviceToHost, c->stream));
+  PLG_CUDA(cudaMemcpyAsync(qs, L.qstate, sizeof(qs), cudaMemcpyDeviceToHost, c->stream));
   PLG_CUDA(cudaStreamSynchronize(c->stream));
   if (flags[1]) return set_status(st, PLG_NonFinite, -1, -1, "estimate_var: non-finite entries in series");
-  if (flags[0] < n_cols) return set_status(st, PLG_SingularDesign, -1, -1, "estimate_var: rank-deficient design matrix");
+  if (qs[0] < n_cols) return set_status(st, PLG_SingularDesign, -1, -1, "estimate_var: rank-deficient design matrix");
   if (coef_out)
     PLG_CUDA(cudaMemcpyAsync(coef_out, B, static_cast<size_t>(n_cols) * d * sizeof(double), cudaMemcpyDeviceToHost,
                              c->stream));
@@ -1427,6 +1524,8 @@ extern "C" int plg_estimate_var(plg_ctx* c, const double* ts, int64_t T, int32_t
 
 extern "C" int plg_var_lagged_weights(plg_ctx* c, const double* B0, const double* M, int32_t d, int32_t lag,
                                       double* out, plg_status* st) {
+  if (!c) return set_status(st, PLG_OutOfRange, -1, -1, "null context");
+  std::lock_guard<std::mutex> lock_(c->mu);
   // var_lingam.cpp:55-70: B_tau = (I - B0) M_tau = M_tau - B0 M_tau for every lag, one FP64
   // GEMM launch per lag (var_resid_kernel with Z = B0, Y = B = M_tau).
   if (!c) return set_status(st, PLG_OutOfRange, -1, -1, "null context");
@@ -1448,13 +1547,18 @@ extern "C" int plg_var_lagged_weights(plg_ctx* c, const double* B0, const double
   return ok(st);
 }
 
+
 extern "C" int plg_fit_weights(plg_ctx* c, const double* X, int64_t n, int32_t d, int64_t ld,
                                const int32_t* order, double* B_out, int32_t* used_pinv,
                                plg_status* st) {
-  // DirectLingam::fit weights (direct_lingam.cpp:40-70): every predecessor regression of
-  // the centred data at once. With S = P^T Sigma P (order-permuted covariance) = L L^T,
-  // the coefficients of position p on positions 0..p-1 are -T[p, 0:p] / T[p, p], T = L^-1.
-  // The covariance comes from the device Gram of the standardised columns.
+  if (!c) return set_status(st, PLG_OutOfRange, -1, -1, "null context");
+  std::lock_guard<std::mutex> lock_(c->mu);
+  // DirectLingam::fit weights (direct_lingam.cpp:46-70): per target, least squares of the
+  // centred target on its centred predecessors (ColPivHouseholderQR, rank() < p ->
+  // CompleteOrthogonalDecomposition minimum-norm solution). Device: ONE Householder QR of
+  // the order-permuted centred design in echelon form (qr_kernels.cu) gives every
+  // predecessor regression; the rank test is ColPivHouseholderQR's threshold; targets with
+  // dependent predecessors take the minimum-norm correction on the device.
   if (!c) return set_status(st, PLG_OutOfRange, -1, -1, "null context");
   if (int rc = check_shape(n, d, ld, st)) return rc;
   std::vector<int> seen(d, 0);
@@ -1466,53 +1570,30 @@ extern "C" int plg_fit_weights(plg_ctx* c, const double* X, int64_t n, int32_t d
   if (int rc = upload_x(c, X, n, d, ld, st)) return rc;
   const int64_t ldw = round_up(n, 16);
   if (int rc = reserve_run(c, n, d, ldw, st)) return rc;
+  // validate (types.cpp:21-47, called by DirectLingam::fit first): NonFinite / ZeroVariance
   if (int rc = standardize_validate(c, c->Xd.p, n, n, d, nullptr, nullptr, ldw, true, st)) return rc;
-  plg::launch_gram(c->W.p, ldw, n, d, c->C.p, d, c->gscr.p, c->stream);
-  // Device: S = permuted correlation, S = L L^T (blocked FP64 Cholesky, chol_kernels.cu),
-  // then one backward substitution per target. Positions p <= deficient_from have a
-  // full-rank predecessor design.
   const size_t dd = static_cast<size_t>(d) * d;
-  PLG_CUDA(c->part.reserve(2 * dd));  // scratch: S/L and the per-target beta rows
-  PLG_CUDA(c->scores.reserve(dd));    // B on device
+  QrLayout L{};
+  if (int rc = qr_reserve(c, n, d, &L, st)) return rc;
+  PLG_CUDA(c->scores.reserve(dd));  // B on device
   PLG_CUDA(c->idx.reserve(d));
-  PLG_CUDA(c->stat.reserve(2));
   PLG_CUDA(cudaMemcpyAsync(c->idx.p, order, d * sizeof(int32_t), cudaMemcpyHostToDevice, c->stream));
-  PLG_CUDA(cudaMemcpyAsync(c->stat.p, &d, sizeof(int32_t), cudaMemcpyHostToDevice, c->stream));
   PLG_CUDA(cudaMemsetAsync(c->scores.p, 0, dd * sizeof(double), c->stream));
-  double* S = c->part.p;
-  plg::launch_permute(c->C.p, d, c->idx.p, d, S, c->stream);
-  plg::launch_cholesky(S, d, kZeroVarTol, c->stat.p, c->stream);
-  int deficient_from = d;
-  PLG_CUDA(cudaMemcpyAsync(&deficient_from, c->stat.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  plg::launch_qr_center(c->Xd.p, n, n, c->idx.p, d, 1, c->W.p, ldw, L.cn, c->stream);
+  plg::launch_qr_thr_prefix(L.cn, n, d, L.thr, L.qstate, c->stream);
+  PLG_CUDA(plg::launch_qr_factor(c->W.p, ldw, n, d, L.thr, L.qstate, L.rbefore, L.rowcol, L.tau, L.dep, L.pinfo, L.T,
+                                 L.Yp, L.Z, c->stream));
+  PLG_CUDA(plg::launch_qr_solve(c->W.p, ldw, d, 1, L.rbefore, L.rowcol, L.coef, d, c->idx.p, c->scores.p, d,
+                                c->stream));
+  c->launches += 4 + 4 * ((d + plg::kQrNB - 1) / plg::kQrNB);
+  std::vector<int> dep_h(d);
+  PLG_CUDA(cudaMemcpyAsync(dep_h.data(), L.dep, d * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   PLG_CUDA(cudaStreamSynchronize(c->stream));
-  const int full = std::min(d, deficient_from + 1);
-  plg::launch_regress_rows(S, d, c->idx.p, c->msd.p, full, c->part.p + dd, c->scores.p, d, c->stream);
+  int any = 0;
+  if (int rc = qr_mincorr(c, L, d, dep_h, c->idx.p, c->scores.p, d, &any, st)) return rc;
   PLG_CUDA(cudaMemcpyAsync(B_out, c->scores.p, dd * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-  std::vector<double> C, msd(2 * static_cast<size_t>(d));
-  PLG_CUDA(cudaMemcpyAsync(msd.data(), c->msd.p, msd.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-  if (full < d) {
-    C.resize(dd);
-    PLG_CUDA(cudaMemcpyAsync(C.data(), c->C.p, dd * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-  }
   PLG_CUDA(cudaStreamSynchronize(c->stream));
   PLG_CUDA(cudaGetLastError());
-  *used_pinv = 0;
-  // Rank-deficient predecessor designs (rare): minimum-norm solution on the unscaled
-  // covariance, on the host.
-  for (int p = full; p < d; ++p) {
-    *used_pinv = 1;
-    std::vector<double> A(static_cast<size_t>(p) * p), b(p), x(p);
-    const int t = order[p];
-    for (int i = 0; i < p; ++i) {
-      const int oi = order[i];
-      for (int j = 0; j < p; ++j) {
-        const int oj = order[j];
-        A[static_cast<size_t>(i) * p + j] = C[static_cast<size_t>(oi) * d + oj] * msd[2 * oi + 1] * msd[2 * oj + 1];
-      }
-      b[i] = C[static_cast<size_t>(oi) * d + t] * msd[2 * oi + 1] * msd[2 * t + 1];
-    }
-    pinv_solve_sym(A, p, b.data(), x.data());
-    for (int q = 0; q < p; ++q) B_out[t + static_cast<int64_t>(d) * order[q]] = x[q];
-  }
+  *used_pinv = any;
   return ok(st);
 }

@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <memory>
 #include <mutex>
 
 #include "../../../include/plingam_b200.h"
@@ -108,9 +109,14 @@ bool permuted_is_lower_triangular(const WeightedDag& dag) {  // types.cpp:73-88
 namespace gpu {
 
 namespace {
+// The process-wide context of the reference-shaped API. Calls hold a shared reference for
+// their duration, so set_device()/reset() never destroy a context a call is still using
+// (the last reference destroys it); plg_ctx serialises concurrent calls on one context.
 std::mutex g_mu;
-plg_ctx* g_ctx = nullptr;
+std::shared_ptr<plg_ctx> g_ctx;
 int g_device = 0;
+
+std::shared_ptr<plg_ctx> own(plg_ctx* c) { return std::shared_ptr<plg_ctx>(c, [](plg_ctx* p) { plg_ctx_destroy(p); }); }
 }  // namespace
 
 void check(int rc, const void* status) {
@@ -121,28 +127,26 @@ void check(int rc, const void* status) {
   throw Error(code, st->msg, static_cast<long>(st->row), static_cast<long>(st->col));
 }
 
-plg_ctx* context() {
+std::shared_ptr<plg_ctx> context() {
   std::lock_guard<std::mutex> lk(g_mu);
   if (!g_ctx) {
     plg_status st{};
-    check(plg_ctx_create(g_device, &g_ctx, &st), &st);
+    plg_ctx* c = nullptr;
+    check(plg_ctx_create(g_device, &c, &st), &st);
+    g_ctx = own(c);
   }
   return g_ctx;
 }
 
 void set_device(int device) {
   std::lock_guard<std::mutex> lk(g_mu);
-  if (g_ctx && device != g_device) {
-    plg_ctx_destroy(g_ctx);
-    g_ctx = nullptr;
-  }
+  if (g_ctx && device != g_device) g_ctx.reset();
   g_device = device;
 }
 
 void reset() {
   std::lock_guard<std::mutex> lk(g_mu);
-  if (g_ctx) plg_ctx_destroy(g_ctx);
-  g_ctx = nullptr;
+  g_ctx.reset();
 }
 
 std::string nccl_unique_id() {
@@ -155,11 +159,12 @@ std::string nccl_unique_id() {
 void init_distributed(int device, int rank, int world, const std::string& nccl_uid) {
   if (nccl_uid.size() != 128) throw Error(ErrorCode::OutOfRange, "init_distributed: NCCL id must be 128 bytes");
   std::lock_guard<std::mutex> lk(g_mu);
-  if (g_ctx) plg_ctx_destroy(g_ctx);
-  g_ctx = nullptr;
+  g_ctx.reset();
   g_device = device;
   plg_status st{};
-  check(plg_ctx_create_dist(device, rank, world, nccl_uid.data(), &g_ctx, &st), &st);
+  plg_ctx* c = nullptr;
+  check(plg_ctx_create_dist(device, rank, world, nccl_uid.data(), &c, &st), &st);
+  g_ctx = own(c);
 }
 
 }  // namespace gpu
@@ -170,7 +175,7 @@ SearchResult search_causal_order(const DataMatrix& X, std::span<const int> U) {
   res.scores.scores.assign(static_cast<std::size_t>(X.dims()), 0.0);
   std::vector<int32_t> u(U.begin(), U.end());
   plg_status st{};
-  gpu::check(plg_search(gpu::context(), X.values.data(), X.samples(), static_cast<int32_t>(X.dims()),
+  gpu::check(plg_search(gpu::context().get(), X.values.data(), X.samples(), static_cast<int32_t>(X.dims()),
                         X.samples(), u.data(), static_cast<int32_t>(u.size()), &res.chosen,
                         res.scores.scores.data(), &st),
              &st);
@@ -188,7 +193,7 @@ DataMatrix regress_out(const DataMatrix& X, int exog, std::span<const int> remai
   std::vector<int32_t> rem(remaining.begin(), remaining.end());
   std::vector<double> out(static_cast<std::size_t>(X.samples()) * rem.size());
   plg_status st{};
-  gpu::check(plg_regress_out(gpu::context(), X.values.data(), X.samples(), static_cast<int32_t>(X.dims()),
+  gpu::check(plg_regress_out(gpu::context().get(), X.values.data(), X.samples(), static_cast<int32_t>(X.dims()),
                              X.samples(), exog, rem.data(), static_cast<int32_t>(rem.size()), out.data(), &st),
              &st);
   std::vector<std::string> names;
@@ -209,7 +214,7 @@ CausalOrder causal_order(const DataMatrix& X, bool parallel, int workers) {
   CausalOrder result;
   result.order.assign(static_cast<std::size_t>(std::max<std::int64_t>(X.dims(), 0)), -1);
   plg_status st{};
-  gpu::check(plg_causal_order(gpu::context(), X.values.data(), X.samples(), static_cast<int32_t>(X.dims()),
+  gpu::check(plg_causal_order(gpu::context().get(), X.values.data(), X.samples(), static_cast<int32_t>(X.dims()),
                               std::max<std::int64_t>(X.samples(), 1), result.order.data(), &st),
              &st);
   return result;
@@ -238,7 +243,7 @@ WeightedDag DirectLingam::fit(const DataMatrix& X, FitPhases& phases) const {  /
   int32_t used_pinv = 0;
   if (dag.d > 1) {
     plg_status st{};
-    gpu::check(plg_fit_weights(gpu::context(), X.values.data(), X.samples(), dag.d, X.samples(),
+    gpu::check(plg_fit_weights(gpu::context().get(), X.values.data(), X.samples(), dag.d, X.samples(),
                                order.order.data(), dag.weights.data(), &used_pinv, &st),
                &st);
   }

@@ -20,6 +20,7 @@
 #include <set>
 #include <span>
 #include <stdexcept>
+#include <memory>
 #include <string>
 #include <utility>
 #include <vector>
@@ -156,7 +157,7 @@ namespace gpu {
 
 // The engine the API above runs on: device `device` (default: the current CUDA device,
 // 0 if none set), single rank unless init_distributed was called.
-plg_ctx* context();
+std::shared_ptr<plg_ctx> context();
 // One process per GPU: every rank calls this with the same 128-byte NCCL unique id
 // (nccl_unique_id() on rank 0, broadcast by the caller). Replaces context().
 void init_distributed(int device, int rank, int world, const std::string& nccl_uid);

@@ -115,7 +115,7 @@ PYBIND11_MODULE(_core, m) {
         int rc;
         {
           py::gil_scoped_release rel;
-          rc = plg_causal_order(gpu::context(), X.data(), n, d, std::max<std::int64_t>(n, 1), order.data(), &st);
+          rc = plg_causal_order(gpu::context().get(), X.data(), n, d, std::max<std::int64_t>(n, 1), order.data(), &st);
         }
         gpu::check(rc, &st);
         order.resize(static_cast<std::size_t>(std::max(d, 0)));
@@ -137,7 +137,7 @@ PYBIND11_MODULE(_core, m) {
     int rc;
     {
       py::gil_scoped_release rel;
-      rc = plg_search(gpu::context(), X.data(), n, d, std::max<std::int64_t>(n, 1), U.data(),
+      rc = plg_search(gpu::context().get(), X.data(), n, d, std::max<std::int64_t>(n, 1), U.data(),
                       static_cast<int32_t>(U.size()), &chosen, scores.data(), &st);
     }
     gpu::check(rc, &st);
@@ -190,10 +190,10 @@ PYBIND11_MODULE(_core, m) {
           py::gil_scoped_release rel;
           using Clock = std::chrono::steady_clock;
           const auto t0 = Clock::now();
-          rc = plg_causal_order(gpu::context(), X.data(), n, d, std::max<std::int64_t>(n, 1), dag.order.order.data(), &st);
+          rc = plg_causal_order(gpu::context().get(), X.data(), n, d, std::max<std::int64_t>(n, 1), dag.order.order.data(), &st);
           const auto t1 = Clock::now();
           if (rc == 0 && d > 1)
-            rc = plg_fit_weights(gpu::context(), X.data(), n, d, n, dag.order.order.data(), dag.weights.data(), &pinv, &st);
+            rc = plg_fit_weights(gpu::context().get(), X.data(), n, d, n, dag.order.order.data(), dag.weights.data(), &pinv, &st);
           const auto t2 = Clock::now();
           phases.ordering_seconds = std::chrono::duration<double>(t1 - t0).count();
           phases.weights_seconds = std::chrono::duration<double>(t2 - t1).count();
@@ -224,7 +224,7 @@ PYBIND11_MODULE(_core, m) {
         int rc;
         {
           py::gil_scoped_release rel;
-          rc = plg_standardize(gpu::context(), x.data(), x.size(), out.mutable_data(), &st);
+          rc = plg_standardize(gpu::context().get(), x.data(), x.size(), out.mutable_data(), &st);
         }
         gpu::check(rc, &st);
         return out;
@@ -238,7 +238,7 @@ PYBIND11_MODULE(_core, m) {
         int rc;
         {
           py::gil_scoped_release rel;
-          rc = plg_residual(gpu::context(), xi.data(), xi.size(), xj.data(), xj.size(), out.mutable_data(), &st);
+          rc = plg_residual(gpu::context().get(), xi.data(), xi.size(), xj.data(), xj.size(), out.mutable_data(), &st);
         }
         gpu::check(rc, &st);
         return out;
@@ -252,7 +252,7 @@ PYBIND11_MODULE(_core, m) {
         int rc;
         {
           py::gil_scoped_release rel;
-          rc = plg_entropy_approx(gpu::context(), u.data(), u.size(), &out, &st);
+          rc = plg_entropy_approx(gpu::context().get(), u.data(), u.size(), &out, &st);
         }
         gpu::check(rc, &st);
         return out;
@@ -268,7 +268,7 @@ PYBIND11_MODULE(_core, m) {
         int rc;
         {
           py::gil_scoped_release rel;
-          rc = plg_diff_mutual_info(gpu::context(), xi.data(), xj.data(), ri.data(), rj.data(), xi.size(), &out, &st);
+          rc = plg_diff_mutual_info(gpu::context().get(), xi.data(), xj.data(), ri.data(), rj.data(), xi.size(), &out, &st);
         }
         gpu::check(rc, &st);
         return out;
@@ -527,6 +527,17 @@ PYBIND11_MODULE(_core, m) {
             return out;
           },
           py::arg("u"))
+      .def("round_gaps",
+           [](Engine& e) {
+             plg_stats s{};
+             plg_last_stats(e.ctx, &s);
+             std::vector<double> g(static_cast<std::size_t>(std::max(s.rounds, 0)));
+             int32_t cnt = 0;
+             plg_status st{};
+             gpu::check(plg_last_round_gaps(e.ctx, g.data(), static_cast<int32_t>(g.size()), &cnt, &st), &st);
+             g.resize(static_cast<std::size_t>(cnt));
+             return g;
+           })
       .def("round_k",
            [](Engine& e) {
              plg_stats s{};
@@ -570,6 +581,9 @@ PYBIND11_MODULE(_core, m) {
         d["d2h_bytes"] = s.d2h_bytes;
         d["resid_ms"] = s.resid_ms;
         d["resid_bytes"] = s.resid_bytes;
+        d["near_ties"] = s.near_ties;
+        d["min_gap"] = s.min_gap;
+        d["min_gap_round"] = s.min_gap_round;
         return d;
       });
 }

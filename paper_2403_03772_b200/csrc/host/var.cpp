@@ -95,7 +95,7 @@ VarEstimate estimate_var(const DataMatrix& ts, int lag) {
   std::vector<double> coef(static_cast<size_t>(std::max<int64_t>(n_cols, 1) * std::max<int64_t>(d, 1)));
   std::vector<double> res(static_cast<size_t>(std::max<int64_t>(n_rows, 1) * std::max<int64_t>(d, 1)));
   plg_status st{};
-  gpu::check(plg_estimate_var(gpu::context(), ts.values.data(), T, static_cast<int32_t>(d), std::max<int64_t>(T, 1),
+  gpu::check(plg_estimate_var(gpu::context().get(), ts.values.data(), T, static_cast<int32_t>(d), std::max<int64_t>(T, 1),
                               lag, coef.data(), res.data(), &st),
              &st);
   VarEstimate est;
@@ -189,7 +189,7 @@ VarModel fit_varlingam(const DataMatrix& ts, int lag, const DirectLingamConfig& 
   std::vector<double> ms(dd * model.m_raw.size()), out(dd * model.m_raw.size());
   for (size_t t = 0; t < model.m_raw.size(); ++t) std::copy(model.m_raw[t].begin(), model.m_raw[t].end(), ms.begin() + t * dd);
   plg_status st{};
-  gpu::check(plg_var_lagged_weights(gpu::context(), model.b0.weights.data(), ms.data(), d,
+  gpu::check(plg_var_lagged_weights(gpu::context().get(), model.b0.weights.data(), ms.data(), d,
                                     static_cast<int32_t>(model.m_raw.size()), out.data(), &st),
              &st);
   for (size_t t = 0; t < model.m_raw.size(); ++t)

@@ -528,12 +528,12 @@ __global__ void math_probe_kernel(const double* u, int64_t n, double* out, const
 
 template <int NI, int NJ, bool kDedicated, bool kClampA>
 void launch_pair_cfg(const PairLaunch& a, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
+  static DeviceCache attr;
+  attr.get([] {
     cudaFuncSetAttribute(pair_kernel<NI, NJ, kDedicated, kClampA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(kPairSmem));
-    attr = true;
-  }
+    return 1;
+  });
   pair_kernel<NI, NJ, kDedicated, kClampA>
       <<<a.ntiles * a.nseg, PairCfg<NI, NJ, kDedicated>::kThreads, kPairSmem, s>>>(a);
 }
@@ -567,11 +567,11 @@ void launch_finalize(const PairLaunch& a, cudaStream_t s) {
 namespace {
 template <bool kClampA>
 void launch_pair_small_cfg(const PairLaunch& a, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
+  static DeviceCache attr;
+  attr.get([] {
     cudaFuncSetAttribute(pair_small_kernel<kClampA>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTableBytes);
-    attr = true;
-  }
+    return 1;
+  });
   const int npairs = a.u * (a.u - 1) / 2;
   pair_small_kernel<kClampA>
       <<<dim3((npairs + kSmallThreads - 1) / kSmallThreads, a.nseg), kSmallThreads, kTableBytes, s>>>(a);
@@ -592,11 +592,11 @@ void launch_colent(const double* W, int64_t ldw, int64_t n, const double* C, int
                    const int* act, int u, double* H, const double* g_exp, const double2* g_log,
                    const int* nz, const int* col_var, int round, unsigned long long* err,
                    cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
+  static DeviceCache attr;
+  attr.get([] {
     cudaFuncSetAttribute(colent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTableBytes);
-    attr = true;
-  }
+    return 1;
+  });
   const int grid = u < 4 * 148 ? u : 4 * 148;
   colent_kernel<<<grid, kColentThreads, kTableBytes, s>>>(W, ldw, n, C, ldc, act, u, H, g_exp,
                                                           g_log, nz, col_var, round, err);
@@ -607,15 +607,15 @@ int resid_chunks(int64_t n) { return static_cast<int>((n + kResidChunk - 1) / kR
 void launch_resid_ent(double* W, int64_t ldw, int64_t n, const double* C, int64_t ldc, const int* act_nxt, int ur,
                       const RoundState* rs, int* nz, int tag, const unsigned long long* err, double* hpart,
                       const double* g_exp, const double2* g_log, cudaStream_t s) {
-  static int grid = 0;
-  if (!grid) {
+  static DeviceCache gridc;
+  const int grid = gridc.get([] {
     cudaFuncSetAttribute(resid_ent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTableBytes);
     int dev = 0, sms = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, resid_ent_kernel, kResidThreads, kTableBytes);
-    grid = sms * (per > 0 ? per : 1);
-  }
+    return sms * (per > 0 ? per : 1);
+  });
   const int nch = resid_chunks(n);
   const int need = (ur * nch + kResidThreads / 32 - 1) / (kResidThreads / 32);
   const int g = need < grid ? need : grid;
@@ -631,22 +631,22 @@ void launch_hfin(const double* hpart, int64_t n, const double* C, int64_t ldc, c
 
 void launch_entropy_vec(const double* u, int64_t n, double scale, double* out, const double* g_exp,
                         const double2* g_log, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
+  static DeviceCache attr;
+  attr.get([] {
     cudaFuncSetAttribute(entropy_vec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTableBytes);
-    attr = true;
-  }
+    return 1;
+  });
   entropy_vec_kernel<<<1, kColentThreads, kTableBytes, s>>>(u, n, scale, out, g_exp, g_log);
 }
 
 void launch_math_probe(const double* u, int64_t n, double* out, const double* g_exp,
                        const double2* g_log, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
+  static DeviceCache attr;
+  attr.get([] {
     cudaFuncSetAttribute(math_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kTableBytes);
-    attr = true;
-  }
+    return 1;
+  });
   int grid = static_cast<int>((n + 255) / 256);
   if (grid > 1184) grid = 1184;
   if (grid < 1) grid = 1;

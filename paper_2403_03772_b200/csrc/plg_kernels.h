@@ -2,9 +2,30 @@
 // Internal to libplingam_b200.so (the C-ABI in include/plingam_b200.h is the boundary).
 #pragma once
 #include <cuda_runtime.h>
+#include <atomic>
 #include <cstdint>
 
 namespace plg {
+
+// Per-device once-values. Kernel attributes (the dynamic shared memory opt-in above 48 KB)
+// and occupancy-derived grids belong to the device current at launch, so a process that
+// switches devices (set_device, one context per GPU) must not reuse another device's.
+constexpr int kMaxDevices = 64;
+struct DeviceCache {
+  std::atomic<int> v[kMaxDevices] = {};
+  template <class F>
+  int get(F f) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::atomic<int>& a = v[dev & (kMaxDevices - 1)];
+    int x = a.load(std::memory_order_acquire);
+    if (!x) {
+      x = f();
+      a.store(x, std::memory_order_release);
+    }
+    return x;
+  }
+};
 
 constexpr int kBT = 32;           // active positions per tile side
 constexpr int kTilePairs = kBT * kBT;
@@ -188,7 +209,7 @@ void launch_prune_top(const PruneArgs& a, int R, cudaStream_t s);
 // beta > 0 (refine): deficit mode — predicted contributions reaching beta x the row's deficit
 void launch_prune_select(const PruneArgs& a, int stage, int m, double beta, cudaStream_t s);
 void launch_prune_scan(const PruneArgs& a, cudaStream_t s);
-void launch_prune_pairs(const PruneArgs& a, cudaStream_t s);
+cudaError_t launch_prune_pairs(const PruneArgs& a, cudaStream_t s);  // cooperative launch result
 // multi-rank: all ranks' results (res, `world` slots of `slot` entries; entry k of the list
 // sits at (k / cnt) slot + k % cnt with cnt = ceil(total / world)) into Md / KN
 void launch_prune_scatter(const PruneArgs& a, int world, int slot, cudaStream_t s);
@@ -199,10 +220,12 @@ int prune_pairs_grid();  // co-resident CTAs of the cooperative list kernel
 constexpr int kMaxPruneStages = 8;
 
 // argmin over k (lowest position on ties), order/score bookkeeping, active-list compaction;
-// round_k (optional): the winning k of each round.
+// round_k (optional): the winning k of each round; round_second (optional): the runner-up's
+// k, with lb[p] standing in for rows whose k a pruned round left at +inf (near-tie guard).
 void launch_commit(const double* k, const int* act_cur, int* act_nxt, int u, const int* col_var,
                    int* order, int round, double* scores, RoundState* rs,
-                   const unsigned long long* err, cudaStream_t s, double* round_k = nullptr);
+                   const unsigned long long* err, cudaStream_t s, double* round_k = nullptr,
+                   const double* lb = nullptr, double* round_second = nullptr);
 
 // Rank-1 Schur update of the remaining Gram block.
 void launch_update_gram(double* C, int64_t ldc, const int* act_nxt, int ur, const RoundState* rs,
@@ -218,21 +241,28 @@ void launch_residualize(double* W, int64_t ldw, int64_t n, const double* C, int6
 void launch_regress_out(const double* X, int64_t ldx, int64_t n, int exog, const int* remaining,
                         int r, double* out, int64_t ldo, int* zero_var_flag, cudaStream_t s);
 
-// Weight step (chol_kernels.cu): S = C[order][order]; in-place blocked Cholesky of the
-// correlation S (fail = first position whose pivot is <= tol, else untouched); beta rows of
-// every target p < limit written as B[order[p] + ldb * order[q]] in original units.
-void launch_permute(const double* C, int64_t ldc, const int* order, int n, double* S, cudaStream_t s);
-void launch_cholesky(double* S, int n, double tol, int* fail, cudaStream_t s);
-void launch_regress_rows(const double* L, int n, const int* order, const double* msd, int limit, double* beta,
-                         double* B, int64_t ldb, cudaStream_t s);
+// FP64 blocked Householder QR in echelon form (qr_kernels.cu): weights of DirectLiNGAM
+// (every predecessor regression from one QR of the order-permuted centred design) and the
+// VAR least squares. A (n x ncol, lda) is factored in place; thr[k]: a column whose residual
+// norm is <= thr[k] is dependent (no reflector). qstate = {rank, dependent count}.
+constexpr int kQrNB = 32;
+void launch_qr_center(const double* X, int64_t ldx, int64_t n, const int* order, int ncol, int center, double* A,
+                      int64_t lda, double* cn, cudaStream_t s);
+void launch_qr_thr_prefix(const double* cn, int64_t n, int d, double* thr, int* qstate, cudaStream_t s);
+void launch_qr_thr_design(const double* cn, int64_t n, int ncol, int ntot, double* thr, int* qstate, cudaStream_t s);
+int64_t qr_scratch_doubles(int64_t n, int ncol);  // Yp + Z of the trailing updates
+cudaError_t launch_qr_factor(double* A, int64_t lda, int64_t n, int ncol, const double* thr, int* qstate,
+                             int* rbefore, int* rowcol, double* tau, int* dep, int* pinfo, double* T, double* Yp,
+                             double* Z, cudaStream_t s);
+cudaError_t launch_qr_solve(const double* A, int64_t lda, int ncol, int k_first, const int* rbefore, const int* rowcol,
+                            double* coef, int64_t ldcoef, const int* order, double* B, int64_t ldb, cudaStream_t s);
+cudaError_t launch_qr_mincorr(const double* coef, int64_t ldcoef, const int* rbefore, const int* rowcol,
+                              const int* deps, const int* tg, const int* mcount, int ntg, const int* order, double* N,
+                              int mmax, double* B, int64_t ldb, cudaStream_t s);
 
 // VarLiNGAM front-end (var_kernels.cu): stacked design, normal equations, residuals.
 void launch_build_var_design(const double* ts, int64_t ldt, int64_t n_rows, int d, int lag, double* A, int64_t lda,
                              int* nonfinite, cudaStream_t s);
-void launch_var_scale(const double* G, int64_t ldg, int n_cols, int d, double* S, double* S0, double* R, double* D,
-                      cudaStream_t s);
-void launch_var_solve(const double* L, const double* S0, const double* R, const double* D, int n_cols, int d,
-                      double* B, const int* fail, cudaStream_t s);
 void launch_var_resid(const double* A, int64_t lda, int64_t n_rows, int n_cols, int d, const double* B, double* E,
                       int64_t lde, cudaStream_t s);
 

@@ -959,8 +959,8 @@ __global__ void __launch_bounds__(256) prune_bound_kernel(const PruneArgs a, int
 
 template <bool kClampA, int kVar>
 int pairs_grid_for() {
-  static int grid = 0;
-  if (!grid) {
+  static DeviceCache gridc;
+  return gridc.get([] {
     cudaFuncSetAttribute(prune_pairs_kernel<kClampA, kVar>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kTableAlignedBytes);
     int dev = 0, sms = 0, per = 0;
@@ -968,18 +968,19 @@ int pairs_grid_for() {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, prune_pairs_kernel<kClampA, kVar>, kListThreads,
                                                   kTableAlignedBytes);
-    grid = sms * (per > 0 ? per : 1);
-  }
-  return grid;
+    return sms * (per > 0 ? per : 1);
+  });
 }
 
 template <bool kClampA, int kVar>
-void launch_pairs_cfg(const PruneArgs& a, cudaStream_t s) {
+cudaError_t launch_pairs_cfg(const PruneArgs& a, cudaStream_t s) {
   const int grid = pairs_grid_for<kClampA, kVar>();
   PruneArgs args = a;
   void* params[] = {&args};
-  cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(prune_pairs_kernel<kClampA, kVar>), dim3(grid),
-                              dim3(kListThreads), params, kTableAlignedBytes, s);
+  // the grid barrier between batches needs every CTA resident: a failed cooperative launch
+  // (e.g. fewer co-resident CTAs under a tool) must surface, not be skipped silently
+  return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(prune_pairs_kernel<kClampA, kVar>), dim3(grid),
+                                     dim3(kListThreads), params, kTableAlignedBytes, s);
 }
 
 }  // namespace
@@ -997,11 +998,11 @@ void launch_prune_select(const PruneArgs& a, int stage, int m, double beta, cuda
   else {
     prune_rowl_kernel<<<a.u, kRowThreads, 0, s>>>(a);
     // the row's predictions cached in shared memory (u <= 24 576; larger rows re-read them)
-    static bool attr = false;
-    if (!attr) {
+    static DeviceCache attr;
+    attr.get([] {
       cudaFuncSetAttribute(prune_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 24576 * 8);
-      attr = true;
-    }
+      return 1;
+    });
     const int cache = a.u <= 24576 ? 1 : 0;
     prune_select_kernel<<<a.u, kSelThreads, cache ? a.u * sizeof(double) : 0, s>>>(a, stage, m, beta, cache);
   }
@@ -1009,16 +1010,16 @@ void launch_prune_select(const PruneArgs& a, int stage, int m, double beta, cuda
 
 void launch_prune_scan(const PruneArgs& a, cudaStream_t s) { prune_scan_kernel<<<1, 1024, 0, s>>>(a); }
 
-void launch_prune_pairs(const PruneArgs& a, cudaStream_t s) {
+cudaError_t launch_prune_pairs(const PruneArgs& a, cudaStream_t s) {
   static const int var = [] {  // PLG_LIST_VAR: load-pipeline variant (tuning knob)
     const char* v = std::getenv("PLG_LIST_VAR");
     return v ? std::atoi(v) : 0;
   }();
-  if (a.n > 90000) launch_pairs_cfg<true, 0>(a, s);
-  else if (var == 1) launch_pairs_cfg<false, 1>(a, s);
-  else if (var == 2) launch_pairs_cfg<false, 2>(a, s);
-  else if (var == 4) launch_pairs_cfg<false, 4>(a, s);
-  else launch_pairs_cfg<false, 0>(a, s);
+  if (a.n > 90000) return launch_pairs_cfg<true, 0>(a, s);
+  if (var == 1) return launch_pairs_cfg<false, 1>(a, s);
+  if (var == 2) return launch_pairs_cfg<false, 2>(a, s);
+  if (var == 4) return launch_pairs_cfg<false, 4>(a, s);
+  return launch_pairs_cfg<false, 0>(a, s);
 }
 
 void launch_prune_scatter(const PruneArgs& a, int world, int slot, cudaStream_t s) {

@@ -204,9 +204,10 @@ constexpr int kCommitThreads = 1024;
 __global__ void __launch_bounds__(kCommitThreads)
     commit_kernel(const double* k, const int* act_cur, int* act_nxt, int u, const int* col_var,
                   int* order, int round, double* scores, RoundState* rs,
-                  const unsigned long long* err, double* round_k) {
+                  const unsigned long long* err, double* round_k, const double* lb, double* round_second) {
   __shared__ double sk[kCommitThreads];
   __shared__ int sp[kCommitThreads];
+  __shared__ double s2[kCommitThreads];
   if (*err != kNoError) return;
   double best = 0.0;
   int bp = -1;
@@ -234,6 +235,24 @@ __global__ void __launch_bounds__(kCommitThreads)
   }
   const int pc = sp[0];
   const int m = act_cur[pc];
+  if (round_second) {
+    // Near-tie guard: the runner-up's k (exact for fully evaluated rows; for rows a pruned
+    // round left at +inf, their partial k lb[p] — a lower bound above k* (1 + 1e-9)).
+    double v2 = INFINITY;
+    for (int p = threadIdx.x; p < u; p += kCommitThreads) {
+      if (p == pc) continue;
+      double v = k[p];
+      if (lb && isinf(v)) v = lb[p];
+      v2 = fmin(v2, v);
+    }
+    s2[threadIdx.x] = v2;
+    __syncthreads();
+    for (int s = kCommitThreads / 2; s > 0; s >>= 1) {
+      if (threadIdx.x < s) s2[threadIdx.x] = fmin(s2[threadIdx.x], s2[threadIdx.x + s]);
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) round_second[round] = s2[0];
+  }
   if (threadIdx.x == 0) {
     rs->chosen_pos = pc;
     rs->chosen_col = m;
@@ -352,9 +371,9 @@ void launch_kreduce(const double* epack, const double* H, int u, int nb, double*
 
 void launch_commit(const double* k, const int* act_cur, int* act_nxt, int u, const int* col_var,
                    int* order, int round, double* scores, RoundState* rs,
-                   const unsigned long long* err, cudaStream_t s, double* round_k) {
+                   const unsigned long long* err, cudaStream_t s, double* round_k, const double* lb, double* round_second) {
   commit_kernel<<<1, kCommitThreads, 0, s>>>(k, act_cur, act_nxt, u, col_var, order, round, scores,
-                                             rs, err, round_k);
+                                             rs, err, round_k, lb, round_second);
 }
 
 void launch_update_gram(double* C, int64_t ldc, const int* act_nxt, int ur, const RoundState* rs,

@@ -126,12 +126,15 @@ def make_full(name):
     mode, tests/test_oracle_kats.py) over the whole order of a large config."""
     X = config_input(name)
     t0 = time.time()
-    order, wk, pairs = oracle_lib.causal_order_pruned(X, workers=WORKERS)
+    order, wk, pairs, sk = oracle_lib.causal_order_pruned(X, workers=WORKERS, return_second=True)
     el = time.time() - t0
     n, d = X.shape
     with open(os.path.join(HERE, f"{name}_order_full.json"), "w") as f:
         json.dump({"config": name, "n": int(n), "d": int(d), "sha256": digest(X), "order": order,
                    "winner_k": [float(v).hex() for v in wk],
+                   # lower bound of each round's runner-up k (exact when that row was fully
+                   # evaluated): second_k - winner_k bounds the best-vs-second gap from below
+                   "second_k": [float(v).hex() for v in sk],
                    "oracle": "orc_causal_order_pruned (exact branch and bound over the faithful "
                              "pair statistics; same order and winning k as orc_causal_order)",
                    "pairs_evaluated": int(pairs), "pairs_exhaustive": int(d * (d - 1) * (d + 1) // 6),

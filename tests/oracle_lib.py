@@ -209,18 +209,21 @@ def causal_order(X, parallel: bool = False, workers: int = 1, fast: bool = False
     return (out, scores[:rounds]) if return_scores else out
 
 
-def causal_order_pruned(X, workers: int = 1):
-    """Exact pruned rounds (orc_causal_order_pruned): (order, winning k per round, pairs)."""
+def causal_order_pruned(X, workers: int = 1, return_second: bool = False):
+    """Exact pruned rounds (orc_causal_order_pruned): (order, winning k per round, pairs),
+    plus, with return_second, a lower bound of each round's runner-up k."""
     X = _mat(X)
     n, d = X.shape
     order = np.full(max(d, 1), -1, dtype=np.int32)
     wk = np.zeros(max(d - 1, 1), dtype=np.float64)
+    sk = np.zeros(max(d - 1, 1), dtype=np.float64)
     pairs = ctypes.c_int64(0)
     st = _Status()
     _check(lib().orc_causal_order_pruned(_dp(X), ctypes.c_int64(n), ctypes.c_int32(d), ctypes.c_int64(max(n, 1)),
-                                         ctypes.c_int32(workers), _ip(order), _dp(wk), ctypes.byref(pairs),
+                                         ctypes.c_int32(workers), _ip(order), _dp(wk), _dp(sk), ctypes.byref(pairs),
                                          ctypes.byref(st)), st)
-    return [int(v) for v in order[:d]], wk[: max(d - 1, 0)], pairs.value
+    out = ([int(v) for v in order[:d]], wk[: max(d - 1, 0)], pairs.value)
+    return out + (sk[: max(d - 1, 0)],) if return_second else out
 
 
 def fit_weights(X, order):
@@ -232,4 +235,38 @@ def fit_weights(X, order):
     st = _Status()
     _check(lib().orc_fit_weights(_dp(X), ctypes.c_int64(n), ctypes.c_int32(d), ctypes.c_int64(n), _ip(o), _dp(B),
                                  ctypes.byref(pinv), ctypes.byref(st)), st)
+    return B, bool(pinv.value)
+
+
+def fit_weights_prefix(X, order, workers: int | None = None):
+    """Weights from one prefix QR of the order-permuted centred design (the large-d
+    reference; cross-checked against the per-target column-pivoted QR of fit_weights).
+    Returns (B, used_pinv, n_dependent)."""
+    X = _mat(X)
+    n, d = X.shape
+    o = np.ascontiguousarray(order, dtype=np.int32)
+    B = np.zeros((d, d), dtype=np.float64, order="F")
+    pinv = ctypes.c_int32(0)
+    ndep = ctypes.c_int32(0)
+    st = _Status()
+    w = workers if workers is not None else (os.cpu_count() or 1)
+    _check(lib().orc_fit_weights_prefix(_dp(X), ctypes.c_int64(n), ctypes.c_int32(d), ctypes.c_int64(n), _ip(o),
+                                        ctypes.c_int32(w), _dp(B), ctypes.byref(pinv), ctypes.byref(ndep),
+                                        ctypes.byref(st)), st)
+    return B, bool(pinv.value), int(ndep.value)
+
+
+def fit_weights_targets(X, order, positions):
+    """Per-target column-pivoted QR (the faithful route) for the targets at the given order
+    positions only; B rows of the other targets are zero."""
+    X = _mat(X)
+    n, d = X.shape
+    o = np.ascontiguousarray(order, dtype=np.int32)
+    pos = np.ascontiguousarray(positions, dtype=np.int32)
+    B = np.zeros((d, d), dtype=np.float64, order="F")
+    pinv = ctypes.c_int32(0)
+    st = _Status()
+    _check(lib().orc_fit_weights_targets(_dp(X), ctypes.c_int64(n), ctypes.c_int32(d), ctypes.c_int64(n), _ip(o),
+                                         _ip(pos), ctypes.c_int32(len(pos)), _dp(B), ctypes.byref(pinv),
+                                         ctypes.byref(st)), st)
     return B, bool(pinv.value)

@@ -425,3 +425,45 @@ def test_pruned_oracle_matches_faithful(plg, oracle, d, n, seed, kind):
     assert order_p == order
     assert np.array_equal(wk, np.array([-scores[r][order[r]] for r in range(d - 1)]))
     assert 0 < pairs < d * (d - 1) * (d + 1) // 6
+
+
+def _deficient_design(d, n, seed):
+    """Exact linear dependencies x_3 = x_1 + x_2 and x_(d-2) = 2 x_4 - x_5 + x_1, placed
+    late in a random order."""
+    rng = np.random.default_rng(seed)
+    X = rng.laplace(size=(n, d))
+    X[:, 3] = X[:, 1] + X[:, 2]
+    X[:, d - 2] = 2.0 * X[:, 4] - X[:, 5] + X[:, 1]
+    order = [int(v) for v in rng.permutation(d)]
+    for v in (3, d - 2):
+        order.remove(v)
+    order = order[: d // 2] + [3] + order[d // 2:] + [d - 2]
+    return np.asfortranarray(X), order
+
+
+def test_prefix_qr_oracle_matches_per_target(oracle):
+    """The large-d weights reference (one prefix QR of the order-permuted centred design,
+    echelon rank handling + minimum-norm correction) against the faithful per-target
+    column-pivoted QR / COD restatement of direct_lingam.cpp:46-70, at d <= 200, full rank,
+    n < d and rank deficient."""
+    rng = np.random.default_rng(11)
+    for n, d in [(500, 20), (1500, 200), (50, 80)]:
+        X = np.asfortranarray(rng.laplace(size=(n, d)) @ np.triu(rng.normal(size=(d, d)) * (rng.random((d, d)) < 0.1))
+                              + rng.laplace(size=(n, d)))
+        order = [int(v) for v in rng.permutation(d)]
+        B1, p1 = oracle.fit_weights(X, order)
+        B2, p2, _ = oracle.fit_weights_prefix(X, order)
+        assert p1 == p2
+        assert np.max(np.abs(B1 - B2) / np.maximum(1.0, np.abs(B1))) <= 1e-9
+    for d, n, seed in [(12, 300, 1), (80, 400, 4)]:
+        X, order = _deficient_design(d, n, seed)
+        B1, p1 = oracle.fit_weights(X, order)
+        B2, p2, ndep = oracle.fit_weights_prefix(X, order)
+        assert p1 and p2 and ndep == 2
+        assert np.max(np.abs(B1 - B2) / np.maximum(1.0, np.abs(B1))) <= 1e-9
+    # targets subset == the full per-target route on those rows
+    X, order = _deficient_design(40, 300, 5)
+    B1, _ = oracle.fit_weights(X, order)
+    Bt, _ = oracle.fit_weights_targets(X, order, [5, 39])
+    for p in (5, 39):
+        assert np.array_equal(Bt[order[p]], B1[order[p]])
