@@ -125,6 +125,16 @@ int orc_fit_weights_prefix(const double* X, int64_t n, int32_t d, int64_t ld, co
                            int32_t nthreads, double* B, int32_t* used_pinv, int32_t* n_dependent,
                            orc_status* st);
 
+/* ---- benchmark inputs without the product library (simgen_oracle.c; bench.py's reference
+ * arm). Same bits as the package's generators (host/simgen.cpp). W is d x d column-major,
+ * W[v + d*j] = weight of parent j in x_v; order = causal order; X is n x d column-major.
+ * kind: 0 uniform(lo, hi), 1 Laplace(scale hi), 2 Student-t3 (scale hi). */
+int orc_gen_two_level_dag(int32_t d, uint64_t seed, double edge_prob, double* W, int32_t* order);
+int orc_gen_sparse_dag(int32_t d, double avg_parents, uint64_t seed, double wmin, double wmax, double* W,
+                       int32_t* order);
+int orc_sample_lingam(const double* W, const int32_t* order, int32_t d, int64_t n, uint64_t seed, int32_t kind,
+                      double lo, double hi, double* X);
+
 #ifdef __cplusplus
 }
 #endif

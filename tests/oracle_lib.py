@@ -42,7 +42,7 @@ _I = ctypes.POINTER(ctypes.c_int32)
 
 
 def build() -> str:
-    src = [os.path.join(ORACLE_DIR, f) for f in ("plingam_oracle.c", "plingam_oracle.h", "Makefile")]
+    src = [os.path.join(ORACLE_DIR, f) for f in ("plingam_oracle.c", "simgen_oracle.c", "plingam_oracle.h", "Makefile")]
     if not os.path.exists(LIB_PATH) or any(os.path.getmtime(s) > os.path.getmtime(LIB_PATH) for s in src):
         subprocess.run(["make", "-C", ORACLE_DIR], check=True, capture_output=True)
     return LIB_PATH
@@ -270,3 +270,37 @@ def fit_weights_targets(X, order, positions):
                                          _ip(pos), ctypes.c_int32(len(pos)), _dp(B), ctypes.byref(pinv),
                                          ctypes.byref(st)), st)
     return B, bool(pinv.value)
+
+
+_NOISE = {"uniform": 0, "laplace": 1, "t3": 2}
+
+
+def gen_two_level_dag(d: int, seed: int, edge_prob: float = 0.5):
+    """(W, order) as the package's gen_two_level_dag (simgen_oracle.c; no product library)."""
+    W = np.zeros((d, d), dtype=np.float64, order="F")
+    order = np.zeros(d, dtype=np.int32)
+    if lib().orc_gen_two_level_dag(ctypes.c_int32(d), ctypes.c_uint64(seed), ctypes.c_double(edge_prob), _dp(W),
+                                   _ip(order)):
+        raise ValueError("gen_two_level_dag: d must be >= 2")
+    return W, order
+
+
+def gen_sparse_dag(d: int, avg_parents: float = 2.0, seed: int = 1, wmin: float = 0.5, wmax: float = 1.5):
+    W = np.zeros((d, d), dtype=np.float64, order="F")
+    order = np.zeros(d, dtype=np.int32)
+    if lib().orc_gen_sparse_dag(ctypes.c_int32(d), ctypes.c_double(avg_parents), ctypes.c_uint64(seed),
+                                ctypes.c_double(wmin), ctypes.c_double(wmax), _dp(W), _ip(order)):
+        raise ValueError("gen_sparse_dag: d must be >= 2")
+    return W, order
+
+
+def sample_lingam(dag, n: int, seed: int, noise=(0.0, 1.0), kind: str = "uniform"):
+    W, order = dag
+    d = W.shape[0]
+    X = np.zeros((n, d), dtype=np.float64, order="F")
+    if lib().orc_sample_lingam(_dp(np.asfortranarray(W)), _ip(np.ascontiguousarray(order, dtype=np.int32)),
+                               ctypes.c_int32(d), ctypes.c_int64(n), ctypes.c_uint64(seed),
+                               ctypes.c_int32(_NOISE[kind]), ctypes.c_double(noise[0]), ctypes.c_double(noise[1]),
+                               _dp(X)):
+        raise MemoryError("sample_lingam")
+    return X

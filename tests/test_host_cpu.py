@@ -236,3 +236,24 @@ def test_sample_svar_deterministic_and_stable(plg):
     with pytest.raises(plg.Error) as e:  # explosive lag matrix trips the overflow guard
         plg.sample_svar(dag, [np.asfortranarray(np.eye(4) * 3.0)], T=2000, burn_in=0, seed=1)
     assert e.value.code == "UnstableSystem"
+
+
+def test_oracle_generators_match_package(plg):
+    """bench.py's reference arm builds its inputs with the oracle's generators (no product
+    library in that process): they must be the package's generators bit for bit."""
+    import oracle_lib
+
+    for d, seed in ((7, 3), (40, 11)):
+        a = plg.gen_two_level_dag(d, seed=seed)
+        W, order = oracle_lib.gen_two_level_dag(d, seed)
+        assert np.array_equal(a.weights, W) and list(a.order) == list(order)
+        Xa = plg.sample_lingam(a, 300, seed=seed)
+        Xo = oracle_lib.sample_lingam((W, order), 300, seed)
+        assert np.array_equal(Xa, Xo)
+    for kind in ("uniform", "laplace", "t3"):
+        a = plg.gen_sparse_dag(60, avg_parents=2.0, seed=5)
+        dag = oracle_lib.gen_sparse_dag(60, 2.0, 5)
+        assert np.array_equal(a.weights, dag[0]) and list(a.order) == list(dag[1])
+        Xa = plg.sample_lingam(a, 500, seed=9, noise=(0.0, 1.0), kind=kind)
+        Xo = oracle_lib.sample_lingam(dag, 500, 9, (0.0, 1.0), kind)
+        assert np.array_equal(Xa, Xo), kind
