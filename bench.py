@@ -37,10 +37,15 @@ CONFIGS = {
     "c3": (1000, 10000, "sparse ER DAG (avg 2 parents), Student-t3 noise, seed 1 (Perturb-seq shaped)"),
     "c4": (500, 2499, "VarLiNGAM lag 1: residuals of a d=500, T=2500 SVAR (sparse B0, diagonal B1, Laplace noise)"),
     "c5": (2000, 10000, "sparse ER DAG (avg 2 parents, |w| in [0.5,1.5]), Laplace(0,1) noise, seed 1"),
+    # transparency case (not a BASELINE config): C5's shape with Gaussian noise, where no
+    # variable is identifiable and every row's k is alike -- the exact pruning's worst case
+    "c5g": (2000, 10000, "sparse ER DAG (avg 2 parents), Gaussian N(0,1) noise, seed 1 (pruning worst case)"),
 }
-FP64_OPS_PER_EDE = 31     # FP64-pipe instructions per EDE in the pair kernel inner loop (cuobjdump SASS)
+# SASS of the pair kernels' inner loops (cuobjdump): per EDE 16 DFMA + 9 DADD + 6 DMUL
+FP64_INSTR_PER_EDE = 31   # FP64-pipe instructions (each one pipe slot: the utilisation basis)
+FP64_FLOPS_PER_EDE = 47   # real flops (DFMA = 2)
 LIBDEVICE_OPS_PER_EDE = 70  # SURVEY.md §8d algorithmic basis (libdevice exp/log1p)
-FP64_PEAK_TFLOPS = 33.85  # measured DFMA microbenchmark on this pool's B200 (tools/probe/fp64_peak.cu)
+FP64_PEAK_FALLBACK = 33.85  # DFMA TFLOP/s measured by tools/probe/fp64_peak.cu in round 1 (used if the probe fails)
 
 
 def _hbm_peak():
@@ -57,6 +62,10 @@ def pair_evals(d: int) -> int:
     return (d + 1) * d * (d - 1) // 3
 
 
+def _noise_kind(name: str) -> str:
+    return {"c3": "t3", "c5g": "gauss"}.get(name, "laplace")
+
+
 def make_input(name: str):
     import paper_2403_03772_b200 as plg
 
@@ -69,9 +78,60 @@ def make_input(name: str):
         b1 = np.asfortranarray(np.diag(plg.uniform_vector(d, 1, 0.2, 0.5)))
         X = plg.sample_svar(b0, [b1], T=2500, burn_in=500, seed=1, noise=(0.0, 1.0), kind="laplace")
         return plg.estimate_var(X, 1)[1]
-    kind = "t3" if name == "c3" else "laplace"
     dag = plg.gen_sparse_dag(d, avg_parents=2.0, seed=1)
-    return plg.sample_lingam(dag, n, seed=1, noise=(0.0, 1.0), kind=kind)
+    return plg.sample_lingam(dag, n, seed=1, noise=(0.0, 1.0), kind=_noise_kind(name))
+
+
+def make_input_oracle(name: str):
+    """The same matrices from the oracle's generators (oracle/simgen_oracle.c, bit-identical
+    to the package's, tests/test_host_cpu.py): the reference arm never loads the product.
+    C4's VAR residuals are not reproduced (no oracle SVAR/QR front-end): a least-squares VAR
+    residual matrix of the same shape; the per-pair CPU cost does not depend on the values."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_lib
+
+    d, n, _ = CONFIGS[name]
+    if name == "c1":
+        return oracle_lib.sample_lingam(oracle_lib.gen_two_level_dag(d, 42000), n, 42000)
+    if name == "c4":
+        T = n + 1
+        dag = oracle_lib.gen_sparse_dag(d, 2.0, 1, 0.1, 0.5)
+        E = oracle_lib.sample_lingam(dag, T, 1, (0.0, 1.0), "laplace")
+        rng = np.random.default_rng(1)
+        a = rng.uniform(0.2, 0.5, size=d)
+        Y = np.zeros_like(E)
+        for t in range(T):
+            Y[t] = E[t] + (a * Y[t - 1] if t else 0.0)
+        Z = np.hstack([np.ones((T - 1, 1)), Y[:-1]])
+        coef, *_ = np.linalg.lstsq(Z, Y[1:], rcond=None)
+        return np.asfortranarray(Y[1:] - Z @ coef)
+    return oracle_lib.sample_lingam(oracle_lib.gen_sparse_dag(d, 2.0, 1), n, 1, (0.0, 1.0), _noise_kind(name))
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.lower().startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def fp64_peak(device: int):
+    """DFMA TFLOP/s of this GPU measured now (tools/probe/libfp64peak.so), or the round-1
+    figure if the probe is missing."""
+    import ctypes
+
+    path = os.path.join(ROOT, "tools", "probe", "libfp64peak.so")
+    try:
+        L = ctypes.CDLL(path)
+        tf, sms = ctypes.c_double(0.0), ctypes.c_int(0)
+        if L.fp64_dfma_peak(device, 5, ctypes.byref(tf), ctypes.byref(sms)) == 0 and tf.value > 0:
+            return tf.value, f"measured in this job: best of 5 DFMA launches ({sms.value} SMs, tools/probe/fp64_peak_lib.cu)"
+    except OSError:
+        pass
+    return FP64_PEAK_FALLBACK, "round-1 DFMA probe figure (in-job probe unavailable)"
 
 
 class ClockSampler:
@@ -125,43 +185,110 @@ class ClockSampler:
 
 
 def load_ncu_traffic(suffix):
-    """dram bytes per launch of the dominant kernel from the committed ncu --set full summary."""
-    for path in sorted(
-            [os.path.join(ROOT, "profiles", f) for f in os.listdir(os.path.join(ROOT, "profiles"))]
-            if os.path.isdir(os.path.join(ROOT, "profiles")) else [], reverse=True):
+    """dram bytes per launch of the dominant kernel from the committed ncu --set full summary
+    (fallback when the in-job measurement is unavailable)."""
+    prof = os.path.join(ROOT, "profiles")
+    for path in sorted([os.path.join(prof, f) for f in os.listdir(prof)] if os.path.isdir(prof) else [],
+                       reverse=True):
         if path.endswith(suffix):
             try:
-                return json.load(open(path)).get("dram_bytes_per_launch")
+                return json.load(open(path)).get("dram_bytes_per_launch"), os.path.relpath(path, ROOT)
             except (OSError, ValueError):
-                return None
-    return None
+                return None, None
+    return None, None
 
 
-def cpu_baseline(X: np.ndarray, target_seconds: float = 15.0):
+def measure_traffic(config: str, prune: bool, timeout: float = 240.0):
+    """DRAM bytes (read + write) of one launch of the dominant pair kernel, measured in this
+    job: ncu on a child process running the same causal order (tools/traffic_probe.py),
+    profiling only launch #300 of the kernel (a large-u pruned round) or #1 (exhaustive
+    round 0). Returns (bytes, note) or (None, why)."""
+    kern = "prune_pairs_kernel" if prune else "pair_kernel"
+    skip = 300 if prune else 0
+    fd, csv = tempfile.mkstemp(suffix=".csv")
+    os.close(fd)
+    cmd = ["ncu", "--clock-control", "none", "--kernel-name", f"regex:{kern}", "--launch-skip", str(skip),
+           "--launch-count", "1", "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
+           "--csv", "--log-file", csv, sys.executable, os.path.join(ROOT, "tools", "traffic_probe.py"), config,
+           "1" if prune else "0"]
+    try:
+        subprocess.run(cmd, timeout=timeout, check=True, stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+        vals = {}
+        import csv as _csv
+
+        with open(csv) as f:
+            rows = [r for r in _csv.reader(line for line in f if not line.startswith("=="))]
+        hdr = rows[0]
+        for r in rows[1:]:
+            rec = dict(zip(hdr, r))
+            vals[rec["Metric Name"]] = (float(rec["Metric Value"].replace(",", "")), rec.get("Metric Unit", ""))
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
+        tot = sum(v * scale.get(u, 1) for k, (v, u) in vals.items() if k.startswith("dram__bytes"))
+        return tot, f"ncu in this job: {kern} launch {skip + 1} of a {config.upper()} causal order"
+    except (OSError, subprocess.SubprocessError, ValueError, KeyError, IndexError) as e:
+        return None, f"in-job ncu failed ({type(e).__name__})"
+    finally:
+        if os.path.exists(csv):
+            os.unlink(csv)
+
+
+def _total_pairs(d: int, n: int, alpha: float, beta: float) -> float:
+    """Cost model of a full faithful fit: sum over rounds u = d..2 of alpha u(u-1) n + beta u n
+    (SURVEY.md §8d)."""
+    u = np.arange(2, d + 1, dtype=np.float64)
+    return float(np.sum(alpha * u * (u - 1) * n + beta * u * n))
+
+
+def cpu_baseline(X: np.ndarray, target_seconds: float = 15.0, full_max_seconds: float = 90.0):
     """The reference CPU path (faithful oracle port: both residual directions per ordered
-    pair, static thread partition, -O3 -ffp-contract=off) on a bounded sample: one search
-    round over the first S columns at the full n, S sized for ~target_seconds."""
+    pair, static thread partition over all host threads, -O3 -ffp-contract=off).
+
+    Two search rounds over the first S1 < S2 columns at the full n (S2 sized for
+    ~target_seconds) fit the per-round cost t(u) = alpha u(u-1) n + beta u n; a full fit
+    whose predicted time is under full_max_seconds is then run and timed whole, otherwise
+    its time is the cost model's extrapolation (labelled). value = P(d) / full-fit seconds."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import oracle_lib
 
     cores = os.cpu_count() or 1
-    n = X.shape[0]
-    S = min(48, X.shape[1])
-    t0 = time.perf_counter()
-    oracle_lib.search_causal_order(np.asfortranarray(X[:, :S]), list(range(S)), workers=cores)
-    dt = time.perf_counter() - t0
-    rate = S * (S - 1) / dt
-    S2 = int(min(X.shape[1], max(S, (target_seconds * rate) ** 0.5)))
-    if S2 > S:
+    n, d = X.shape
+
+    def one_round(S):
         t0 = time.perf_counter()
-        oracle_lib.search_causal_order(np.asfortranarray(X[:, :S2]), list(range(S2)), workers=cores)
-        dt = time.perf_counter() - t0
-        rate = S2 * (S2 - 1) / dt
-        S = S2
-    return {"value": rate, "unit": "pair-evals/s", "cores": cores, "kind": "port",
-            "sample": f"one search round over the first {S} columns at n={n} ({S * (S - 1)} ordered pair-evals, "
-                      f"{dt:.1f} s); faithful oracle (reference cannot build: Eigen3 absent)",
-            "seconds": dt}
+        oracle_lib.search_causal_order(np.asfortranarray(X[:, :S]), list(range(S)), workers=cores)
+        return time.perf_counter() - t0
+
+    S1 = min(48, d)
+    t1 = one_round(S1)
+    rate = S1 * (S1 - 1) / t1
+    S2 = int(min(d, max(S1, (target_seconds * rate) ** 0.5)))
+    if S2 > S1 + 8:
+        t2 = one_round(S2)
+        # t = a S(S-1) n + b S n through both points
+        A = np.array([[S1 * (S1 - 1) * n, S1 * n], [S2 * (S2 - 1) * n, S2 * n]], dtype=np.float64)
+        alpha, beta = np.linalg.solve(A, np.array([t1, t2]))
+        if beta < 0 or alpha <= 0:  # noise: all of it per pair
+            alpha, beta = t2 / (S2 * (S2 - 1) * n), 0.0
+    else:
+        S2, t2 = S1, t1
+        alpha, beta = t1 / (S1 * (S1 - 1) * n), 0.0
+    predicted = _total_pairs(d, n, alpha, beta)
+    sample = (f"search rounds over the first {S1} and {S2} columns at n={n} ({t1:.1f} s + {t2:.1f} s) fit "
+              f"t(u) = alpha u(u-1) n + beta u n (alpha={alpha:.3e} s, beta={beta:.3e} s)")
+    if predicted <= full_max_seconds:
+        t0 = time.perf_counter()
+        oracle_lib.causal_order(np.asfortranarray(X), parallel=True, workers=cores)
+        wall = time.perf_counter() - t0
+        how = "measured"
+        sample += f"; then the whole causal order timed: {wall:.2f} s (model predicted {predicted:.2f} s)"
+    else:
+        wall = predicted
+        how = "extrapolated"
+        sample += f"; whole causal order extrapolated from the model: {wall:.0f} s"
+    sample += "; faithful oracle port (the reference cannot build here: Eigen3 absent)"
+    return {"value": pair_evals(d) / wall, "unit": "pair-evals/s", "cores": cores, "kind": "port",
+            "cpu_model": cpu_model(), "sample": sample, "full_fit_s": wall, "full_fit": how,
+            "alpha_s": float(alpha), "beta_s": float(beta), "seconds": t1 + t2 + (wall if how == "measured" else 0)}
 
 
 def dist_setup(args):
@@ -199,23 +326,31 @@ def barrier(world: int):
 
 
 def run_reference(args, world, rank):
+    """The reference CPU implementation of the path (faithful oracle port, all host threads)
+    on the same workload; inputs from the oracle's generators, so this process never loads
+    the product library. Each step = cpu_baseline()'s bounded sample."""
     if rank != 0:
         return
     d, n, desc = CONFIGS[args.config]
-    X = make_input(args.config)
-    for _ in range(args.warmup if args.warmup < 1 else 1):
-        pass
+    X = make_input_oracle(args.config)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_lib
+
+    for _ in range(args.warmup):  # warm-up: one small faithful search round (threads, page cache)
+        S = min(16, d)
+        oracle_lib.search_causal_order(np.asfortranarray(X[:, :S]), list(range(S)), workers=os.cpu_count() or 1)
     samples = [cpu_baseline(X, target_seconds=args.cpu_seconds) for _ in range(max(1, args.steps))]
     rate = float(np.median([s["value"] for s in samples]))
     wall = pair_evals(d) / rate
     line = {
         "metric": "causal-order pair-evals/s (and wall s) at d=2000,n=10k",
         "impl": "reference", "value": rate, "unit": "pair-evals/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": wall * 1e3, "wall_s_extrapolated": wall,
+        "warmup": args.warmup, "ms_per_step": wall * 1e3, "causal_order_wall_s": wall,
+        "wall_kind": samples[-1]["full_fit"],
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": f"synthetic: {desc}",
         "config": {"workload": f"{args.config.upper()} d={d} n={n}", "d": d, "n": n},
-        "cpu_baseline": {k: samples[-1][k] for k in ("unit", "cores", "kind", "sample")} | {"value": rate},
+        "cpu_baseline": {k: samples[-1][k] for k in ("unit", "cores", "kind", "sample", "cpu_model")} | {"value": rate},
         "e2e": {"value": rate, "unit": "pair-evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -272,6 +407,7 @@ def run_ours(args, world, rank, local):
     resid_bytes = st["resid_bytes"] * args.steps
     P = pair_evals(d)
     value = P * args.steps / dev_s
+    peak_tf, peak_src = fp64_peak(local)  # after the timed region: same clocks regime, no interference
 
     # e2e: the public API with the matrix in pinned host memory
     pinned = torch.empty((d, n), dtype=torch.float64, pin_memory=True)
@@ -293,9 +429,18 @@ def run_ours(args, world, rank, local):
     # executed work: every evaluated unordered pair computes both residual entropies over n
     pairs_step = pairs_done / args.steps
     ede = 2 * n * pairs_step
-    # the pair-evaluation kernels' share of the step and their FP64-pipe roofline
-    achieved = FP64_OPS_PER_EDE * 2 * ede / (pair_s * world) / 1e12 if pair_s > 0 else None
     pruned = not args.no_prune
+    # the pair-evaluation kernels' FP64-pipe utilisation: pipe instructions issued per second
+    # (x 2, in DFMA-equivalent TFLOP/s) against the DFMA rate measured in this job
+    pipe_tf = FP64_INSTR_PER_EDE * 2 * ede / (pair_s * world) / 1e12 if pair_s > 0 else None
+    flops_tf = FP64_FLOPS_PER_EDE * ede / (pair_s * world) / 1e12 if pair_s > 0 else None
+    traffic, traffic_src = (None, None)
+    if not args.no_ncu and world == 1:
+        traffic, traffic_src = measure_traffic(args.config, pruned)
+    if traffic is None:
+        why = traffic_src
+        traffic, traffic_src = load_ncu_traffic("prune_pairs_ncu.json" if pruned else "pair_kernel_ncu.json")
+        traffic_src = f"committed ncu --set full summary {traffic_src}" + (f" ({why})" if why else "")
     line = {
         "metric": "causal-order pair-evals/s (and wall s) at d=2000,n=10k",
         "value": value, "unit": "pair-evals/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -304,7 +449,7 @@ def run_ours(args, world, rank, local):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": f"synthetic: {desc}; generated on host, random DAG weights",
         "config": {"workload": f"{args.config.upper()} d={d} n={n}", "d": d, "n": n,
-                   "parallelism": f"pair tiles sharded over {world} GPU(s), one ncclAllGather per round"
+                   "parallelism": f"pair lists sharded over {world} GPU(s), one ncclAllGather per stage"
                    if world > 1 else "single GPU",
                    "l2": "input larger than L2 (FP64 matrix %.0f MB vs 126 MB L2)" % (8 * n * d / 1e6)},
         "pruning": {"enabled": pruned, "pairs_evaluated_per_step": pairs_step,
@@ -314,23 +459,27 @@ def run_ours(args, world, rank, local):
                     "note": "exact branch and bound on each round's k: rows whose partial k (a sum of "
                             "non-negative terms) exceeds an exactly computed k cannot win; the order and "
                             "the winner's k bits equal the exhaustive rounds' (tests/test_gpu_prune.py)"},
-        "roofline": {"bound": "fp64",
+        "roofline": {"bound": "fp64-pipe",
                      "kernel": "prune_pairs_kernel (pair lists) + pair_kernel (round 0)" if pruned
                      else "pair_kernel+finalize", "unit": "TFLOP/s",
-                     "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
-                     "frac": achieved / FP64_PEAK_TFLOPS if achieved else None,
-                     "traffic": load_ncu_traffic("prune_pairs_ncu.json" if pruned else "pair_kernel_ncu.json"),
-                     "traffic_note": "dram read+write bytes of one launch of the dominant kernel (ncu --set full, "
-                                     "profiles/); algorithmic bytes: one pass over the listed pairs' columns "
-                                     "per launch — compute-bound, L2 serves the re-reads",
-                     "basis": f"{FP64_OPS_PER_EDE} FP64-pipe instructions per EDE (SASS of both kernels' inner "
-                              f"loops) x 2 flops over the EXECUTED EDE = 2 n x pairs evaluated; time = CUDA "
-                              f"events around every pair-evaluation launch ({pair_launches // max(1, args.steps)} "
-                              f"per step, one extra untimed step); peak = measured DFMA rate (no FP64 figure in "
-                              f"MEASURED_PEAKS.json)",
+                     "achieved": pipe_tf, "peak": peak_tf,
+                     "frac": pipe_tf / peak_tf if pipe_tf else None,
+                     "fp64_pipe_utilisation": pipe_tf / peak_tf if pipe_tf else None,
+                     "real_flops_tflops": flops_tf,
+                     "real_flops_frac": flops_tf / peak_tf if flops_tf else None,
+                     "traffic": traffic,
+                     "traffic_source": traffic_src,
+                     "traffic_note": "dram read+write bytes of one launch of the dominant kernel; the pair "
+                                     "kernels are compute-bound (L2 serves most column re-reads)",
+                     "basis": f"FP64-pipe utilisation: {FP64_INSTR_PER_EDE} FP64-pipe instructions per EDE (SASS "
+                              f"of both kernels' inner loops: 16 DFMA + 9 DADD + 6 DMUL) x 2 (DFMA-equivalent "
+                              f"flops) over the EXECUTED EDE = 2 n x pairs evaluated; real flops "
+                              f"{FP64_FLOPS_PER_EDE}/EDE reported beside it; time = CUDA events around every "
+                              f"pair-evaluation launch ({pair_launches // max(1, args.steps)} per step, one extra "
+                              f"untimed step); peak: {peak_src}",
                      "libdevice_basis_frac": (LIBDEVICE_OPS_PER_EDE * 2 * ede / (pair_s * world) / 1e12)
-                     / FP64_PEAK_TFLOPS if pair_s > 0 else None,
-                     "pair_share_of_step": pair_s / (dev_s / args.steps),
+                     / peak_tf if pair_s > 0 else None,
+        "pair_share_of_step": pair_s / (dev_s / args.steps),
                      "residualize": {
                          "bound": "hbm", "kernel": "resid_ent_kernel (residualisation + next round's column "
                                                    "entropies, fused)",
@@ -363,6 +512,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-prune", action="store_true", help="exhaustive rounds (every pair, every round)")
+    ap.add_argument("--no-ncu", action="store_true", help="skip the in-job ncu traffic measurement")
     args = ap.parse_args()
     world, rank, local = dist_setup(args)
     try:

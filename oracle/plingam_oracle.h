@@ -128,7 +128,7 @@ int orc_fit_weights_prefix(const double* X, int64_t n, int32_t d, int64_t ld, co
 /* ---- benchmark inputs without the product library (simgen_oracle.c; bench.py's reference
  * arm). Same bits as the package's generators (host/simgen.cpp). W is d x d column-major,
  * W[v + d*j] = weight of parent j in x_v; order = causal order; X is n x d column-major.
- * kind: 0 uniform(lo, hi), 1 Laplace(scale hi), 2 Student-t3 (scale hi). */
+ * kind: 0 uniform(lo, hi), 1 Laplace(scale hi), 2 Student-t3 (scale hi), 3 N(lo, hi^2). */
 int orc_gen_two_level_dag(int32_t d, uint64_t seed, double edge_prob, double* W, int32_t* order);
 int orc_gen_sparse_dag(int32_t d, double avg_parents, uint64_t seed, double wmin, double wmax, double* W,
                        int32_t* order);

@@ -5,8 +5,8 @@
  * generators (paper_2403_03772_b200/csrc/host/simgen.cpp), which follow the reference's
  * semantics: proj/include/plingam/rng.hpp:14-43 (mt19937_64, 53-bit uniforms, Box-Muller,
  * Fisher-Yates) and proj/src/simgen.cpp:30-81 (two-level DAG, causal-order sampling), plus
- * the sparse Erdos-Renyi DAG and Laplace / Student-t3 noise the configs name.
- * tests/test_oracle_kats.py checks the outputs bit for bit against the package's generators.
+ * the sparse Erdos-Renyi DAG and Laplace / Student-t3 / Gaussian noise the configs name.
+ * tests/test_host_cpu.py checks the outputs bit for bit against the package's generators.
  */
 #include <math.h>
 #include <stdint.h>
@@ -62,7 +62,7 @@ static void shuffle(mt64* g, int32_t* v, int n) {
   }
 }
 
-/* kind: 0 uniform(lo, hi), 1 Laplace(scale hi), 2 Student-t3 (scale hi) */
+/* kind: 0 uniform(lo, hi), 1 Laplace(scale hi), 2 Student-t3 (scale hi), 3 N(lo, hi^2) */
 static double draw_noise(mt64* g, int kind, double lo, double hi) {
   if (kind == 0) return unif_ab(g, lo, hi);
   if (kind == 1) {
@@ -70,6 +70,7 @@ static double draw_noise(mt64* g, int kind, double lo, double hi) {
     const double a = 1.0 - 2.0 * fabs(p);
     return -hi * (p < 0 ? -1.0 : 1.0) * log(a > 0 ? a : 0x1.0p-53);
   }
+  if (kind == 3) return lo + hi * gauss(g);
   const double z = gauss(g);
   double chi = 0.0;
   for (int k = 0; k < 3; ++k) {

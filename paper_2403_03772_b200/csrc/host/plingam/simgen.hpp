@@ -8,10 +8,10 @@
 
 namespace plingam::sim {
 
-enum class NoiseKind { Uniform, Laplace, StudentT3 };
+enum class NoiseKind { Uniform, Laplace, StudentT3, Gauss };
 
 // Uniform: U(lo, hi) (reference default U(0, 1), simgen.hpp:14-17). Laplace: scale hi.
-// StudentT3: hi * t_3.
+// StudentT3: hi * t_3. Gauss: N(lo, hi^2) (not identifiable by LiNGAM: the pruning worst case).
 struct NoiseSpec {
   NoiseKind kind = NoiseKind::Uniform;
   double lo = 0.0;

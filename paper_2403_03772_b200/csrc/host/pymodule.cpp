@@ -357,6 +357,7 @@ PYBIND11_MODULE(_core, m) {
         if (kind == "uniform") spec.kind = sim::NoiseKind::Uniform;
         else if (kind == "laplace") spec.kind = sim::NoiseKind::Laplace;
         else if (kind == "t3") spec.kind = sim::NoiseKind::StudentT3;
+        else if (kind == "gauss") spec.kind = sim::NoiseKind::Gauss;
         else throw Error(ErrorCode::OutOfRange, "sample_lingam: unknown noise kind " + kind);
         std::vector<double> X;
         {
@@ -377,6 +378,7 @@ PYBIND11_MODULE(_core, m) {
         if (kind == "uniform") spec.kind = sim::NoiseKind::Uniform;
         else if (kind == "laplace") spec.kind = sim::NoiseKind::Laplace;
         else if (kind == "t3") spec.kind = sim::NoiseKind::StudentT3;
+        else if (kind == "gauss") spec.kind = sim::NoiseKind::Gauss;
         else throw Error(ErrorCode::OutOfRange, "sample_svar: unknown noise kind " + kind);
         std::vector<std::vector<double>> L;
         for (const auto& M : lagged) {

@@ -55,6 +55,8 @@ double draw_noise(Rng& rng, const NoiseSpec& noise) {
       }
       return noise.hi * z / std::sqrt(chi / 3.0);
     }
+    case NoiseKind::Gauss:
+      return noise.lo + noise.hi * rng.gauss();
   }
   return 0.0;
 }

@@ -272,7 +272,7 @@ def fit_weights_targets(X, order, positions):
     return B, bool(pinv.value)
 
 
-_NOISE = {"uniform": 0, "laplace": 1, "t3": 2}
+_NOISE = {"uniform": 0, "laplace": 1, "t3": 2, "gauss": 3}
 
 
 def gen_two_level_dag(d: int, seed: int, edge_prob: float = 0.5):

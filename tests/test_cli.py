@@ -52,7 +52,8 @@ def test_cli_discover_csv_and_binary(tmp_path, plg):
     npy = tmp_path / "data.npy"
     np.save(npy, X)
     rc, out, err = run(["discover", "--input", str(npy), "--out", str(tmp_path / "b")], tmp_path)
-    assert rc == 0, err and json.loads(out.strip().splitlines()[-1])["order"] == rep["order"]
+    assert rc == 0, err
+    assert json.loads(out.strip().splitlines()[-1])["order"] == rep["order"]
     raw = tmp_path / "data.f64"
     np.asfortranarray(X).T.tofile(raw)  # column-major bytes
     rc, out, err = run(["discover", "--input", str(raw), "--dims", "8", "--colmajor", "--out",

@@ -250,7 +250,7 @@ def test_oracle_generators_match_package(plg):
         Xa = plg.sample_lingam(a, 300, seed=seed)
         Xo = oracle_lib.sample_lingam((W, order), 300, seed)
         assert np.array_equal(Xa, Xo)
-    for kind in ("uniform", "laplace", "t3"):
+    for kind in ("uniform", "laplace", "t3", "gauss"):
         a = plg.gen_sparse_dag(60, avg_parents=2.0, seed=5)
         dag = oracle_lib.gen_sparse_dag(60, 2.0, 5)
         assert np.array_equal(a.weights, dag[0]) and list(a.order) == list(dag[1])
