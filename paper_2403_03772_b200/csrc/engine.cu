@@ -211,6 +211,9 @@ struct plg_ctx {
 
   size_t ev_pairs = 0;  // timing intervals recorded by this call (ev[3 + 2 i], ev[4 + 2 i])
   std::vector<char> ev_kind;  // per interval: 0 pair evaluation, 1 residualisation
+  std::vector<int> ev_tag;    // per interval: round * 16 + pruned stage index (-1: exhaustive / residualisation)
+  DevBuf<int> stage_log;      // PLG_STAGE_LOG: per (round, stage) list lengths
+  int tag_round = 0, tag_stage = -1;
   std::vector<double> last_k, last_second;  // per round of the last causal_order: winner's k, runner-up's
   int64_t resid_bytes = 0;    // algorithmic HBM bytes of the residualisations of this call
 
@@ -232,8 +235,9 @@ size_t pair_timer_begin(plg_ctx* c, char kind = 0) {
   if (!c->timing || !c->detail_timing) return 0;
   const size_t i = 3 + 2 * c->ev_pairs;
   if (c->events(i + 2) != cudaSuccess) return 0;
-  if (c->ev_kind.size() <= c->ev_pairs) c->ev_kind.resize(c->ev_pairs + 1);
+  if (c->ev_kind.size() <= c->ev_pairs) c->ev_kind.resize(c->ev_pairs + 1), c->ev_tag.resize(c->ev_pairs + 1);
   c->ev_kind[c->ev_pairs] = kind;
+  c->ev_tag[c->ev_pairs] = kind == 0 && c->tag_stage >= 0 ? c->tag_round * 16 + c->tag_stage : -1;
   cudaEventRecord(c->ev[i], c->stream);
   return i;
 }
@@ -317,6 +321,9 @@ int ctx_init(plg_ctx* ctx, int device, plg_status* st) {
 int report_error(unsigned long long key, const int* /*unused*/, plg_status* st) {
   const unsigned kind = static_cast<unsigned>((key >> 32) & 0xff);
   const int col = static_cast<int>(key & 0xffffffffu) - 1;
+  if (kind == plg::kErrInternal)
+    return set_status(st, PLG_CudaError, -1, -1,
+                      "internal: a multi-rank pair-list slice exceeded its all-gather slot");
   if (kind == plg::kErrColZeroVar)
     return set_status(st, PLG_ZeroVariance, -1, col,
                       "search_causal_order: column %d has zero variance", col);
@@ -492,6 +499,7 @@ int search_round_pruned(plg_ctx* c, int64_t n, int64_t ldw, int d, int u, const 
   a.round = round;
   a.k = c->k.p;
   a.evals = c->evals.p;
+  a.stage_log = c->stage_log.p;
   int* sa = c->st0.p;
   int* sb = c->st1.p;
   a.state_in = sa;
@@ -510,6 +518,8 @@ int search_round_pruned(plg_ctx* c, int64_t n, int64_t ldw, int d, int u, const 
   a.shard_slot = 0;
   auto stage = [&](int kind, int m, double beta, int pass) -> int {
     a.stage_idx = std::min(stage_idx++, plg::kMaxPruneStages - 1);
+    c->tag_round = round;
+    c->tag_stage = a.stage_idx;
     a.state_in = sa;
     a.state_out = sb;
     cudaStream_t ss = (kind == plg::kStageProbe) ? ps : c->stream;
@@ -600,6 +610,7 @@ int search_round_pruned(plg_ctx* c, int64_t n, int64_t ldw, int d, int u, const 
     }
   }
   if (int rc = stage(plg::kStageFull, 0, 0.0, 2)) return rc;
+  c->tag_stage = -1;
   return 0;
 }
 
@@ -781,6 +792,14 @@ int causal_order_impl(plg_ctx* c, const double* dX, int64_t ldx, int64_t n, int 
   c->pairs_done = 0;
   if (prune)
     if (int rc = reserve_prune(c, n, d, st)) return rc;
+  // PLG_STAGE_LOG=<path> (analysis): per pruned stage its list length and, with detail
+  // timing on, its pair-list launch time, written after the call
+  static const char* stage_log = std::getenv("PLG_STAGE_LOG");
+  if (stage_log && prune) {
+    PLG_CUDA(c->stage_log.reserve(static_cast<size_t>(d) * plg::kMaxPruneStages));
+    PLG_CUDA(cudaMemsetAsync(c->stage_log.p, 0xff, static_cast<size_t>(d) * plg::kMaxPruneStages * sizeof(int),
+                             c->stream));
+  }
   // PLG_ROUND_TIMES=<path> (analysis): per-round device time written after the call
   static const char* round_times = std::getenv("PLG_ROUND_TIMES");
   std::vector<cudaEvent_t> rev;
@@ -857,6 +876,27 @@ int causal_order_impl(plg_ctx* c, const double* dX, int64_t ldx, int64_t n, int 
       std::fclose(f);
     }
     for (auto& e : rev) cudaEventDestroy(e);
+  }
+  if (stage_log && prune) {
+    std::vector<int> lens(static_cast<size_t>(d) * plg::kMaxPruneStages);
+    PLG_CUDA(cudaMemcpy(lens.data(), c->stage_log.p, lens.size() * sizeof(int), cudaMemcpyDeviceToHost));
+    std::vector<float> ms_of(lens.size(), -1.f);
+    for (size_t i = 0; i < c->ev_pairs && i < c->ev_tag.size(); ++i) {
+      const int t = c->ev_tag[i];
+      if (t < 0) continue;
+      const size_t slot = static_cast<size_t>(t / 16) * plg::kMaxPruneStages + t % 16;
+      float ms = 0.f;
+      if (slot < ms_of.size() && cudaEventElapsedTime(&ms, c->ev[3 + 2 * i], c->ev[4 + 2 * i]) == cudaSuccess)
+        ms_of[slot] = (ms_of[slot] < 0.f ? 0.f : ms_of[slot]) + ms;
+    }
+    if (FILE* f = std::fopen(stage_log, "w")) {
+      for (int r = 0; r < rounds; ++r)
+        for (int s = 0; s < plg::kMaxPruneStages; ++s) {
+          const size_t slot = static_cast<size_t>(r) * plg::kMaxPruneStages + s;
+          if (lens[slot] >= 0) std::fprintf(f, "%d %d %d %d %.5f\n", r, d - r, s, lens[slot], ms_of[slot]);
+        }
+      std::fclose(f);
+    }
   }
   pruned_pairs = per_stage[0];
   c->last.pairs_evaluated = c->pairs_done + static_cast<int64_t>(pruned_pairs);

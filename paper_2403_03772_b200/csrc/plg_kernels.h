@@ -36,7 +36,7 @@ constexpr int kSegMin = 256;      // smallest sample segment per CTA
 // Error key: first error in the reference's raising order (ordering.cpp build_cache
 // before candidate_score, rounds ascending). key = round<<40 | kind<<32 | (col+1).
 constexpr unsigned long long kNoError = ~0ull;
-enum ErrKind : unsigned { kErrColZeroVar = 0, kErrPairCollinear = 1 };
+enum ErrKind : unsigned { kErrColZeroVar = 0, kErrPairCollinear = 1, kErrInternal = 255 };
 
 __host__ __device__ inline unsigned long long err_key(int round, unsigned kind, int col) {
   return (static_cast<unsigned long long>(round) << 40) |
@@ -201,6 +201,7 @@ struct PruneArgs {
   int shard_world;              // > 0: slice of this rank planned on the device from the list length
   int shard_rank;
   int shard_slot;               // entries per rank slot in res
+  int* stage_log;               // analysis (PLG_STAGE_LOG): [round][kMaxPruneStages] list lengths, or null
 };
 enum PruneStage : int { kStageProbe = 0, kStageRefine = 1, kStageFull = 2 };
 void launch_prune_predict(const PruneArgs& a, cudaStream_t s);

@@ -655,6 +655,7 @@ __global__ void __launch_bounds__(1024) prune_scan_kernel(const PruneArgs a) {
     a.off[a.u] = s_carry;
     atomicAdd(a.evals, static_cast<unsigned long long>(s_carry));
     atomicAdd(a.evals + 1 + a.stage_idx, static_cast<unsigned long long>(s_carry));
+    if (a.stage_log) a.stage_log[a.round * kMaxPruneStages + a.stage_idx] = s_carry;
   }
   for (int b = threadIdx.x; b <= s_carry / a.batch; b += blockDim.x) a.work[b] = 0;  // fetch counters
   if (threadIdx.x == 0) *a.alive = 0;  // the next stage's surviving-row list starts empty
@@ -845,6 +846,10 @@ __global__ void __launch_bounds__(kListThreads, 2) prune_pairs_kernel(const Prun
     const int cnt = (tot + a.shard_world - 1) / a.shard_world;
     kb = min(tot, a.shard_rank * cnt);
     ke = min(tot, (a.shard_rank + 1) * cnt);
+    if (cnt > a.shard_slot) {  // the host-side slot bound broke: ranks would overwrite each other's slots
+      if (blockIdx.x == 0 && threadIdx.x == 0) atomicMin(a.err, err_key(0, kErrInternal, -1));
+      ke = kb;
+    }
   }
   const int total = ke - kb;
   const int nbatch = (total + a.batch - 1) / a.batch;

@@ -165,3 +165,37 @@ def test_pruned_rounds_multi_batch_lists():
     r = _run(260, 3001, 11, "t3", tileseg=True, batch=256)
     assert r["prune"]["order"] == r["full"]["order"]
     assert r["prune"]["k"] == r["full"]["k"]
+
+
+_GOLDEN_CHILD = r"""
+import json, sys
+sys.path.insert(0, %r)
+sys.path.insert(0, %r)
+import numpy as np
+import bench
+import paper_2403_03772_b200 as plg
+X = np.asfortranarray(bench.make_input("c3"))
+eng = plg.Engine(0)
+order = eng.causal_order(X)
+print(json.dumps({"order": order, "k": [float(v).hex() for v in eng.round_k()],
+                  "pairs": eng.stats()["pairs_evaluated"]}))
+"""
+
+
+@pytest.mark.parametrize("world", [3, 8])
+def test_sharded_schedule_matches_oracle_golden(world):
+    # The multi-rank pruned schedule (slices, fixed-slot gathers, prune_scatter_kernel)
+    # against the CPU oracle itself: BASELINE configs[2] (C3, d = 1000), whole order and
+    # every round's winning k within the score bar.
+    path = os.path.join(ROOT, "tests", "golden", "c3_order_full.json")
+    with open(path) as f:
+        fx = json.load(f)
+    env = dict(os.environ, PLG_EMULATE_WORLD=str(world))
+    env.pop("PLG_PRUNE", None)
+    out = subprocess.run([sys.executable, "-c", _GOLDEN_CHILD % (ROOT, os.path.join(ROOT, "tests"))], env=env,
+                         capture_output=True, text=True, check=True, timeout=900)
+    r = json.loads(out.stdout.strip().splitlines()[-1])
+    assert r["order"] == fx["order"]
+    k = np.array([float.fromhex(v) for v in r["k"]])
+    k_ref = np.array([float.fromhex(v) for v in fx["winner_k"]])
+    assert np.all(np.abs(k - k_ref) <= 1e-9 * np.abs(k_ref) + 1e-15)
