@@ -209,6 +209,16 @@ struct plg_ctx {
   DevBuf<double> qd;  // QR weight step / VAR: thresholds, norms, tau, T, trailing scratch, coefficients
   DevBuf<int> qi;     // QR: qstate, rbefore, rowcol, dep, pinfo, dependent lists
 
+  // CUDA graph of the round loop (run_rounds_graph); PLG_GRAPHS=0 disables
+  bool use_graphs = true;
+  struct GraphCache {
+    std::vector<const void*> key;
+    std::vector<double> knobs;
+    cudaGraphExec_t exec = nullptr;
+    int64_t launches = 0, pairs_done = 0, resid_bytes = 0;
+    bool gram_ready = false;
+  } graph;
+
   size_t ev_pairs = 0;  // timing intervals recorded by this call (ev[3 + 2 i], ev[4 + 2 i])
   std::vector<char> ev_kind;  // per interval: 0 pair evaluation, 1 residualisation
   std::vector<int> ev_tag;    // per interval: round * 16 + pruned stage index (-1: exhaustive / residualisation)
@@ -300,6 +310,7 @@ void parse_prune_env(plg_ctx* ctx) {
   if (const char* v = std::getenv("PLG_PRUNE_SUB")) ctx->prune_sub = std::max<int64_t>(0, std::atoll(v));
   if (const char* v = std::getenv("PLG_PRUNE_MIN_U")) ctx->prune_min_u = std::max(8, std::atoi(v));
   if (const char* v = std::getenv("PLG_PRUNE_BATCH")) ctx->prune_batch = std::max(64, std::atoi(v) / 32 * 32);
+  if (const char* v = std::getenv("PLG_GRAPHS")) ctx->use_graphs = std::atoi(v) != 0;
 }
 
 int ctx_init(plg_ctx* ctx, int device, plg_status* st) {
@@ -770,6 +781,66 @@ int call_round_hook(plg_ctx* c, int u, int round, const int* act_cur, plg_status
   return 0;
 }
 
+// Graph replay of the round loop (causal_order_impl). Key: the shape, the engine knobs that
+// shape the launch sequence, and every buffer address the launches bake in. The first call of
+// a key runs the loop directly; the second captures it (stream capture of the main stream;
+// the side stream joins through its events) and replays it; later calls only replay.
+template <class Loop>
+int run_rounds_graph(plg_ctx* c, int d, int64_t n, int rounds, bool prune, Loop&& run_loop, plg_status* st) {
+  std::vector<const void*> key = {c->W.p, c->C.p, c->part.p, c->epack.p, c->H.p, c->k.p, c->rk.p, c->rsec.p,
+                                  c->hpart.p, c->act0.p, c->act1.p, c->colvar.p, c->order.p, c->nz.p, c->rs.p,
+                                  c->err.p, c->Md.p, c->KN.p, c->pk.p, c->L.p, c->ppart.p, c->st0.p, c->st1.p,
+                                  c->rowsel.p, c->off.p, c->pwork.p, c->pdone.p, c->crow.p, c->cand.p, c->alive.p, c->kstar.p,
+                                  c->evals.p, c->g_exp, c->g_log};
+  std::vector<double> knobs = {static_cast<double>(d), static_cast<double>(n), static_cast<double>(rounds),
+                               prune ? 1.0 : 0.0, static_cast<double>(c->prune_R), static_cast<double>(c->prune_T),
+                               c->prune_beta, static_cast<double>(c->prune_sub), static_cast<double>(c->prune_min_u),
+                               static_cast<double>(c->prune_batch), c->prune_tile_seg ? 1.0 : 0.0};
+  for (double f : c->prune_fracs) knobs.push_back(f);
+  plg_ctx::GraphCache& g = c->graph;
+  const bool same = g.key == key && g.knobs == knobs;
+  if (same && g.exec) {
+    PLG_CUDA(cudaGraphLaunch(g.exec, c->stream));
+    c->launches += g.launches;
+    c->pairs_done += g.pairs_done;
+    c->resid_bytes += g.resid_bytes;
+    c->gram_ready = g.gram_ready;
+    return 0;
+  }
+  if (!same) {  // a new key: run directly, capture on the next call with this key
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    g = plg_ctx::GraphCache{};
+    g.key = key;
+    g.knobs = knobs;
+    return run_loop();
+  }
+  const int64_t l0 = c->launches, p0 = c->pairs_done, b0 = c->resid_bytes;
+  PLG_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  const bool gr0 = c->gram_ready;
+  const int rc = run_loop();
+  cudaGraph_t graph = nullptr;
+  const cudaError_t ec = cudaStreamEndCapture(c->stream, &graph);
+  cudaGraphExec_t exec = nullptr;
+  cudaError_t ei = rc ? cudaErrorStreamCaptureInvalidated : ec;
+  if (ei == cudaSuccess) ei = cudaGraphInstantiate(&exec, graph, 0);
+  if (graph) cudaGraphDestroy(graph);
+  if (ei != cudaSuccess) {  // a launch the capture does not support: run directly from now on
+    cudaGetLastError();
+    c->launches = l0, c->pairs_done = p0, c->resid_bytes = b0;
+    c->gram_ready = gr0;
+    c->use_graphs = false;
+    ok(st);
+    return run_loop();
+  }
+  g.exec = exec;
+  g.launches = c->launches - l0;
+  g.pairs_done = c->pairs_done - p0;
+  g.resid_bytes = c->resid_bytes - b0;
+  g.gram_ready = c->gram_ready;
+  PLG_CUDA(cudaGraphLaunch(g.exec, c->stream));
+  return 0;
+}
+
 // The recursive loop (ordering.cpp:213-244) on device-resident X.
 int causal_order_impl(plg_ctx* c, const double* dX, int64_t ldx, int64_t n, int d, int max_rounds,
                       int32_t* order_out, bool host_in, plg_status* st) {
@@ -807,6 +878,7 @@ int causal_order_impl(plg_ctx* c, const double* dX, int64_t ldx, int64_t n, int 
     rev.resize(static_cast<size_t>(rounds) + 1);
     for (auto& e : rev) cudaEventCreate(&e);
   }
+  auto run_loop = [&]() -> int {
   for (int r = 0; r < rounds; ++r) {
     if (!rev.empty()) cudaEventRecord(rev[r], c->stream);
     const int u = d - r;
@@ -848,6 +920,18 @@ int causal_order_impl(plg_ctx* c, const double* dX, int64_t ldx, int64_t n, int 
       c->resid_bytes += (2 * static_cast<int64_t>(u - 1) + 1) * n * static_cast<int64_t>(sizeof(double));
       c->launches += 2;
     }
+  }
+  return 0;
+  };
+  // The round loop's launch sequence is a pure function of (d, n, knobs): on a single-rank
+  // context without per-launch instrumentation it is captured once into a CUDA graph and
+  // replayed by later calls of the same shape (~20 launches per round, ~40 000 per C5 fit).
+  const bool graphable = c->use_graphs && c->world == 1 && !c->force_nccl && c->emulate_world == 1 && !c->hook &&
+                         !c->detail_timing && rev.empty() && !stage_log;
+  if (graphable) {
+    if (int rc = run_rounds_graph(c, d, n, rounds, prune, run_loop, st)) return rc;
+  } else if (int rc = run_loop()) {
+    return rc;
   }
   if (!rev.empty()) cudaEventRecord(rev[rounds], c->stream);
   if (c->timing) cudaEventRecord(c->ev[1], c->stream);
@@ -1027,6 +1111,7 @@ void plg_ctx_destroy(plg_ctx* c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->comm && nccl().loaded) nccl().CommDestroy(c->comm);
+  if (c->graph.exec) cudaGraphExecDestroy(c->graph.exec);
   for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
   c->Xd.release();
   c->W.release();
