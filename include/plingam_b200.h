@@ -90,6 +90,21 @@ int plg_ctx_create(int32_t device, plg_ctx** out, plg_status* st);
 int plg_nccl_unique_id(void* out_128_bytes, plg_status* st);
 int plg_ctx_create_dist(int32_t device, int32_t rank, int32_t world, const void* nccl_uid_128,
                         plg_ctx** out, plg_status* st);
+
+/* Multi-GPU through peer memory (no collective library): one process per GPU. Each rank
+ * creates its context with the same world size and max_dims (largest d it will be called
+ * with: sizes the exchange arena, 2 x (d^2 + d) + 2 x round-0 tile table doubles), exports the
+ * 64-byte CUDA IPC handle of its arena with plg_p2p_handle, the caller gathers the handles of
+ * all ranks in rank order (any host channel: torch.distributed, MPI, a file) and every rank
+ * calls plg_p2p_connect with the world x 64 bytes. Every exchange is then a store of each
+ * produced value into every rank's arena (NVLink) plus a device-side flag barrier: no host
+ * synchronisation inside a call. world = 1 runs every exchange through its own arena (a
+ * self-test of the exchange path). Calls must be made collectively by all ranks with the
+ * same inputs, as for plg_ctx_create_dist. At most 8 ranks. */
+int plg_ctx_create_p2p(int32_t device, int32_t rank, int32_t world, int32_t max_dims, plg_ctx** out,
+                       plg_status* st);
+int plg_p2p_handle(plg_ctx* ctx, void* out_64_bytes, plg_status* st);
+int plg_p2p_connect(plg_ctx* ctx, const void* handles_world_x_64_bytes, plg_status* st);
 void plg_ctx_destroy(plg_ctx* ctx);
 
 /* plingam::causal_order(X, parallel, workers) — ordering.hpp:42, ordering.cpp:213-244.

@@ -209,6 +209,28 @@ struct plg_ctx {
   DevBuf<double> qd;  // QR weight step / VAR: thresholds, norms, tau, T, trailing scratch, coefficients
   DevBuf<int> qi;     // QR: qstate, rbefore, rowcol, dep, pinfo, dependent lists
 
+  // peer-memory exchange (plg_ctx_create_p2p): this rank's arena, every rank's mapping of it
+  bool p2p = false;
+  bool p2p_connected = false;
+  char* arena = nullptr;
+  size_t arena_bytes = 0;
+  int p2p_max_dims = 0;
+  int64_t off_pres[2] = {0, 0}, off_epack[2] = {0, 0};
+  size_t pres_cap = 0, epack_cap = 0;  // doubles per parity
+  char* peer_base[plg::kMaxPeers] = {};
+  int xchg = 0;  // exchanges of the current call (buffer parity xchg & 1)
+  plg::PeerTable peers() const {
+    plg::PeerTable t;
+    t.n = world;
+    t.rank = rank;
+    for (int r = 0; r < world && r < plg::kMaxPeers; ++r) t.base[r] = peer_base[r];
+    return t;
+  }
+  double* arena_doubles(int64_t off) const { return reinterpret_cast<double*>(arena + off); }
+  unsigned long long* arena_errs(int parity) const {
+    return reinterpret_cast<unsigned long long*>(arena + plg::kArenaErrs) + parity * plg::kMaxPeers;
+  }
+
   // CUDA graph of the round loop (run_rounds_graph); PLG_GRAPHS=0 disables
   bool use_graphs = true;
   struct GraphCache {
@@ -420,6 +442,12 @@ int search_round(plg_ctx* c, int64_t n, int64_t ldw, int ldc, int u, const int* 
   a.g_log = c->g_log;
   a.err = c->err.p;
   a.round = round;
+  const bool p2p_xchg = c->p2p && !rp.replicated;
+  const int parity = c->xchg & 1;
+  if (p2p_xchg) {  // the tiles go straight into every rank's copy of the table (peer memory)
+    a.epack = c->arena_doubles(c->off_epack[parity]);
+    a.peers = c->peers();
+  }
   const size_t tm = pair_timer_begin(c);
   if (rp.replicated) {
     plg::launch_pair_small(a, c->stream);
@@ -431,7 +459,18 @@ int search_round(plg_ctx* c, int64_t n, int64_t ldw, int ldc, int u, const int* 
     c->launches += 2;
   }
   pair_timer_end(c, tm);
-  const bool exchange = (c->world > 1 || c->force_nccl) && !rp.replicated;
+  const bool exchange = (c->world > 1 || c->force_nccl) && !rp.replicated && !c->p2p;
+  if (p2p_xchg) {
+    plg::launch_p2p_signal(a.peers, c->err.p, plg::kArenaErrs + parity * plg::kMaxPeers * 8, c->stream);
+    plg::launch_p2p_wait(a.peers, c->stream);
+    c->launches += 2;
+    ++c->xchg;
+    plg::launch_kreduce(a.epack, c->H.p, u, rp.nb, c->k.p, c->err.p, c->arena_errs(parity), c->world, act_cur, KN,
+                        ldc, c->stream);
+    ++c->launches;
+    c->pairs_done += static_cast<int64_t>(u) * (u - 1) / 2;
+    return 0;
+  }
   if (exchange) {
     // One grouped exchange per round: the entropy tiles (in place, rank slots of tpr tiles)
     // and every rank's error key.
@@ -520,6 +559,7 @@ int search_round_pruned(plg_ctx* c, int64_t n, int64_t ldw, int d, int u, const 
   c->launches += 2;
   int stage_idx = 0;
   const int shards = c->world > 1 ? c->world : c->emulate_world;
+  if (c->p2p) a.peers = c->peers();
   a.k_begin = 0;
   a.k_end = -1;
   a.res = nullptr;
@@ -541,7 +581,27 @@ int search_round_pruned(plg_ctx* c, int64_t n, int64_t ldw, int d, int u, const 
       PLG_CUDA(cudaEventRecord(c->ev_side, ss));
       PLG_CUDA(cudaStreamWaitEvent(c->stream, c->ev_side, 0));
     }
-    if (shards == 1 && !c->force_nccl) {
+    if (c->p2p) {
+      // Peer memory: rank r evaluates its device-planned slice of the (identical) list and
+      // stores entry k's M at res[k] of every rank; one signal/wait, then the local scatter.
+      // No slot bound, no host synchronisation, no collective.
+      const int parity = c->xchg & 1;
+      a.res = c->arena_doubles(c->off_pres[parity]);
+      a.shard_world = c->world;
+      a.shard_rank = c->rank;
+      a.shard_slot = INT32_MAX;
+      a.res_base = 0;
+      const size_t tm = pair_timer_begin(c);
+      PLG_CUDA(plg::launch_prune_pairs(a, c->stream));
+      pair_timer_end(c, tm);
+      plg::launch_p2p_signal(a.peers, c->err.p, -1, c->stream);
+      plg::launch_p2p_wait(a.peers, c->stream);
+      ++c->xchg;
+      plg::launch_prune_scatter(a, 1, 1, c->stream);  // res[k] = entry k
+      c->launches += 4;
+      a.res = nullptr;
+      a.shard_world = 0;
+    } else if (shards == 1 && !c->force_nccl) {
       const size_t tm = pair_timer_begin(c);
       PLG_CUDA(plg::launch_prune_pairs(a, c->stream));
       pair_timer_end(c, tm);
@@ -683,7 +743,7 @@ int reserve_prune(plg_ctx* c, int64_t n, int d, plg_status* st) {
   PLG_CUDA(c->cand.reserve(static_cast<size_t>(d) * 8));
   PLG_CUDA(c->alive.reserve(static_cast<size_t>(d) + 1));
   PLG_CUDA(cudaMemsetAsync(c->alive.p, 0, sizeof(int), c->stream));
-  if (c->world > 1 || c->emulate_world > 1 || c->force_nccl) PLG_CUDA(c->pres.reserve(max_list + 64));
+  if ((c->world > 1 && !c->p2p) || c->emulate_world > 1 || c->force_nccl) PLG_CUDA(c->pres.reserve(max_list + 64));
   PLG_CUDA(cudaMemsetAsync(c->pdone.p, 0, (c->prune_batch / 32) * sizeof(int), c->stream));
   PLG_CUDA(cudaMemsetAsync(c->evals.p, 0, (1 + plg::kMaxPruneStages) * sizeof(unsigned long long), c->stream));
   return 0;
@@ -781,6 +841,27 @@ int call_round_hook(plg_ctx* c, int u, int round, const int* act_cur, plg_status
   return 0;
 }
 
+// Peer-memory contexts: the arena was sized for at most p2p_max_dims variables.
+int p2p_check_dims(plg_ctx* c, int d, plg_status* st) {
+  if (!c->p2p) return 0;
+  if (!c->p2p_connected) return set_status(st, PLG_OutOfRange, -1, -1, "peer-memory context not connected");
+  if (d > c->p2p_max_dims)
+    return set_status(st, PLG_OutOfRange, -1, -1, "%d variables exceed the exchange arena (max_dims %d)", d,
+                      c->p2p_max_dims);
+  c->xchg = 0;
+  return 0;
+}
+
+// End of a call on a peer-memory context: no rank may start the next call's stores into a
+// peer's buffers before that peer has finished reading this call's last exchange.
+void p2p_end_barrier(plg_ctx* c) {
+  if (!c->p2p) return;
+  const plg::PeerTable t = c->peers();
+  plg::launch_p2p_signal(t, c->err.p, -1, c->stream);
+  plg::launch_p2p_wait(t, c->stream);
+  c->launches += 2;
+}
+
 // Graph replay of the round loop (causal_order_impl). Key: the shape, the engine knobs that
 // shape the launch sequence, and every buffer address the launches bake in. The first call of
 // a key runs the loop directly; the second captures it (stream capture of the main stream;
@@ -795,7 +876,9 @@ int run_rounds_graph(plg_ctx* c, int d, int64_t n, int rounds, bool prune, Loop&
   std::vector<double> knobs = {static_cast<double>(d), static_cast<double>(n), static_cast<double>(rounds),
                                prune ? 1.0 : 0.0, static_cast<double>(c->prune_R), static_cast<double>(c->prune_T),
                                c->prune_beta, static_cast<double>(c->prune_sub), static_cast<double>(c->prune_min_u),
-                               static_cast<double>(c->prune_batch), c->prune_tile_seg ? 1.0 : 0.0};
+                               static_cast<double>(c->prune_batch), c->prune_tile_seg ? 1.0 : 0.0,
+                               c->p2p ? 1.0 : 0.0, static_cast<double>(c->world), static_cast<double>(c->rank)};
+  key.push_back(c->arena);
   for (double f : c->prune_fracs) knobs.push_back(f);
   plg_ctx::GraphCache& g = c->graph;
   const bool same = g.key == key && g.knobs == knobs;
@@ -844,6 +927,7 @@ int run_rounds_graph(plg_ctx* c, int d, int64_t n, int rounds, bool prune, Loop&
 // The recursive loop (ordering.cpp:213-244) on device-resident X.
 int causal_order_impl(plg_ctx* c, const double* dX, int64_t ldx, int64_t n, int d, int max_rounds,
                       int32_t* order_out, bool host_in, plg_status* st) {
+  if (int rc = p2p_check_dims(c, d, st)) return rc;
   const int64_t ldw = round_up(std::max<int64_t>(n, 2), 16);
   if (int rc = reserve_run(c, n, d, ldw, st)) return rc;
   if (int rc = standardize_validate(c, dX, ldx, n, d, nullptr, nullptr, ldw, true, st)) return rc;
@@ -921,13 +1005,14 @@ int causal_order_impl(plg_ctx* c, const double* dX, int64_t ldx, int64_t n, int 
       c->launches += 2;
     }
   }
+  p2p_end_barrier(c);
   return 0;
   };
   // The round loop's launch sequence is a pure function of (d, n, knobs): on a single-rank
   // context without per-launch instrumentation it is captured once into a CUDA graph and
   // replayed by later calls of the same shape (~20 launches per round, ~40 000 per C5 fit).
-  const bool graphable = c->use_graphs && c->world == 1 && !c->force_nccl && c->emulate_world == 1 && !c->hook &&
-                         !c->detail_timing && rev.empty() && !stage_log;
+  const bool graphable = c->use_graphs && (c->world == 1 || c->p2p) && !c->force_nccl && c->emulate_world == 1 &&
+                         !c->hook && !c->detail_timing && rev.empty() && !stage_log;
   if (graphable) {
     if (int rc = run_rounds_graph(c, d, n, rounds, prune, run_loop, st)) return rc;
   } else if (int rc = run_loop()) {
@@ -1103,6 +1188,74 @@ int plg_ctx_create_dist(int32_t device, int32_t rank, int32_t world, const void*
   return ok(st);
 }
 
+int plg_ctx_create_p2p(int32_t device, int32_t rank, int32_t world, int32_t max_dims, plg_ctx** out,
+                       plg_status* st) {
+  if (!out) return set_status(st, PLG_OutOfRange, -1, -1, "null output pointer");
+  *out = nullptr;
+  if (world < 1 || world > plg::kMaxPeers || rank < 0 || rank >= world)
+    return set_status(st, PLG_OutOfRange, -1, -1, "invalid rank %d / world %d (1..%d ranks)", rank, world,
+                      plg::kMaxPeers);
+  if (max_dims < 2) return set_status(st, PLG_OutOfRange, -1, -1, "max_dims must be >= 2");
+  plg_ctx* c = new plg_ctx();
+  int rc = ctx_init(c, device, st);
+  if (!rc) {
+    c->rank = rank;
+    c->world = world;
+    c->p2p = true;
+    c->p2p_max_dims = max_dims;
+    // pres: one stage list (u (u - 1) entries + slack); epack: every tile of round 0 at the
+    // widest rank split (ceil(tiles / world) per rank)
+    const size_t dd = static_cast<size_t>(max_dims);
+    c->pres_cap = dd * dd + dd + 64;
+    const size_t nb = (dd + kBT - 1) / kBT, ntiles = nb * (nb + 1) / 2;
+    c->epack_cap = (ntiles + world - 1) / world * world * 2 * kTilePairs;
+    c->off_pres[0] = plg::kArenaData;
+    c->off_pres[1] = c->off_pres[0] + static_cast<int64_t>(c->pres_cap * sizeof(double));
+    c->off_epack[0] = c->off_pres[1] + static_cast<int64_t>(c->pres_cap * sizeof(double));
+    c->off_epack[1] = c->off_epack[0] + static_cast<int64_t>(c->epack_cap * sizeof(double));
+    c->arena_bytes = static_cast<size_t>(c->off_epack[1]) + c->epack_cap * sizeof(double);
+    cudaError_t e = cudaMalloc(&c->arena, c->arena_bytes);
+    if (e == cudaSuccess) e = cudaMemset(c->arena, 0, plg::kArenaData);  // flags and error slots
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) rc = set_status(st, PLG_CudaError, -1, -1, "exchange arena: %s", cudaGetErrorString(e));
+    c->peer_base[rank] = c->arena;
+    c->p2p_connected = (world == 1);
+  }
+  if (rc) {
+    plg_ctx_destroy(c);
+    return rc;
+  }
+  *out = c;
+  return ok(st);
+}
+
+int plg_p2p_handle(plg_ctx* c, void* out_64_bytes, plg_status* st) {
+  if (!c || !c->p2p) return set_status(st, PLG_OutOfRange, -1, -1, "not a peer-memory context");
+  PLG_CUDA(cudaSetDevice(c->device));
+  cudaIpcMemHandle_t h;
+  PLG_CUDA(cudaIpcGetMemHandle(&h, c->arena));
+  memcpy(out_64_bytes, &h, sizeof(h));
+  return ok(st);
+}
+
+int plg_p2p_connect(plg_ctx* c, const void* handles, plg_status* st) {
+  if (!c || !c->p2p) return set_status(st, PLG_OutOfRange, -1, -1, "not a peer-memory context");
+  std::lock_guard<std::mutex> lock_(c->mu);
+  PLG_CUDA(cudaSetDevice(c->device));
+  if (c->p2p_connected) return ok(st);
+  const unsigned char* hb = static_cast<const unsigned char*>(handles);
+  for (int r = 0; r < c->world; ++r) {
+    if (r == c->rank) continue;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, hb + static_cast<size_t>(r) * sizeof(h), sizeof(h));
+    void* p = nullptr;
+    PLG_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    c->peer_base[r] = static_cast<char*>(p);
+  }
+  c->p2p_connected = true;
+  return ok(st);
+}
+
 void plg_ctx_destroy(plg_ctx* c) {
   if (c) {  // wait for an in-flight call on this context
     std::lock_guard<std::mutex> lock_(c->mu);
@@ -1112,6 +1265,11 @@ void plg_ctx_destroy(plg_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->comm && nccl().loaded) nccl().CommDestroy(c->comm);
   if (c->graph.exec) cudaGraphExecDestroy(c->graph.exec);
+  if (c->p2p) {
+    for (int r = 0; r < c->world && r < plg::kMaxPeers; ++r)
+      if (r != c->rank && c->peer_base[r]) cudaIpcCloseMemHandle(c->peer_base[r]);
+    if (c->arena) cudaFree(c->arena);
+  }
   for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
   c->Xd.release();
   c->W.release();
@@ -1184,6 +1342,7 @@ int plg_search(plg_ctx* c, const double* X, int64_t n, int32_t d, int64_t ld, co
   if (n < 2) return set_status(st, PLG_TooShort, -1, -1, "standardize: need at least 2 samples");
   if (ld < n) return set_status(st, PLG_DimensionMismatch, -1, -1, "leading dimension smaller than n");
   if (int rc = begin_call(c, st)) return rc;
+  if (int rc = p2p_check_dims(c, u, st)) return rc;
   if (int rc = upload_x(c, X, n, d, ld, st)) return rc;
   const int64_t ldw = round_up(n, 16);
   if (int rc = reserve_run(c, n, u, ldw, st)) return rc;
@@ -1194,6 +1353,7 @@ int plg_search(plg_ctx* c, const double* X, int64_t n, int32_t d, int64_t ld, co
   plg::launch_gram(c->W.p, ldw, n, u, c->C.p, u, c->gscr.p, c->stream);
   ++c->launches;
   if (int rc = search_round(c, n, ldw, u, u, c->act0.p, 0, st)) return rc;
+  p2p_end_barrier(c);
   PLG_CUDA(c->scores.reserve(d));
   std::vector<double> ninf(d, -std::numeric_limits<double>::infinity());
   PLG_CUDA(cudaMemcpyAsync(c->scores.p, ninf.data(), d * sizeof(double), cudaMemcpyHostToDevice, c->stream));

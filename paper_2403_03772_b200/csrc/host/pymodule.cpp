@@ -441,6 +441,41 @@ PYBIND11_MODULE(_core, m) {
             return e;
           },
           py::arg("device"), py::arg("rank"), py::arg("world"), py::arg("uid"))
+      .def_static(
+          "peer",
+          [](int device, int rank, int world, int max_dims) {
+            // peer-memory multi-GPU context: connect with p2p_connect(handles of all ranks)
+            auto e = std::make_unique<Engine>();
+            plg_status st{};
+            gpu::check(plg_ctx_create_p2p(device, rank, world, max_dims, &e->ctx, &st), &st);
+            return e;
+          },
+          py::arg("device"), py::arg("rank"), py::arg("world"), py::arg("max_dims"))
+      .def("p2p_handle",
+           [](Engine& e) {
+             std::string h(64, '\0');
+             plg_status st{};
+             gpu::check(plg_p2p_handle(e.ctx, h.data(), &st), &st);
+             return py::bytes(h);
+           })
+      .def(
+          "p2p_connect",
+          [](Engine& e, const std::vector<py::bytes>& handles) {
+            std::string all;
+            for (const auto& h : handles) {
+              const std::string b(h);
+              if (b.size() != 64) throw Error(ErrorCode::OutOfRange, "IPC handles must be 64 bytes");
+              all += b;
+            }
+            plg_status st{};
+            int rc;
+            {
+              py::gil_scoped_release rel;
+              rc = plg_p2p_connect(e.ctx, all.data(), &st);
+            }
+            gpu::check(rc, &st);
+          },
+          py::arg("handles"))
       .def("causal_order", &engine_causal_order, py::arg("X"))
       .def(
           "causal_order_device",

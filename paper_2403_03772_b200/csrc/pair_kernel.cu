@@ -224,6 +224,12 @@ __global__ void finalize_kernel(const PairLaunch a) {
     e2 = entropy_from_sums(l2, p2, inv_n);
   }
   double* tile = a.epack + static_cast<int64_t>(a.tile_begin + tl) * 2 * kTilePairs;
+  if (a.peers.n > 0) {  // every rank's copy of the table (peer memory), then p2p_signal
+    peer_store(a.peers, &tile[x * kBT + y], e1);
+    peer_store(a.peers, &tile[kTilePairs + y * kBT + x], e2);
+    __threadfence_system();
+    return;
+  }
   tile[x * kBT + y] = e1;
   tile[kTilePairs + y * kBT + x] = e2;
 }

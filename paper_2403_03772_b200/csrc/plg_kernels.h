@@ -59,6 +59,36 @@ __host__ __device__ inline void tile_decode(int t, int nb, int& bi, int& bj) {
   bj = row + (t - start);
 }
 
+// ---- peer-memory exchange (multi-rank contexts created with plg_ctx_create_p2p) ----
+// Every rank owns one exchange arena; all ranks map every arena (CUDA IPC over NVLink). A
+// kernel that produces exchanged values stores each one into its local arena position and
+// the same offset of every peer's arena (peer_store), then a signal kernel publishes a
+// sequence number into every peer's flag slot for this rank and the consumer's wait kernel
+// waits for every rank's slot (p2p_kernels.cu). No host synchronisation, no collective.
+constexpr int kMaxPeers = 8;
+struct PeerTable {
+  int n = 0;  // ranks mirrored to (0: local only, no exchange through peer memory)
+  int rank = 0;
+  char* base[kMaxPeers] = {};  // every rank's arena as mapped in this process (base[rank]: own)
+};
+#ifdef __CUDACC__
+__device__ __forceinline__ void peer_store(const PeerTable& pt, double* local, double v) {
+  const int64_t off = reinterpret_cast<char*>(local) - pt.base[pt.rank];
+#pragma unroll 1
+  for (int r = 0; r < pt.n; ++r) *reinterpret_cast<double*>(pt.base[r] + off) = v;
+}
+#endif
+// Arena layout (byte offsets): flags [0, 1024): u64 {signals sent, waits done, peer r's last
+// signal at 2 + r}; errs (two parities x kMaxPeers u64) at 1024; then pres[2] and epack[2].
+constexpr int64_t kArenaFlags = 0;
+constexpr int64_t kArenaErrs = 1024;
+constexpr int64_t kArenaData = 2048;
+// signal: this rank's error key into every peer's errs[parity][rank] (err_off >= 0), a
+// system-scope fence, then the next sequence number into every peer's flag slot for this rank
+void launch_p2p_signal(const PeerTable& pt, const unsigned long long* err, int64_t err_off, cudaStream_t s);
+// wait: until every rank's flag slot in the local arena holds this rank's next expected sequence
+void launch_p2p_wait(const PeerTable& pt, cudaStream_t s);
+
 struct PairLaunch {
   const double* W;
   int64_t ldw;
@@ -78,6 +108,7 @@ struct PairLaunch {
   const double2* g_log;
   unsigned long long* err;
   int round;
+  PeerTable peers;  // n > 0: the entropy tiles are also stored into every rank's epack (same offset)
 };
 
 void launch_pair(const PairLaunch& a, cudaStream_t s);
@@ -202,6 +233,7 @@ struct PruneArgs {
   int shard_rank;
   int shard_slot;               // entries per rank slot in res
   int* stage_log;               // analysis (PLG_STAGE_LOG): [round][kMaxPruneStages] list lengths, or null
+  PeerTable peers;              // n > 0: list entry k's M goes to res[k] of every rank (peer memory)
 };
 enum PruneStage : int { kStageProbe = 0, kStageRefine = 1, kStageFull = 2 };
 void launch_prune_predict(const PruneArgs& a, cudaStream_t s);

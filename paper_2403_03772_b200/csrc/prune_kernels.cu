@@ -823,7 +823,14 @@ __device__ __forceinline__ void finalize_chunk(const PruneArgs& a, const double*
   // ordering.cpp:93-94 (kreduce_kernel's expression); M_qp = -M_pq exactly
   const double mpq = (a.H[q] + e_pq) - (a.H[p] + e_qp);
   store_pair(a, p, q, mpq);
-  if (a.res) a.res[a.res_base + (base + kk - kb)] = mpq;  // multi-rank: this rank's slot
+  if (a.res) {
+    if (a.peers.n > 0) {  // peer memory: entry k of the stage list at res[k] of every rank
+      peer_store(a.peers, &a.res[base + kk], mpq);
+      __threadfence_system();
+    } else {
+      a.res[a.res_base + (base + kk - kb)] = mpq;  // multi-rank (NCCL): this rank's slot
+    }
+  }
 }
 
 // Work items (chunk of 32 list entries, sample segment) are fetched dynamically, chunk-major;

@@ -49,3 +49,33 @@ def test_repeat_runs_bit_identical(engine, plg):
     c2, s2 = engine.search(X, list(range(80)))
     assert c1 == c2 and np.asarray(s1).tobytes() == np.asarray(s2).tobytes()
     assert engine.causal_order(X) == engine.causal_order(X)
+
+
+_GRAPH_CHILD = r"""
+import json, sys
+sys.path.insert(0, %r)
+import numpy as np
+import paper_2403_03772_b200 as plg
+eng = plg.Engine(0)
+out = []
+for seed in (21, 22, 23, 24, 25):  # one shape: call 1 runs directly, 2 captures, 3-5 replay
+    dag = plg.gen_sparse_dag(220, avg_parents=2.0, seed=seed)
+    X = plg.sample_lingam(dag, 2500, seed=seed, kind="laplace")
+    order = eng.causal_order(X)
+    out.append({"order": order, "k": [float(v).hex() for v in eng.round_k()],
+                "launches": eng.stats()["launches"], "pairs": eng.stats()["pairs_evaluated"]})
+print(json.dumps(out))
+"""
+
+
+def test_graph_replay_matches_direct_launches():
+    # The round loop is captured into a CUDA graph on the second call of a shape and replayed
+    # afterwards (engine.cu run_rounds_graph): every call, on different data of one shape,
+    # must give the bits of the directly launched loop (PLG_GRAPHS=0), and the same stats.
+    runs = {}
+    for g in ("0", "1"):
+        env = dict(os.environ, PLG_GRAPHS=g)
+        out = subprocess.run([sys.executable, "-c", _GRAPH_CHILD % ROOT], env=env, capture_output=True, text=True,
+                             check=True, timeout=900)
+        runs[g] = json.loads(out.stdout.strip().splitlines()[-1])
+    assert runs["0"] == runs["1"]

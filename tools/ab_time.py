@@ -20,10 +20,12 @@ def main():
     ap.add_argument("--config", default="c5")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--tag", default="")
+    ap.add_argument("--pkg", default="", help="directory holding an A/B snapshot of the package (tools/ab_snapshot.sh)")
     args = ap.parse_args()
-    import bench
+    if args.pkg:
+        sys.path.insert(0, os.path.join(ROOT, args.pkg))
     import paper_2403_03772_b200 as plg
-
+    import bench
     X = bench.make_input(args.config)
     eng = plg.Engine(0)
     order = eng.causal_order(X)
@@ -33,7 +35,7 @@ def main():
         ms.append(eng.stats()["total_ms"])
     k = eng.round_k()
     st = eng.stats()
-    print(json.dumps({"tag": args.tag, "config": args.config, "median_ms": float(np.median(ms)), "ms": ms,
+    print(json.dumps({"tag": args.tag, "pkg": os.path.dirname(plg.__file__), "config": args.config, "median_ms": float(np.median(ms)), "ms": ms,
                       "pairs": st["pairs_evaluated"], "launches": st["launches"],
                       "order_sha": hashlib.sha1(str(order).encode()).hexdigest()[:12],
                       "k_sha": hashlib.sha1(np.asarray(k).tobytes()).hexdigest()[:12]}), flush=True)
