@@ -14,40 +14,19 @@ namespace plg {
 
 namespace {
 
-__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
 __global__ void p2p_signal_kernel(const PeerTable pt, const unsigned long long* err, int64_t err_off) {
   if (threadIdx.x != 0) return;
-  unsigned long long* f = reinterpret_cast<unsigned long long*>(pt.base[pt.rank] + kArenaFlags);
-  const unsigned long long seq = f[0] + 1;
-  f[0] = seq;
   if (err_off >= 0) {
     const unsigned long long e = *err;
     for (int r = 0; r < pt.n; ++r)
       *reinterpret_cast<unsigned long long*>(pt.base[r] + err_off + 8 * pt.rank) = e;
   }
-  __threadfence_system();
-  for (int r = 0; r < pt.n; ++r)
-    st_release_sys(reinterpret_cast<unsigned long long*>(pt.base[r] + kArenaFlags) + 2 + pt.rank, seq);
+  p2p_signal_dev(pt);
 }
 
 __global__ void p2p_wait_kernel(const PeerTable pt) {
-  unsigned long long* f = reinterpret_cast<unsigned long long*>(pt.base[pt.rank] + kArenaFlags);
-  const unsigned long long target = f[1] + 1;
-  if (threadIdx.x < pt.n) {
-    const unsigned long long* slot = f + 2 + threadIdx.x;
-    while (ld_acquire_sys(slot) < target) __nanosleep(200);
-  }
+  if (threadIdx.x == 0) p2p_wait_dev(pt);
   __syncthreads();
-  if (threadIdx.x == 0) f[1] = target;
-  __threadfence();
 }
 
 }  // namespace

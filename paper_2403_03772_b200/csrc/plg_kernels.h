@@ -71,18 +71,47 @@ struct PeerTable {
   int rank = 0;
   char* base[kMaxPeers] = {};  // every rank's arena as mapped in this process (base[rank]: own)
 };
+// Arena layout (byte offsets): flags [0, 1024): u64 {signals sent, unused, peer r's last
+// signal at 2 + r}; errs (two parities x kMaxPeers u64) at 1024; then pres[2] and epack[2].
+constexpr int64_t kArenaFlags = 0;
+constexpr int64_t kArenaErrs = 1024;
+constexpr int64_t kArenaData = 2048;
 #ifdef __CUDACC__
 __device__ __forceinline__ void peer_store(const PeerTable& pt, double* local, double v) {
   const int64_t off = reinterpret_cast<char*>(local) - pt.base[pt.rank];
 #pragma unroll 1
   for (int r = 0; r < pt.n; ++r) *reinterpret_cast<double*>(pt.base[r] + off) = v;
 }
+// One thread: publish this rank's next sequence number in every rank's flag slot for it
+// (after the caller's stores; release at system scope). Returns the sequence number.
+__device__ __forceinline__ unsigned long long p2p_signal_dev(const PeerTable& pt) {
+  unsigned long long* f = reinterpret_cast<unsigned long long*>(pt.base[pt.rank] + kArenaFlags);
+  const unsigned long long seq = f[0] + 1;
+  f[0] = seq;
+  __threadfence_system();
+#pragma unroll 1
+  for (int r = 0; r < pt.n; ++r) {
+    unsigned long long* slot = reinterpret_cast<unsigned long long*>(pt.base[r] + kArenaFlags) + 2 + pt.rank;
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(slot), "l"(seq) : "memory");
+  }
+  return seq;
+}
+// One thread: until every rank has signalled as often as this rank (every rank signals once
+// per exchange, so this rank's count is the exchange's sequence number).
+__device__ __forceinline__ void p2p_wait_dev(const PeerTable& pt) {
+  const unsigned long long* f = reinterpret_cast<const unsigned long long*>(pt.base[pt.rank] + kArenaFlags);
+  const unsigned long long target = *reinterpret_cast<const volatile unsigned long long*>(f);
+#pragma unroll 1
+  for (int r = 0; r < pt.n; ++r) {
+    for (;;) {
+      unsigned long long v;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f + 2 + r) : "memory");
+      if (v >= target) break;
+      __nanosleep(200);
+    }
+  }
+}
 #endif
-// Arena layout (byte offsets): flags [0, 1024): u64 {signals sent, waits done, peer r's last
-// signal at 2 + r}; errs (two parities x kMaxPeers u64) at 1024; then pres[2] and epack[2].
-constexpr int64_t kArenaFlags = 0;
-constexpr int64_t kArenaErrs = 1024;
-constexpr int64_t kArenaData = 2048;
 // signal: this rank's error key into every peer's errs[parity][rank] (err_off >= 0), a
 // system-scope fence, then the next sequence number into every peer's flag slot for this rank
 void launch_p2p_signal(const PeerTable& pt, const unsigned long long* err, int64_t err_off, cudaStream_t s);

@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--config", default="c5")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--tag", default="")
+    ap.add_argument("--peer", action="store_true", help="one-rank peer-memory context (every exchange through its arena)")
     ap.add_argument("--pkg", default="", help="directory holding an A/B snapshot of the package (tools/ab_snapshot.sh)")
     args = ap.parse_args()
     if args.pkg:
@@ -27,7 +28,7 @@ def main():
     import paper_2403_03772_b200 as plg
     import bench
     X = bench.make_input(args.config)
-    eng = plg.Engine(0)
+    eng = plg.Engine.peer(0, 0, 1, X.shape[1]) if args.peer else plg.Engine(0)
     order = eng.causal_order(X)
     ms = []
     for _ in range(args.reps):
