@@ -299,6 +299,9 @@ def dist_setup(args):
         import torch
         import torch.distributed as dist
 
+        # NCCL's INIT lines (one per rank) let the driver verify the rank count
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return world, rank, local
@@ -380,6 +383,8 @@ def run_ours(args, world, rank, local):
         dist.all_gather_object(handles, eng.p2p_handle())
         eng.p2p_connect(handles)
         dist.barrier()
+        print(f"[bench] rank {rank}/{world} on cuda:{local}: peer-memory exchange, {world - 1} peer arenas mapped",
+              file=sys.stderr, flush=True)
     else:
         torch.cuda.set_device(local)
         eng = plg.Engine(local)
@@ -449,10 +454,12 @@ def run_ours(args, world, rank, local):
     traffic, traffic_src = (None, None)
     if not args.no_ncu and world == 1:
         traffic, traffic_src = measure_traffic(args.config, pruned)
-    if traffic is None:
+    if traffic is None and args.config == "c5":  # the committed summaries are C5 launches
         why = traffic_src
         traffic, traffic_src = load_ncu_traffic("prune_pairs_ncu.json" if pruned else "pair_kernel_ncu.json")
         traffic_src = f"committed ncu --set full summary {traffic_src}" + (f" ({why})" if why else "")
+    elif traffic is None:
+        traffic_src = traffic_src or "not measured (--no-ncu)"
     line = {
         "metric": "causal-order pair-evals/s (and wall s) at d=2000,n=10k",
         "value": value, "unit": "pair-evals/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,

@@ -6,9 +6,9 @@ B200 two ways:
 
 * a one-rank peer context routes every exchange through its own arena (in-process): same
   order and winning-k bits as a local context, pruned and exhaustive rounds, search scores;
-* two processes on the same GPU, each a rank of a world-2 context, arenas mapped across
+* two and three processes on the same GPU, each a rank of a world-2/3 context, arenas mapped across
   processes with CUDA IPC (the mechanism used between GPUs over NVLink), handles exchanged
-  through files: both ranks return the single-rank order and winning-k bits.
+  through files: every rank returns the single-rank order and winning-k bits.
 """
 
 import json
@@ -87,11 +87,12 @@ print(json.dumps(out))
 """
 
 
-def test_p2p_two_ranks_across_processes(plg, tmp_path):
+@pytest.mark.parametrize("world", [2, 3])
+def test_p2p_ranks_across_processes(plg, tmp_path, world):
     d, n, seed = 200, 2000, 29
     src = _RANK % (ROOT, d, n, seed)
-    procs = [subprocess.Popen([sys.executable, "-c", src, str(r), "2", str(tmp_path)], stdout=subprocess.PIPE,
-                              stderr=subprocess.PIPE, text=True) for r in range(2)]
+    procs = [subprocess.Popen([sys.executable, "-c", src, str(r), str(world), str(tmp_path)],
+                              stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True) for r in range(world)]
     outs = []
     for p in procs:
         try:
@@ -110,5 +111,5 @@ def test_p2p_two_ranks_across_processes(plg, tmp_path):
         ref.append({"order": local.causal_order(X), "k": [float(v).hex() for v in local.round_k()]})
     c, s = local.search(X, list(range(d)))
     ref.append({"chosen": c, "scores": [float(v).hex() for v in s]})
-    assert outs[0] == ref
-    assert outs[1] == ref
+    for out in outs:
+        assert out == ref

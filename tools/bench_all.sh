@@ -16,8 +16,8 @@ run c5_noprune --config c5 --steps 2 --warmup 3 --no-prune --no-cpu --no-ncu
 run c5g --config c5g --steps 2 --warmup 3 --no-cpu
 run c3 --config c3 --steps 5 --warmup 3 --no-cpu
 run c4 --config c4 --steps 5 --warmup 3 --no-cpu --no-ncu
-run c2 --config c2 --steps 5 --warmup 3 --no-cpu --no-ncu
-run c1 --config c1 --steps 5 --warmup 3 --no-cpu --no-ncu
+run c2 --config c2 --steps 100 --warmup 5 --no-cpu --no-ncu
+run c1 --config c1 --steps 2000 --warmup 20 --no-cpu --no-ncu
 run ref_c5 --impl reference --config c5 --steps 1 --warmup 1
 run ref_c2 --impl reference --config c2 --steps 1 --warmup 1
 run ref_c1 --impl reference --config c1 --steps 3 --warmup 1
