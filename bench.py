@@ -39,7 +39,10 @@ CONFIGS = {
     "c5": (2000, 10000, "sparse ER DAG (avg 2 parents, |w| in [0.5,1.5]), Laplace(0,1) noise, seed 1"),
     # transparency case (not a BASELINE config): C5's shape with Gaussian noise, where no
     # variable is identifiable and every row's k is alike -- the exact pruning's worst case
-    "c5g": (2000, 10000, "sparse ER DAG (avg 2 parents), Gaussian N(0,1) noise, seed 1 (pruning worst case)"),
+    "c5g": (2000, 10000, "sparse ER DAG (avg 2 parents), Gaussian N(0,1) noise, seed 1 (non-identifiable noise)"),
+    # C5's shape with no edges at all: every variable is exchangeable and every row's k is
+    # alike, the hardest case for the exact pruning
+    "c5x": (2000, 10000, "2000 independent Laplace(0,1) columns (empty DAG), seed 1 (exchangeable: pruning worst case)"),
 }
 # SASS of the pair kernels' inner loops (cuobjdump): per EDE 16 DFMA + 9 DADD + 6 DMUL
 FP64_INSTR_PER_EDE = 31   # FP64-pipe instructions (each one pipe slot: the utilisation basis)
@@ -78,7 +81,7 @@ def make_input(name: str):
         b1 = np.asfortranarray(np.diag(plg.uniform_vector(d, 1, 0.2, 0.5)))
         X = plg.sample_svar(b0, [b1], T=2500, burn_in=500, seed=1, noise=(0.0, 1.0), kind="laplace")
         return plg.estimate_var(X, 1)[1]
-    dag = plg.gen_sparse_dag(d, avg_parents=2.0, seed=1)
+    dag = plg.gen_sparse_dag(d, avg_parents=0.0 if name == "c5x" else 2.0, seed=1)
     return plg.sample_lingam(dag, n, seed=1, noise=(0.0, 1.0), kind=_noise_kind(name))
 
 
@@ -105,7 +108,8 @@ def make_input_oracle(name: str):
         Z = np.hstack([np.ones((T - 1, 1)), Y[:-1]])
         coef, *_ = np.linalg.lstsq(Z, Y[1:], rcond=None)
         return np.asfortranarray(Y[1:] - Z @ coef)
-    return oracle_lib.sample_lingam(oracle_lib.gen_sparse_dag(d, 2.0, 1), n, 1, (0.0, 1.0), _noise_kind(name))
+    dag = oracle_lib.gen_sparse_dag(d, 0.0 if name == "c5x" else 2.0, 1)
+    return oracle_lib.sample_lingam(dag, n, 1, (0.0, 1.0), _noise_kind(name))
 
 
 def cpu_model() -> str:

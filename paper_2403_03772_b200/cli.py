@@ -86,8 +86,9 @@ def _manifest(command: str, config: dict, digest: str) -> dict:
     return {"command": command, "config": config, "input_digest": digest, "artifact_version": VERSION}
 
 
-def _setup_gpus(gpus: int) -> None:
-    """--gpus N under torchrun: every rank joins one NCCL communicator inside the engine."""
+def _setup_gpus(gpus: int, dims: int, transport: str = "p2p") -> None:
+    """--gpus N under torchrun: every rank maps every rank's exchange arena (peer memory,
+    the default) or joins one NCCL communicator inside the engine (--transport nccl)."""
     if gpus <= 1:
         return
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -98,14 +99,23 @@ def _setup_gpus(gpus: int) -> None:
     rank = int(os.environ["RANK"])
     local = int(os.environ.get("LOCAL_RANK", rank))
     dist.init_process_group("gloo")
-    obj = [_core.nccl_unique_id() if rank == 0 else None]
-    dist.broadcast_object_list(obj, src=0)
-    _core.init_distributed(local, rank, world, obj[0])
+    if transport == "nccl":
+        obj = [_core.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        _core.init_distributed(local, rank, world, obj[0])
+        return
+
+    def allgather(handle: bytes):
+        out = [None] * world
+        dist.all_gather_object(out, handle)
+        return out
+
+    _core.init_peer(local, rank, world, max(2, dims), allgather)
 
 
 def run_discover(args) -> int:
     X, names = read_input(args.input, args.dims, args.colmajor)
-    _setup_gpus(args.gpus)
+    _setup_gpus(args.gpus, X.shape[1], args.transport)
     rank = int(os.environ.get("RANK", "0"))
     dag = _core.fit_direct_lingam(X, edge_threshold=args.threshold)
     order, B, used_pinv, phases = dag.order, dag.weights, dag.used_pinv, dag.phases
@@ -176,6 +186,8 @@ def main(argv=None) -> int:
         p.add_argument("--workers", type=int, default=0, help="accepted for compatibility (no effect)")
         if name == "discover":
             p.add_argument("--gpus", type=int, default=1, help="ranks of a torchrun job sharing the search")
+            p.add_argument("--transport", choices=["p2p", "nccl"], default="p2p",
+                           help="multi-GPU exchange: peer memory (default) or NCCL")
         else:
             p.add_argument("--lag", type=int, default=1)
             p.add_argument("--difference", action="store_true")

@@ -1,6 +1,8 @@
 // plingam.cpp — host side of the reference API over the B200 engine's C-ABI.
 #include "plingam/plingam.hpp"
 
+#include <functional>
+
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -165,6 +167,28 @@ void init_distributed(int device, int rank, int world, const std::string& nccl_u
   plg_ctx* c = nullptr;
   check(plg_ctx_create_dist(device, rank, world, nccl_uid.data(), &c, &st), &st);
   g_ctx = own(c);
+}
+
+void init_peer(int device, int rank, int world, int max_dims,
+               const std::function<std::vector<std::string>(const std::string&)>& allgather) {
+  plg_status st{};
+  plg_ctx* c = nullptr;
+  check(plg_ctx_create_p2p(device, rank, world, max_dims, &c, &st), &st);
+  auto ctx = own(c);
+  std::string mine(64, '\0');
+  check(plg_p2p_handle(c, mine.data(), &st), &st);
+  const std::vector<std::string> all = allgather(mine);
+  if (static_cast<int>(all.size()) != world)
+    throw Error(ErrorCode::DimensionMismatch, "init_peer: the exchange returned a handle count != world");
+  std::string cat;
+  for (const auto& h : all) {
+    if (h.size() != 64) throw Error(ErrorCode::OutOfRange, "init_peer: IPC handles are 64 bytes");
+    cat += h;
+  }
+  check(plg_p2p_connect(c, cat.data(), &st), &st);
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_ctx = ctx;
+  g_device = device;
 }
 
 }  // namespace gpu

@@ -21,6 +21,7 @@
 #include <span>
 #include <stdexcept>
 #include <memory>
+#include <functional>
 #include <string>
 #include <utility>
 #include <vector>
@@ -161,6 +162,10 @@ std::shared_ptr<plg_ctx> context();
 // One process per GPU: every rank calls this with the same 128-byte NCCL unique id
 // (nccl_unique_id() on rank 0, broadcast by the caller). Replaces context().
 void init_distributed(int device, int rank, int world, const std::string& nccl_uid);
+// Multi-GPU through peer memory (plg_ctx_create_p2p): allgather(this rank's 64-byte IPC
+// handle) must return every rank's handle in rank order (any host channel).
+void init_peer(int device, int rank, int world, int max_dims,
+               const std::function<std::vector<std::string>(const std::string&)>& allgather);
 std::string nccl_unique_id();
 void set_device(int device);
 void reset();

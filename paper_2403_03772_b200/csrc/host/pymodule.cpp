@@ -337,6 +337,17 @@ PYBIND11_MODULE(_core, m) {
         gpu::init_distributed(device, rank, world, std::string(uid));
       },
       py::arg("device"), py::arg("rank"), py::arg("world"), py::arg("uid"));
+  m.def(
+      "init_peer",
+      [](int device, int rank, int world, int max_dims, py::function allgather) {
+        gpu::init_peer(device, rank, world, max_dims, [&](const std::string& mine) {
+          py::list got = allgather(py::bytes(mine));
+          std::vector<std::string> out;
+          for (auto h : got) out.push_back(std::string(py::cast<py::bytes>(h)));
+          return out;
+        });
+      },
+      py::arg("device"), py::arg("rank"), py::arg("world"), py::arg("max_dims"), py::arg("allgather"));
 
   // ---- synthetic inputs (support; simgen.cpp semantics) ----
   py::class_<sim::Dag>(m, "SimDag")
