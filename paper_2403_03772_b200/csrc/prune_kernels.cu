@@ -1054,12 +1054,12 @@ cudaError_t launch_prune_pairs(const PruneArgs& a, cudaStream_t s) {
     const char* v = std::getenv("PLG_LIST_VAR");
     return v ? std::atoi(v) : 0;
   }();
-  if (a.n > 90000) return launch_pairs_cfg<true, 0>(a, s);
+  if (a.n > 90000) return launch_pairs_cfg<true, 5>(a, s);
   if (var == 1) return launch_pairs_cfg<false, 1>(a, s);
   if (var == 2) return launch_pairs_cfg<false, 2>(a, s);
   if (var == 4) return launch_pairs_cfg<false, 4>(a, s);
-  if (var == 5) return launch_pairs_cfg<false, 5>(a, s);
-  return launch_pairs_cfg<false, 0>(a, s);
+  if (var == 10) return launch_pairs_cfg<false, 0>(a, s);  // 128-bit loads (round-1 default)
+  return launch_pairs_cfg<false, 5>(a, s);  // 256-bit loads: LDG.E.ENL2.256
 }
 
 void launch_prune_scatter(const PruneArgs& a, int world, int slot, cudaStream_t s) {
@@ -1070,6 +1070,6 @@ void launch_prune_bound(const PruneArgs& a, int pass, cudaStream_t s) {
   prune_bound_kernel<<<(a.u + 7) / 8, 256, 0, s>>>(a, pass);
 }
 
-int prune_pairs_grid() { return pairs_grid_for<false, 0>(); }
+int prune_pairs_grid() { return pairs_grid_for<false, 5>(); }
 
 }  // namespace plg
