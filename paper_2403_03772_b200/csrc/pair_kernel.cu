@@ -265,25 +265,33 @@ __global__ void __launch_bounds__(kSmallThreads) pair_small_kernel(const PairLau
   const double* wj = a.W + static_cast<int64_t>(a.act[q]) * a.ldw;
   const TabPtr tp = table_ptrs(smem, threadIdx.x & 31);
   EdeAcc acc1, acc2;
-  const int64_t t0 = static_cast<int64_t>(seg) * a.seg_len;  // multiple of 16: 16-byte aligned
+  const int64_t t0 = static_cast<int64_t>(seg) * a.seg_len;  // multiple of 16: 32-byte aligned
   const int64_t t1 = lmin(a.n, t0 + a.seg_len);
   int64_t t = t0;
-#pragma unroll 1
-  for (; t + 1 < t1; t += 2) {
-    const double2 x = __ldg(reinterpret_cast<const double2*>(wi + t));
-    const double2 y = __ldg(reinterpret_cast<const double2*>(wj + t));
-    const double u1a = fma(y.x, -bs1, x.x * s1), u2a = fma(x.x, -bs2, y.x * s2);
-    const double u1b = fma(y.y, -bs1, x.y * s1), u2b = fma(x.y, -bs2, y.y * s2);
-    ede_accumulate<kClampA>(u1a, acc1, tp);
-    ede_accumulate<kClampA>(u2a, acc2, tp);
-    ede_accumulate<kClampA>(u1b, acc1, tp);
-    ede_accumulate<kClampA>(u2b, acc2, tp);
-  }
-  if (t < t1) {
-    const double x = wi[t], y = wj[t];
+  auto ede2 = [&](double x, double y) {
     ede_accumulate<kClampA>(fma(y, -bs1, x * s1), acc1, tp);
     ede_accumulate<kClampA>(fma(x, -bs2, y * s2), acc2, tp);
+  };
+  // 4 samples per step with 256-bit loads, the next step's loads issued before this step's math
+  const int nstep = static_cast<int>((t1 - t0) >> 2);
+  if (nstep > 0) {
+    const double* pi = wi + t0;
+    const double* pj = wj + t0;
+    double4 x = ldg256(pi), y = ldg256(pj);
+#pragma unroll 1
+    for (int i = 1; i <= nstep; ++i) {
+      const double4 cx = x, cy = y;
+      pi += 4;
+      pj += 4;
+      if (i < nstep) x = ldg256(pi), y = ldg256(pj);
+      ede2(cx.x, cy.x);
+      ede2(cx.y, cy.y);
+      ede2(cx.z, cy.z);
+      ede2(cx.w, cy.w);
+    }
+    t += 4 * static_cast<int64_t>(nstep);
   }
+  for (; t < t1; ++t) ede2(wi[t], wj[t]);
   double2* dst = reinterpret_cast<double2*>(a.part + (static_cast<int64_t>(seg) * npairs + pair) * 4);
   dst[0] = make_double2(acc_lc(acc1), acc_pdf(acc1));
   dst[1] = make_double2(acc_lc(acc2), acc_pdf(acc2));

@@ -68,4 +68,12 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// 32-byte (256-bit) read-only load of 4 consecutive doubles, 32-byte aligned (sm_100: one
+// LDG.E.ENL2.256 instead of two 128-bit loads, half the L1 wavefronts of per-lane loads)
+__device__ __forceinline__ double4 ldg256(const double* p) {
+  double4 v;
+  asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+  return v;
+}
+
 }  // namespace plg

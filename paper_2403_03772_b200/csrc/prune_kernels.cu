@@ -33,6 +33,7 @@
 #include <cstdint>
 #include <cstdlib>
 
+#include "plg_async.cuh"
 #include "plg_kernels.h"
 #include "plg_math.cuh"
 #include "plg_pair.cuh"
@@ -689,14 +690,6 @@ __device__ __forceinline__ void ede2(double xa, double ya, double s1, double bs1
 // ascending order per direction. Loads go straight to registers with a software prefetch:
 // kVar 0: 4 samples per step, 1 step ahead; 1: 2 samples per step, 2 steps ahead;
 // 2: 4 samples per step, 2 steps ahead.
-// 32-byte (256-bit) read-only load of 4 consecutive doubles (sm_100: one LDG.E.ENL2.256
-// instead of two 128-bit loads, half the L1 wavefronts of the per-lane column loads)
-__device__ __forceinline__ double4 ldg256(const double* p) {
-  double4 v;
-  asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
-  return v;
-}
-
 template <bool kClampA, int kVar, typename Tab>
 __device__ __forceinline__ void eval_segment(const double* wi, const double* wj, int64_t t0, int64_t t1, double s1,
                                              double bs1, double s2, double bs2, EdeAcc& acc1, EdeAcc& acc2,
