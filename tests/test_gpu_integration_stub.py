@@ -37,3 +37,34 @@ def test_integration_ctypes_stub_verbatim(monkeypatch, plg):
     bad[5, 3] = np.nan
     with pytest.raises(RuntimeError, match=r"error 1 \(row 5, col 3\)"):
         ns["causal_order"](bad)
+
+
+def _p2p_python_source() -> str:
+    text = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    sec = text.split("## 8. Multi-GPU through peer memory", 1)[1]
+    blocks = re.findall(r"```python\n(.*?)```", sec, re.S)
+    assert blocks, "INTEGRATION.md §8 has no python block"
+    return blocks[0]
+
+
+@pytest.mark.gpu
+def test_integration_peer_memory_snippet_verbatim(plg):
+    # INTEGRATION.md §8's Python block, as written, in a one-rank torch.distributed group
+    import socket
+
+    import torch.distributed as dist
+
+    import oracle_lib
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        dag = plg.gen_sparse_dag(40, avg_parents=2.0, seed=8)
+        X = plg.sample_lingam(dag, 3000, seed=8, kind="laplace")
+        ns = {"local_rank": 0, "rank": 0, "world": 1, "d": 40, "X": X}
+        exec(compile(_p2p_python_source(), "INTEGRATION.md#8", "exec"), ns)
+        assert ns["order"] == oracle_lib.causal_order(X)
+    finally:
+        dist.destroy_process_group()
