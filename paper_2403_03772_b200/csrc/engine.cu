@@ -533,9 +533,12 @@ int search_round_pruned(plg_ctx* c, int64_t n, int64_t ldw, int d, int u, const 
   a.batch = c->prune_batch;
   a.seg_len = sp.seg_len;
   a.nseg = sp.nseg;
+  // pair-list item order: segment-major (default) walks one 128-sample window of every listed
+  // column at a time, so the working set stays in L2 (C5 launch at u ~ 1925: 183 MB of DRAM
+  // traffic instead of 581 MB, -2% time); PLG_SEG_MAJOR=0 gives chunk-major order
   static const int seg_major = [] {
     const char* v = std::getenv("PLG_SEG_MAJOR");
-    return v ? std::atoi(v) : 0;
+    return v ? std::atoi(v) : 1;
   }();
   a.seg_major = seg_major;
   static const double top_ratio = [] {
