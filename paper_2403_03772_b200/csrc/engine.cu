@@ -541,6 +541,11 @@ int search_round_pruned(plg_ctx* c, int64_t n, int64_t ldw, int d, int u, const 
     return v ? std::atoi(v) : 1;
   }();
   a.seg_major = seg_major;
+  static const int fine_items = [] {  // PLG_FINE_ITEMS: short-list segment split threshold (items)
+    const char* v = std::getenv("PLG_FINE_ITEMS");
+    return v ? std::max(0, std::atoi(v)) : 2400;  // ~ one item per resident warp
+  }();
+  a.fine_items = c->prune_tile_seg ? 0 : fine_items;
   static const double top_ratio = [] {
     const char* v = std::getenv("PLG_TOP_RATIO");
     return v ? std::atof(v) : 0.0;

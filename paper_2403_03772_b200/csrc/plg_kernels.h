@@ -246,6 +246,7 @@ struct PruneArgs {
   int seg_len;
   int nseg;
   int seg_major;                // pair-list item order: segment-major (1) or chunk-major (0)
+  int fine_items;               // lists with fewer items split their segments (0: never)
   double top_ratio;             // > 0: one top row when its prediction < top_ratio x the runner-up's
   const double* g_exp;
   const double2* g_log;

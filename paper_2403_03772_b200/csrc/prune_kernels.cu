@@ -670,6 +670,8 @@ __global__ void __launch_bounds__(1024) prune_scan_kernel(const PruneArgs a) {
 
 // ---- pairs: cooperative persistent evaluation of the list ----
 constexpr int kListThreads = 256;
+constexpr int kMinSegLen = 32;  // finest sample segment of a short list (a multiple of 4)
+constexpr int64_t kFineMaxN = 4096;  // short columns: few segments per pair, so short lists have few items
 
 // Entry k of the stage's list: the row holding the entry's 32-chunk start (chunk_row, from the
 // scan), then forward over rows that end before k (rows with zero entries share offsets).
@@ -853,6 +855,41 @@ __device__ __forceinline__ void finalize_chunk(const PruneArgs& a, const double*
   }
 }
 
+__device__ __forceinline__ void finalize_chunk_fine(const PruneArgs& a, const double* part, int base, int m, int chunk,
+                                               int lane, int kb, int nseg, int64_t pstride) {
+  const int kk = chunk * 32 + lane;
+  if (kk >= m) return;
+  int p, q;
+  list_entry(a, base + kk, p, q);
+  double l1 = 0.0, p1 = 0.0, l2 = 0.0, p2 = 0.0;
+  const double2* src = reinterpret_cast<const double2*>(part + static_cast<int64_t>(kk) * 4);
+  const int64_t stride = pstride * 2;  // double2 per segment
+#pragma unroll 8
+  for (int s = 0; s < nseg; ++s) {  // loads run ahead; the adds stay in ascending order
+    const double2 v1 = __ldcg(src);  // written by other SMs: bypass L1
+    const double2 v2 = __ldcg(src + 1);
+    l1 += v1.x;
+    p1 += v1.y;
+    l2 += v2.x;
+    p2 += v2.y;
+    src += stride;
+  }
+  const double inv_n = 1.0 / static_cast<double>(a.n);
+  const double e_pq = entropy_from_sums(l1, p1, inv_n);  // E(p | q)
+  const double e_qp = entropy_from_sums(l2, p2, inv_n);  // E(q | p)
+  // ordering.cpp:93-94 (kreduce_kernel's expression); M_qp = -M_pq exactly
+  const double mpq = (a.H[q] + e_pq) - (a.H[p] + e_qp);
+  store_pair(a, p, q, mpq);
+  if (a.res) {
+    if (a.peers.n > 0) {  // peer memory: entry k of the stage list at res[k] of every rank
+      peer_store(a.peers, &a.res[base + kk], mpq);
+      __threadfence_system();
+    } else {
+      a.res[a.res_base + (base + kk - kb)] = mpq;  // multi-rank (NCCL): this rank's slot
+    }
+  }
+}
+
 // Work items (chunk of 32 list entries, sample segment) are fetched dynamically, chunk-major;
 // the warp completing a chunk's last segment finalises it, so a batch needs no grid barrier.
 // Lists longer than one batch (part-buffer capacity) run batch after batch with a grid
@@ -942,6 +979,122 @@ __global__ void __launch_bounds__(kListThreads, 2) prune_pairs_kernel(const Prun
   }
 }
 
+// The same kernel for short columns (n <= kFineMaxN, where short lists have few items): the
+// list's segmentation may be refined at run time (below). A separate kernel because the
+// long-column kernel's hot loop has no registers to spare: even values re-read from shared
+// memory cost the long lists ~2% (measured).
+template <bool kClampA, int kVar>
+__global__ void __launch_bounds__(kListThreads, 2) prune_pairs_fine_kernel(const PruneArgs a) {
+  constexpr bool kFine = true;
+  extern __shared__ __align__(128) unsigned char smem[];
+  // segmentation of this list, re-read from shared memory where it is used
+  __shared__ int s_seg[2];
+  __shared__ long long s_pstride;
+  const int lane = threadIdx.x & 31;
+  const TabAddr tp = load_tables_aligned(smem, a.g_exp, a.g_log, lane);
+  if (kFine && threadIdx.x == 0) {
+    // Short lists (fewer items than a.fine_items): finer sample segments, so that a stage of
+    // a few hundred pairs still spreads over every SM. A pure function of the whole stage
+    // list's length and n (not of this rank's slice), so a pair's bits do not depend on the
+    // rank count; the part buffer holds nseg x pstride entries either way.
+    int seg_len = a.seg_len, nseg = a.nseg;
+    long long pstride = a.batch;
+    const int all = a.off[a.u];
+    const int all_chunks = (all + 31) / 32;
+    while (all_chunks * nseg < a.fine_items && seg_len >= 2 * kMinSegLen && 2 * all <= pstride) {
+      seg_len >>= 1;
+      nseg = static_cast<int>((a.n + seg_len - 1) / seg_len);
+      pstride >>= 1;
+    }
+    s_seg[0] = seg_len;
+    s_seg[1] = nseg;
+    s_pstride = pstride;
+  }
+  __syncthreads();
+  const volatile int* vseg = s_seg;
+  const volatile long long* vps = &s_pstride;
+  cg::grid_group grid = cg::this_grid();
+  const bool skip = (*a.err != kNoError);  // only skips work: every CTA still meets the barriers
+  // this launch's share of the list: [kb, ke) — host-planned (k_end < 0: to the end of the
+  // list), or this rank's slice of ceil(total / shard_world) entries planned here
+  int kb = a.k_begin, ke = a.k_end >= 0 ? a.k_end : a.off[a.u];
+  if (a.shard_world > 0) {
+    const int tot = a.off[a.u];
+    const int cnt = (tot + a.shard_world - 1) / a.shard_world;
+    kb = min(tot, a.shard_rank * cnt);
+    ke = min(tot, (a.shard_rank + 1) * cnt);
+    if (cnt > a.shard_slot) {  // the host-side slot bound broke: ranks would overwrite each other's slots
+      if (blockIdx.x == 0 && threadIdx.x == 0) atomicMin(a.err, err_key(0, kErrInternal, -1));
+      ke = kb;
+    }
+  }
+  const int total = ke - kb;
+  const int nbatch = (total + a.batch - 1) / a.batch;
+  for (int b = 0; b < nbatch; ++b) {
+    if (b > 0) grid.sync();  // every chunk of batch b - 1 is finalised: the part slab is free
+    const int base = kb + b * a.batch;
+    const int m = min(a.batch, total - b * a.batch);
+    const int chunks = (m + 31) / 32;
+    while (!skip) {
+      int it = 0;
+      if (lane == 0) it = atomicAdd(&a.work[b], 1);
+      it = __shfl_sync(0xffffffffu, it, 0);
+      int nseg = kFine ? vseg[1] : a.nseg;
+      if (it >= chunks * nseg) break;
+      int chunk, seg;
+      if (a.seg_major) {  // a sample window of every chunk at a time: column slices stay in L2
+        seg = it / chunks;
+        chunk = it - seg * chunks;
+      } else {  // a chunk's segments back to back: its partial sums stay in L2
+        chunk = it / nseg;
+        seg = it - chunk * nseg;
+      }
+      const int kk = chunk * 32 + lane;
+      if (kk < m) {
+        int p, q;
+        list_entry(a, base + kk, p, q);
+        const int ci = a.act[p], cj = a.act[q];
+        const double* wi = a.W + static_cast<int64_t>(ci) * a.ldw;
+        const double* wj = a.W + static_cast<int64_t>(cj) * a.ldw;
+        const int seg_len = kFine ? vseg[0] : a.seg_len;
+        const int64_t t0 = static_cast<int64_t>(seg) * seg_len;  // multiple of 4: 32-byte aligned
+        const int64_t t1 = lmin(a.n, t0 + seg_len);
+        EdeAcc acc1, acc2;
+        if (kVar == 4) {
+          double2 xa = make_double2(0.0, 0.0), xb = xa, ya = xa, yb = xa;
+          if (t0 + 3 < t1) {
+            const double2* pi = reinterpret_cast<const double2*>(wi + t0);
+            const double2* pj = reinterpret_cast<const double2*>(wj + t0);
+            xa = __ldg(pi), xb = __ldg(pi + 1), ya = __ldg(pj), yb = __ldg(pj + 1);
+          }
+          double s1, bs1, s2, bs2;
+          pair_scales(a.C, a.ldc, ci, cj, s1, bs1, s2, bs2);  // collinear pairs: zeros (flagged by predict)
+          eval_segment_pre<kClampA>(wi, wj, t0, t1, s1, bs1, s2, bs2, acc1, acc2, tp, xa, xb, ya, yb);
+        } else {
+          double s1, bs1, s2, bs2;
+          pair_scales(a.C, a.ldc, ci, cj, s1, bs1, s2, bs2);  // collinear pairs: zeros (flagged by predict)
+          eval_segment<kClampA, kVar>(wi, wj, t0, t1, s1, bs1, s2, bs2, acc1, acc2, tp);
+        }
+        double2* dst = reinterpret_cast<double2*>(a.part + (static_cast<int64_t>(seg) * (kFine ? static_cast<int64_t>(*vps) : static_cast<int64_t>(a.batch)) + kk) * 4);
+        __stcg(dst, make_double2(acc_lc(acc1), acc_pdf(acc1)));
+        __stcg(dst + 1, make_double2(acc_lc(acc2), acc_pdf(acc2)));
+      }
+      __threadfence();  // release this segment's partials before counting it
+      __syncwarp();
+      nseg = kFine ? vseg[1] : a.nseg;
+      int last = 0;
+      if (lane == 0) last = (atomicAdd(&a.done[chunk], 1) == nseg - 1);
+      last = __shfl_sync(0xffffffffu, last, 0);
+      if (last) {
+        __threadfence();  // acquire the other segments' partials
+        finalize_chunk_fine(a, a.part, base, m, chunk, lane, kb, nseg,
+                       kFine ? static_cast<int64_t>(*vps) : static_cast<int64_t>(a.batch));
+        if (lane == 0) a.done[chunk] = 0;  // ready for the next batch / launch
+      }
+    }
+  }
+}
+
 // ---- scatter (multi-rank): every rank's results of the stage's list into Md / KN ----
 __global__ void prune_scatter_kernel(const PruneArgs a, int world, int slot) {
   const int total = a.off[a.u];
@@ -989,30 +1142,32 @@ __global__ void __launch_bounds__(256) prune_bound_kernel(const PruneArgs a, int
   }
 }
 
-template <bool kClampA, int kVar>
+template <bool kClampA, int kVar, bool kFine = false>
 int pairs_grid_for() {
   static DeviceCache gridc;
-  return gridc.get([] {
-    cudaFuncSetAttribute(prune_pairs_kernel<kClampA, kVar>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const auto k = kFine ? prune_pairs_fine_kernel<kClampA, kVar> : prune_pairs_kernel<kClampA, kVar>;
+  return gridc.get([k] {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kTableAlignedBytes);
     int dev = 0, sms = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, prune_pairs_kernel<kClampA, kVar>, kListThreads,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, kListThreads,
                                                   kTableAlignedBytes);
     return sms * (per > 0 ? per : 1);
   });
 }
 
-template <bool kClampA, int kVar>
+template <bool kClampA, int kVar, bool kFine = false>
 cudaError_t launch_pairs_cfg(const PruneArgs& a, cudaStream_t s) {
-  const int grid = pairs_grid_for<kClampA, kVar>();
+  const int grid = pairs_grid_for<kClampA, kVar, kFine>();
+  const auto k = kFine ? prune_pairs_fine_kernel<kClampA, kVar> : prune_pairs_kernel<kClampA, kVar>;
   PruneArgs args = a;
   void* params[] = {&args};
   // the grid barrier between batches needs every CTA resident: a failed cooperative launch
   // (e.g. fewer co-resident CTAs under a tool) must surface, not be skipped silently
-  return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(prune_pairs_kernel<kClampA, kVar>), dim3(grid),
-                                     dim3(kListThreads), params, kTableAlignedBytes, s);
+  return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k),
+                                     dim3(grid), dim3(kListThreads), params, kTableAlignedBytes, s);
 }
 
 }  // namespace
@@ -1048,6 +1203,7 @@ cudaError_t launch_prune_pairs(const PruneArgs& a, cudaStream_t s) {
     return v ? std::atoi(v) : 0;
   }();
   if (a.n > 90000) return launch_pairs_cfg<true, 5>(a, s);
+  if (a.fine_items > 0 && a.n <= kFineMaxN) return launch_pairs_cfg<false, 5, true>(a, s);
   if (var == 1) return launch_pairs_cfg<false, 1>(a, s);
   if (var == 2) return launch_pairs_cfg<false, 2>(a, s);
   if (var == 4) return launch_pairs_cfg<false, 4>(a, s);
