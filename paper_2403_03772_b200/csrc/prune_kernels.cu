@@ -1203,7 +1203,11 @@ cudaError_t launch_prune_pairs(const PruneArgs& a, cudaStream_t s) {
     return v ? std::atoi(v) : 0;
   }();
   if (a.n > 90000) return launch_pairs_cfg<true, 5>(a, s);
-  if (a.fine_items > 0 && a.n <= kFineMaxN) return launch_pairs_cfg<false, 5, true>(a, s);
+  static const int fine_max_u = [] {  // PLG_FINE_MAX_U: the short-list kernel also for rounds up to this u
+    const char* v = std::getenv("PLG_FINE_MAX_U");
+    return v ? std::atoi(v) : 700;  // C3 -2%, C5 -0.3% (the long lists of large rounds keep the lean kernel)
+  }();
+  if (a.fine_items > 0 && (a.n <= kFineMaxN || a.u <= fine_max_u)) return launch_pairs_cfg<false, 5, true>(a, s);
   if (var == 1) return launch_pairs_cfg<false, 1>(a, s);
   if (var == 2) return launch_pairs_cfg<false, 2>(a, s);
   if (var == 4) return launch_pairs_cfg<false, 4>(a, s);
