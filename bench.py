@@ -378,17 +378,39 @@ def run_ours(args, world, rank, local):
     elif world > 1:
         # peer-memory exchange: every rank maps every rank's arena (CUDA IPC over NVLink); the
         # 64-byte handles travel once through torch.distributed, the fits themselves have no
-        # collective and no host synchronisation
+        # collective and no host synchronisation. If any rank cannot map its peers, every rank
+        # falls back to the NCCL exchange (decided collectively).
         import torch.distributed as dist
 
         torch.cuda.set_device(local)
-        eng = plg.Engine.peer(local, rank, world, d)
+        eng, why = None, ""
+        try:
+            eng = plg.Engine.peer(local, rank, world, d)
+            handle = eng.p2p_handle()
+        except plg.Error as e:
+            handle, why = b"", str(e)
         handles = [None] * world
-        dist.all_gather_object(handles, eng.p2p_handle())
-        eng.p2p_connect(handles)
+        dist.all_gather_object(handles, handle)
+        ok = all(len(h) == 64 for h in handles)
+        if ok:
+            try:
+                eng.p2p_connect(handles)
+            except plg.Error as e:
+                ok, why = False, str(e)
+        flags = [None] * world
+        dist.all_gather_object(flags, ok)
+        if all(flags):
+            print(f"[bench] rank {rank}/{world} on cuda:{local}: peer-memory exchange, {world - 1} peer arenas "
+                  f"mapped", file=sys.stderr, flush=True)
+        else:
+            print(f"[bench] rank {rank}: peer memory unavailable ({why or 'another rank failed'}); NCCL exchange",
+                  file=sys.stderr, flush=True)
+            args.transport = "nccl"
+            del eng
+            obj = [plg.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            eng = plg.Engine.distributed(local, rank, world, obj[0])
         dist.barrier()
-        print(f"[bench] rank {rank}/{world} on cuda:{local}: peer-memory exchange, {world - 1} peer arenas mapped",
-              file=sys.stderr, flush=True)
     else:
         torch.cuda.set_device(local)
         eng = plg.Engine(local)
