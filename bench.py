@@ -295,19 +295,28 @@ def cpu_baseline(X: np.ndarray, target_seconds: float = 15.0, full_max_seconds: 
             "alpha_s": float(alpha), "beta_s": float(beta), "seconds": t1 + t2 + (wall if how == "measured" else 0)}
 
 
+# Test hook (not for measurements): PLG_BENCH_SHARED_GPU=1 runs every rank of a torchrun job
+# on cuda:0 with a gloo process group, so the multi-rank path (peer-memory exchange across
+# processes, max-over-ranks timing, the JSON line) can be exercised on a one-GPU box.
+SHARED_GPU = os.environ.get("PLG_BENCH_SHARED_GPU") == "1"
+
+
 def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = 0 if SHARED_GPU else int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch
         import torch.distributed as dist
 
-        # NCCL's INIT lines (one per rank) let the driver verify the rank count
-        os.environ.setdefault("NCCL_DEBUG", "INFO")
-        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if SHARED_GPU:
+            dist.init_process_group("gloo")
+        else:
+            # NCCL's INIT lines (one per rank) let the driver verify the rank count
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return world, rank, local
 
 
@@ -317,7 +326,7 @@ def allreduce_max(x: float, world: int) -> float:
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device="cpu" if SHARED_GPU else "cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 

@@ -113,3 +113,26 @@ def test_p2p_ranks_across_processes(plg, tmp_path, world):
     ref.append({"chosen": c, "scores": [float(v).hex() for v in s]})
     for out in outs:
         assert out == ref
+
+
+def test_bench_two_ranks_on_one_gpu(tmp_path):
+    # bench.py's multi-rank path end to end under torchrun (peer-memory exchange across the two
+    # processes, max-over-ranks timing, one JSON line from rank 0), both ranks sharing cuda:0
+    # through the PLG_BENCH_SHARED_GPU test hook (a gloo process group instead of NCCL)
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ, PLG_BENCH_SHARED_GPU="1")
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+                          "--gpus", "2", "--config", "c4", "--steps", "1", "--warmup", "3", "--no-ncu"],
+                         env=env, capture_output=True, text=True, timeout=900, cwd=str(tmp_path))
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    rec = json.loads(lines[0])
+    assert rec["n_gpus"] == 2 and "peer memory" in rec["config"]["parallelism"]
+    assert rec["pruning"]["fraction_evaluated"] < 0.2 and rec["e2e"]["h2d_bytes_per_step"] > 0
+    assert out.stderr.count("peer-memory exchange") == 2
