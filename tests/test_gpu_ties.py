@@ -112,4 +112,5 @@ def test_large_config_orders_are_certified(engine, name):
         wk = np.array([float.fromhex(v) for v in g["winner_k"]])
         sk = np.array([float.fromhex(v) for v in g["second_k"]])
         assert np.all(sk[:-1] > wk[:-1] * (1 + 1e-9))
-        assert np.allclose(k, wk, rtol=1e-9, atol=0)
+        # the score bar of the order goldens (test_gpu_kernels_var.py::test_full_order_golden)
+        assert np.all(np.abs(k - wk) <= 1e-9 * np.abs(wk) + 1e-15)
