@@ -87,8 +87,9 @@ struct NcclApi {
 };
 
 NcclApi& nccl() {
-  static NcclApi api;
-  if (!api.loaded) {
+  // resolved once, thread-safe (function-local static initialisation)
+  static NcclApi api = [] {
+    NcclApi api;
     void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
     if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
     if (h) {
@@ -102,7 +103,8 @@ NcclApi& nccl() {
       api.loaded = api.GetUniqueId && api.CommInitRank && api.AllGather && api.CommDestroy && api.GroupStart &&
                    api.GroupEnd;
     }
-  }
+    return api;
+  }();
   return api;
 }
 
