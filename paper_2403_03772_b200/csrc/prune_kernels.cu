@@ -250,6 +250,8 @@ __global__ void __launch_bounds__(kTopThreads) prune_top_kernel(const PruneArgs 
 // ---- select: each row's partners for one stage, ascending, into rowsel[p * u + i] ----
 constexpr int kSelThreads = 256;
 constexpr int kBins = 2049;  // 0: known zero; 1 + biased exponent otherwise (1: unknown marker)
+constexpr int kWSplit = 15;            // fixed-point weight = hi << 15 + lo
+constexpr double kWMax = 134217727.0;  // 2^27 - 1: 8x the deficit target (2^24)
 
 __device__ __forceinline__ int key_bin(double v) {
   const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
@@ -323,7 +325,12 @@ __global__ void __launch_bounds__(kRowThreads) prune_rowl_kernel(const PruneArgs
 __global__ void __launch_bounds__(kSelThreads) prune_select_kernel(const PruneArgs a, int stage, int m,
                                                                    double beta, int cache_keys) {
   __shared__ int hist[kBins];
-  __shared__ unsigned long long wt[kBins];
+  // per-bin fixed-point weight sums as two 32-bit halves (native shared atomics: a 64-bit
+  // shared atomicAdd is a CAS loop, and hot bins made it the kernel's top stall)
+  __shared__ unsigned int wlo[kBins], whi[kBins];
+  auto wt = [&](int b) -> unsigned long long {
+    return (static_cast<unsigned long long>(whi[b]) << kWSplit) + wlo[b];
+  };
   __shared__ int s_warp[kSelThreads / 32];
   __shared__ int s_cut[2];  // boundary bin, entries of it to take
   extern __shared__ double s_key[];  // cache_keys: per partner, its prediction or -1 (not eligible)
@@ -378,7 +385,7 @@ __global__ void __launch_bounds__(kSelThreads) prune_select_kernel(const PruneAr
   const double wscale = deficit ? kOne / target : 0.0;
   int cut_bin = -1, cut_take = 0;  // full: every eligible partner
   if (!full) {
-    for (int i = threadIdx.x; i < kBins; i += kSelThreads) hist[i] = 0, wt[i] = 0ull;
+    for (int i = threadIdx.x; i < kBins; i += kSelThreads) hist[i] = 0, wlo[i] = 0u, whi[i] = 0u;
     __syncthreads();
     for (int q0 = 0; q0 < u; q0 += kSelThreads) {  // warp-aggregated bin increments
       const int q = q0 + threadIdx.x;
@@ -388,7 +395,13 @@ __global__ void __launch_bounds__(kSelThreads) prune_select_kernel(const PruneAr
       const unsigned grp = __match_any_sync(0xffffffffu, b);
       const int leader = __ffs(grp) - 1;
       if (e && (threadIdx.x & 31) == leader) atomicAdd(&hist[b], __popc(grp));
-      if (deficit && e) atomicAdd(&wt[b], static_cast<unsigned long long>(fmin(v * wscale, 1099511627776.0)));
+      if (deficit && e) {
+        // weights clamped at kWMax (8x the target): one element that alone reaches the target
+        // gives the same cut bin; the two halves' sums stay below 2^32 for u < 2^17
+        const unsigned long long w = static_cast<unsigned long long>(fmin(v * wscale, kWMax));
+        atomicAdd(&wlo[b], static_cast<unsigned int>(w & ((1ull << kWSplit) - 1)));
+        atomicAdd(&whi[b], static_cast<unsigned int>(w >> kWSplit));
+      }
     }
     __syncthreads();
     if (threadIdx.x < 32) {
@@ -401,7 +414,7 @@ __global__ void __launch_bounds__(kSelThreads) prune_select_kernel(const PruneAr
         unsigned long long own = 0;
         int own_n = 0;
         for (int b = hi; b > hi - per && b >= 0; --b) {
-          own += weighted ? wt[b] : static_cast<unsigned long long>(hist[b]);
+          own += weighted ? wt(b) : static_cast<unsigned long long>(hist[b]);
           own_n += hist[b];
         }
         unsigned long long incl = own;
@@ -421,7 +434,7 @@ __global__ void __launch_bounds__(kSelThreads) prune_select_kernel(const PruneAr
           int cn = incl_n - own_n;
           int b = hi;
           for (;;) {
-            const unsigned long long wb = weighted ? wt[b] : static_cast<unsigned long long>(hist[b]);
+            const unsigned long long wb = weighted ? wt(b) : static_cast<unsigned long long>(hist[b]);
             if (cum + wb >= need_total) break;
             cum += wb;
             cn += hist[b];
@@ -429,7 +442,7 @@ __global__ void __launch_bounds__(kSelThreads) prune_select_kernel(const PruneAr
           }
           const unsigned long long need = need_total - cum;  // > 0, <= the bin's weight
           r_bin = b;
-          r_take = weighted ? static_cast<int>((need * static_cast<unsigned long long>(hist[b]) + wt[b] - 1) / wt[b])
+          r_take = weighted ? static_cast<int>((need * static_cast<unsigned long long>(hist[b]) + wt(b) - 1) / wt(b))
                             : static_cast<int>(need);
           r_cnt = cn;
         }
