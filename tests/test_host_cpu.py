@@ -257,3 +257,20 @@ def test_oracle_generators_match_package(plg):
         Xa = plg.sample_lingam(a, 500, seed=9, noise=(0.0, 1.0), kind=kind)
         Xo = oracle_lib.sample_lingam(dag, 500, 9, (0.0, 1.0), kind)
         assert np.array_equal(Xa, Xo), kind
+
+
+class Status(ctypes.Structure):
+    _fields_ = [("code", ctypes.c_int32), ("row", ctypes.c_int64), ("col", ctypes.c_int64),
+                ("msg", ctypes.c_char * 256)]
+
+
+def test_peer_context_argument_checks(cabi):
+    # plg_ctx_create_p2p validates its arguments before touching a device (PLG_OutOfRange = 11)
+    ctx = ctypes.c_void_p()
+    st = Status()
+    for rank, world, dims in ((0, 9, 100), (2, 2, 100), (-1, 2, 100), (0, 2, 1)):
+        rc = cabi.plg_ctx_create_p2p(0, rank, world, dims, ctypes.byref(ctx), ctypes.byref(st))
+        assert rc == 11 and st.code == 11, (rank, world, dims, st.msg)
+        assert not ctx.value
+    assert cabi.plg_p2p_handle(None, ctypes.create_string_buffer(64), ctypes.byref(st)) == 11
+    assert cabi.plg_p2p_connect(None, ctypes.create_string_buffer(128), ctypes.byref(st)) == 11

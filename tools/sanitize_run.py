@@ -1,8 +1,9 @@
 """Workload for compute-sanitizer (memcheck / racecheck / synccheck / initcheck).
 
 Small config (d = 300, n = 2 000, sparse Laplace DAG) through every hot-path kernel family:
-pruned causal order (cooperative pair-list kernel, atomic work fetch, last-finisher
-finalisation, selection/scan/bound kernels), exhaustive causal order (mbarrier ring pair
+pruned causal order (cooperative pair-list kernels incl. the short-list one, atomic work
+fetch, last-finisher finalisation, selection/scan/bound kernels), the same through a one-rank
+peer-memory context, exhaustive causal order (mbarrier ring pair
 kernel, small-round kernels), one search round, the fused residualisation, the weights
 step and the VAR front-end. Run under a sanitizer as
 
@@ -34,6 +35,8 @@ def main() -> None:
     eng.set_prune(False)
     o_exh = eng.causal_order(X)
     assert o_pruned == o_exh, "pruned and exhaustive orders differ"
+    peer = plg.Engine.peer(0, 0, 1, d)  # every exchange through the peer-memory arena (signal/wait, scatter)
+    assert peer.causal_order(X) == o_exh, "peer-memory and local orders differ"
     chosen, scores = eng.search(X, list(range(d)))
     assert chosen == o_exh[0]
     B, pinv = eng.fit_weights(X, o_exh)
