@@ -30,13 +30,17 @@ def main() -> None:
     X = np.asfortranarray(plg.sample_lingam(dag, n, seed=5, kind="laplace"))
     eng = plg.Engine(0)
     eng.set_prune(True)
+    print("pruned order", flush=True)
     o_pruned = eng.causal_order(X)
     st = eng.stats()
     eng.set_prune(False)
+    print("exhaustive order", flush=True)
     o_exh = eng.causal_order(X)
     assert o_pruned == o_exh, "pruned and exhaustive orders differ"
-    peer = plg.Engine.peer(0, 0, 1, d)  # every exchange through the peer-memory arena (signal/wait, scatter)
-    assert peer.causal_order(X) == o_exh, "peer-memory and local orders differ"
+    if os.environ.get("SAN_PEER", "1") == "1":
+        peer = plg.Engine.peer(0, 0, 1, d)  # every exchange through the peer-memory arena (signal/wait, scatter)
+        assert peer.causal_order(X) == o_exh, "peer-memory and local orders differ"
+    print("orders ok", flush=True)
     chosen, scores = eng.search(X, list(range(d)))
     assert chosen == o_exh[0]
     B, pinv = eng.fit_weights(X, o_exh)
