@@ -370,7 +370,7 @@ __global__ void __launch_bounds__(kColentThreads)
 }
 
 // Residualisation fused with the next round's column entropies: w_r <- w_r - (C_rm / C_mm) w_m
-// in place (residualize_kernel's arithmetic) and, from the new values already in registers,
+// in place (multiply then subtract, as residual_into) and, from the new values already in registers,
 // the entropy sums of w_r / sqrt(C_rr) (C after the rank-1 update) per sample chunk:
 // hpart[(r * nch + c) * 2] = {sum lc, sum pdf}. hfin_kernel adds the chunks in ascending
 // order next round. Persistent CTAs so the tables are staged once per CTA, not per column.

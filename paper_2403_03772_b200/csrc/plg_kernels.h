@@ -160,7 +160,9 @@ void launch_colent(const double* W, int64_t ldw, int64_t n, const double* C, int
                    const int* nz, const int* col_var, int round, unsigned long long* err,
                    cudaStream_t s);
 
-// Residualisation (as launch_residualize) fused with the next round's column-entropy sums per
+// In-place residualisation w_r <- w_r - (C_rm / C_mm) w_m (multiply then subtract, as
+// residual_into, kernels.cpp:81-85; nz[r] = tag when the new column has a nonzero entry)
+// fused with the next round's column-entropy sums per
 // chunk of kResidChunk samples (hpart: [ur][resid_chunks(n)][2]); launch_hfin turns them into
 // H (and runs colent's zero-variance check). Rounds >= 1 of causal_order use this pair.
 constexpr int64_t kResidChunk = 1024;
@@ -279,7 +281,6 @@ void launch_prune_scatter(const PruneArgs& a, int world, int slot, cudaStream_t 
 // pass 0: every row's partial k L[] and k* over the top rows; 1: alive rows' L[]; 2: exact k[]
 // of the top and alive rows (+inf for pruned rows)
 void launch_prune_bound(const PruneArgs& a, int pass, cudaStream_t s);
-int prune_pairs_grid();  // co-resident CTAs of the cooperative list kernel
 constexpr int kMaxPruneStages = 8;
 
 // argmin over k (lowest position on ties), order/score bookkeeping, active-list compaction;
@@ -294,11 +295,6 @@ void launch_commit(const double* k, const int* act_cur, int* act_nxt, int u, con
 void launch_update_gram(double* C, int64_t ldc, const int* act_nxt, int ur, const RoundState* rs,
                         const unsigned long long* err, cudaStream_t s);
 
-// In-place residualisation w_r -= (C_rm / C_mm) w_m of the remaining columns; nz[r] = tag
-// when the new column has a nonzero entry.
-void launch_residualize(double* W, int64_t ldw, int64_t n, const double* C, int64_t ldc,
-                        const int* act_nxt, int ur, const RoundState* rs, int* nz, int tag,
-                        const unsigned long long* err, cudaStream_t s);
 
 // Reference regress_out (ordering.cpp:178-211): raw columns, fresh means, bit-exact.
 void launch_regress_out(const double* X, int64_t ldx, int64_t n, int exog, const int* remaining,

@@ -1236,6 +1236,5 @@ void launch_prune_bound(const PruneArgs& a, int pass, cudaStream_t s) {
   prune_bound_kernel<<<(a.u + 7) / 8, 256, 0, s>>>(a, pass);
 }
 
-int prune_pairs_grid() { return pairs_grid_for<false, 5>(); }
 
 }  // namespace plg

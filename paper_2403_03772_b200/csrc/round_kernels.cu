@@ -286,30 +286,6 @@ __global__ void update_gram_kernel(double* C, int64_t ldc, const int* act_nxt, i
   C[static_cast<int64_t>(r) * ldc + s] = v;
 }
 
-// w_r <- w_r - (C_rm / C_mm) w_m (multiply then subtract, as residual_into, kernels.cpp:81-85).
-// A column left identically zero (an exact duplicate of the root, up to an exact scale)
-// is what makes the reference's next standardize throw; nz[r] = tag marks the others.
-__global__ void residualize_kernel(double* W, int64_t ldw, int64_t n2, const double* C, int64_t ldc,
-                                   const int* act_nxt, const RoundState* rs, int* nz, int tag,
-                                   const unsigned long long* err) {
-  if (*err != kNoError) return;
-  const int m = rs->chosen_col;
-  const int r = act_nxt[blockIdx.y];
-  const double beta = C[static_cast<int64_t>(r) * ldc + m] / C[static_cast<int64_t>(m) * ldc + m];
-  double2* wr = reinterpret_cast<double2*>(W + static_cast<int64_t>(r) * ldw);
-  const double2* wm = reinterpret_cast<const double2*>(W + static_cast<int64_t>(m) * ldw);
-  bool any = false;
-  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n2;
-       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const double2 x = wr[t];
-    const double2 y = wm[t];
-    const double2 o = make_double2(__dsub_rn(x.x, __dmul_rn(beta, y.x)), __dsub_rn(x.y, __dmul_rn(beta, y.y)));
-    wr[t] = o;
-    any |= (o.x != 0.0) | (o.y != 0.0);
-  }
-  if (__any_sync(0xffffffffu, any) && (threadIdx.x & 31) == 0) nz[r] = tag;
-}
-
 // regress_out (ordering.cpp:178-211 -> kernels.cpp:106-121) with the reference's sums.
 __global__ void regress_out_kernel(const double* X, int64_t ldx, int64_t n, int exog,
                                    const int* remaining, double* out, int64_t ldo, int* zero_var) {
@@ -383,14 +359,6 @@ void launch_update_gram(double* C, int64_t ldc, const int* act_nxt, int ur, cons
   update_gram_kernel<<<grd, blk, 0, s>>>(C, ldc, act_nxt, ur, rs, err);
 }
 
-void launch_residualize(double* W, int64_t ldw, int64_t n, const double* C, int64_t ldc,
-                        const int* act_nxt, int ur, const RoundState* rs, int* nz, int tag,
-                        const unsigned long long* err, cudaStream_t s) {
-  const int64_t n2 = (n + 1) / 2;
-  int gx = static_cast<int>((n2 + 255) / 256);
-  if (gx > 8) gx = 8;
-  residualize_kernel<<<dim3(gx, ur), 256, 0, s>>>(W, ldw, n2, C, ldc, act_nxt, rs, nz, tag, err);
-}
 
 void launch_regress_out(const double* X, int64_t ldx, int64_t n, int exog, const int* remaining,
                         int r, double* out, int64_t ldo, int* zero_var_flag, cudaStream_t s) {
