@@ -174,7 +174,9 @@ struct plg_ctx {
   cudaStream_t side = nullptr;       // pruned rounds: predictions overlap the residualisation
   cudaEvent_t ev_gram = nullptr;     // main stream: the round's Gram update is done
   cudaEvent_t ev_side = nullptr;     // side stream: predictions + probe selection are done
+  cudaEvent_t ev_commit = nullptr;   // main stream: the round's root is committed
   bool gram_ready = false;           // ev_gram recorded by the previous round of this call
+  bool gram_on_side = false;         // ... on the side stream (ping-pong Gram update)
   ncclComm_t comm = nullptr;
   bool force_nccl = false;  // PLG_NCCL_SELFTEST=1 on a 1-rank dist context: every exchange through NCCL
   bool timing = true;
@@ -183,7 +185,8 @@ struct plg_ctx {
   double* g_exp = nullptr;
   double2* g_log = nullptr;
 
-  DevBuf<double> Xd, W, C, part, epack, H, k, scores, msd, gscr, rk, rsec, hpart;
+  DevBuf<double> Xd, W, C, C2, part, epack, H, k, scores, msd, gscr, rk, rsec, hpart;
+  double* Cr = nullptr;  // the current round's Gram: C, or C2 of the ping-pong pair (pruned rounds)
   DevBuf<int> act0, act1, colvar, order, stat, idx, nz;
   DevBuf<plg::RoundState> rs;
   DevBuf<unsigned long long> err, errs;
@@ -345,6 +348,7 @@ int ctx_init(plg_ctx* ctx, int device, plg_status* st) {
   PLG_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
   PLG_CUDA(cudaEventCreateWithFlags(&ctx->ev_gram, cudaEventDisableTiming));
   PLG_CUDA(cudaEventCreateWithFlags(&ctx->ev_side, cudaEventDisableTiming));
+  PLG_CUDA(cudaEventCreateWithFlags(&ctx->ev_commit, cudaEventDisableTiming));
   if (int rc = make_tables(ctx, st)) return rc;
   PLG_CUDA(ctx->err.reserve(1));
   PLG_CUDA(ctx->errs.reserve(64));
@@ -413,10 +417,10 @@ size_t part_doubles(const RoundPlan& rp, int u) {
 void round_entropies(plg_ctx* c, int64_t n, int64_t ldw, int ldc, int u, const int* act_cur, int round,
                      bool from_resid) {
   if (from_resid)
-    plg::launch_hfin(c->hpart.p, n, c->C.p, ldc, act_cur, u, c->H.p, c->nz.p, c->colvar.p, round, c->err.p,
+    plg::launch_hfin(c->hpart.p, n, c->Cr, ldc, act_cur, u, c->H.p, c->nz.p, c->colvar.p, round, c->err.p,
                      c->stream);
   else
-    plg::launch_colent(c->W.p, ldw, n, c->C.p, ldc, act_cur, u, c->H.p, c->g_exp, c->g_log, c->nz.p,
+    plg::launch_colent(c->W.p, ldw, n, c->Cr, ldc, act_cur, u, c->H.p, c->g_exp, c->g_log, c->nz.p,
                        c->colvar.p, round, c->err.p, c->stream);
   ++c->launches;
 }
@@ -429,7 +433,7 @@ int search_round(plg_ctx* c, int64_t n, int64_t ldw, int ldc, int u, const int* 
   a.W = c->W.p;
   a.ldw = ldw;
   a.n = n;
-  a.C = c->C.p;
+  a.C = c->Cr;
   a.ldc = ldc;
   a.act = act_cur;
   a.u = u;
@@ -505,7 +509,9 @@ int search_round_pruned(plg_ctx* c, int64_t n, int64_t ldw, int d, int u, const 
   const bool overlap = c->gram_ready && h_from_resid;
   cudaStream_t ps = overlap ? c->side : c->stream;
   if (overlap) PLG_CUDA(cudaStreamWaitEvent(c->side, c->ev_gram, 0));
+  if (c->gram_on_side) PLG_CUDA(cudaStreamWaitEvent(c->stream, c->ev_gram, 0));  // hfin reads the new C_rr
   c->gram_ready = false;
+  c->gram_on_side = false;
   round_entropies(c, n, ldw, d, u, act_cur, round, h_from_resid);
   const SegPlan sp = c->prune_tile_seg ? seg_plan(u, n) : prune_seg_plan(n);
   PLG_CUDA(cudaMemsetAsync(c->Md.p, 0xff, static_cast<size_t>(u) * u * sizeof(double), ps));
@@ -513,7 +519,7 @@ int search_round_pruned(plg_ctx* c, int64_t n, int64_t ldw, int d, int u, const 
   a.W = c->W.p;
   a.ldw = ldw;
   a.n = n;
-  a.C = c->C.p;
+  a.C = c->Cr;
   a.ldc = d;
   a.act = act_cur;
   a.u = u;
@@ -878,7 +884,7 @@ void p2p_end_barrier(plg_ctx* c) {
 // the side stream joins through its events) and replays it; later calls only replay.
 template <class Loop>
 int run_rounds_graph(plg_ctx* c, int d, int64_t n, int rounds, bool prune, Loop&& run_loop, plg_status* st) {
-  std::vector<const void*> key = {c->W.p, c->C.p, c->part.p, c->epack.p, c->H.p, c->k.p, c->rk.p, c->rsec.p,
+  std::vector<const void*> key = {c->W.p, c->C.p, c->C2.p, c->part.p, c->epack.p, c->H.p, c->k.p, c->rk.p, c->rsec.p,
                                   c->hpart.p, c->act0.p, c->act1.p, c->colvar.p, c->order.p, c->nz.p, c->rs.p,
                                   c->err.p, c->Md.p, c->KN.p, c->pk.p, c->L.p, c->ppart.p, c->st0.p, c->st1.p,
                                   c->rowsel.p, c->off.p, c->pwork.p, c->pdone.p, c->crow.p, c->cand.p, c->alive.p, c->kstar.p,
@@ -949,14 +955,17 @@ int causal_order_impl(plg_ctx* c, const double* dX, int64_t ldx, int64_t n, int 
   if (int rc = upload_iota(c, c->colvar.p, d, nullptr, st)) return rc;
   PLG_CUDA(cudaMemsetAsync(c->err.p, 0xff, sizeof(unsigned long long), c->stream));
   plg::launch_gram(c->W.p, ldw, n, d, c->C.p, d, c->gscr.p, c->stream);
+  c->Cr = c->C.p;
   ++c->launches;
   const int rounds = (max_rounds < 0) ? d - 1 : std::min(max_rounds, d - 1);
   // Exact pruning needs a previous exhaustive round's knowledge and pays off above the
   // replicated small-round size.
   const bool prune = c->prune && !c->hook && d > c->prune_min_u + 1 && rounds > 1;
   c->pairs_done = 0;
-  if (prune)
+  if (prune) {
     if (int rc = reserve_prune(c, n, d, st)) return rc;
+    PLG_CUDA(c->C2.reserve(static_cast<size_t>(d) * d));
+  }
   // PLG_STAGE_LOG=<path> (analysis): per pruned stage its list length and, with detail
   // timing on, its pair-list launch time, written after the call
   static const char* stage_log = std::getenv("PLG_STAGE_LOG");
@@ -1001,14 +1010,30 @@ int causal_order_impl(plg_ctx* c, const double* dX, int64_t ldx, int64_t n, int 
     ++c->launches;
     if (u - 1 >= 2 || (u - 1 == 1 && max_rounds >= 0)) {
       // the next round's build_cache check only exists when it has >= 2 candidates
-      plg::launch_update_gram(c->C.p, d, act_nxt, u - 1, c->rs.p, c->err.p, c->stream);
-      if (prune) {
-        PLG_CUDA(cudaEventRecord(c->ev_gram, c->stream));
+      // Pruned next round: the Gram update goes to the other buffer of the ping-pong pair on
+      // the side stream (followed there by the next round's predictions), concurrently with
+      // the residualisation, which reads the pre-update Gram and recomputes each new C_rr.
+      const bool pingpong = prune && (u - 1) > c->prune_min_u;
+      const double* Cold = c->Cr;
+      if (pingpong) {
+        double* Cnew = (c->Cr == c->C.p) ? c->C2.p : c->C.p;
+        PLG_CUDA(cudaEventRecord(c->ev_commit, c->stream));
+        PLG_CUDA(cudaStreamWaitEvent(c->side, c->ev_commit, 0));
+        plg::launch_update_gram(Cold, Cnew, d, act_nxt, u - 1, c->rs.p, c->err.p, c->side);
+        PLG_CUDA(cudaEventRecord(c->ev_gram, c->side));
         c->gram_ready = true;
+        c->gram_on_side = true;
+        c->Cr = Cnew;
+      } else {
+        plg::launch_update_gram(c->Cr, c->Cr, d, act_nxt, u - 1, c->rs.p, c->err.p, c->stream);
+        if (prune) {
+          PLG_CUDA(cudaEventRecord(c->ev_gram, c->stream));
+          c->gram_ready = true;
+        }
       }
       const size_t tr = pair_timer_begin(c, 1);
-      plg::launch_resid_ent(c->W.p, ldw, n, c->C.p, d, act_nxt, u - 1, c->rs.p, c->nz.p, r + 1, c->err.p,
-                            c->hpart.p, c->g_exp, c->g_log, c->stream);
+      plg::launch_resid_ent(c->W.p, ldw, n, Cold, d, act_nxt, u - 1, c->rs.p, c->nz.p, r + 1, c->err.p,
+                            c->hpart.p, c->g_exp, c->g_log, c->stream, !pingpong);
       pair_timer_end(c, tr);
       // read w_r, write w_r for the u - 1 remaining columns, read w_m once
       c->resid_bytes += (2 * static_cast<int64_t>(u - 1) + 1) * n * static_cast<int64_t>(sizeof(double));
@@ -1284,6 +1309,7 @@ void plg_ctx_destroy(plg_ctx* c) {
   c->Xd.release();
   c->W.release();
   c->C.release();
+  c->C2.release();
   c->part.release();
   c->epack.release();
   c->H.release();
@@ -1306,6 +1332,7 @@ void plg_ctx_destroy(plg_ctx* c) {
   if (c->side) cudaStreamDestroy(c->side);
   if (c->ev_gram) cudaEventDestroy(c->ev_gram);
   if (c->ev_side) cudaEventDestroy(c->ev_side);
+  if (c->ev_commit) cudaEventDestroy(c->ev_commit);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -1361,6 +1388,7 @@ int plg_search(plg_ctx* c, const double* X, int64_t n, int32_t d, int64_t ld, co
   if (int rc = upload_iota(c, c->act0.p, u, nullptr, st)) return rc;
   PLG_CUDA(cudaMemsetAsync(c->err.p, 0xff, sizeof(unsigned long long), c->stream));
   plg::launch_gram(c->W.p, ldw, n, u, c->C.p, u, c->gscr.p, c->stream);
+  c->Cr = c->C.p;
   ++c->launches;
   if (int rc = search_round(c, n, ldw, u, u, c->act0.p, 0, st)) return rc;
   p2p_end_barrier(c);

@@ -380,7 +380,8 @@ constexpr int kResidThreads = 256;
 __global__ void __launch_bounds__(kResidThreads)
     resid_ent_kernel(double* W, int64_t ldw, int64_t n, const double* C, int64_t ldc, const int* act_nxt,
                      int ur, const RoundState* rs, int* nz, int tag, const unsigned long long* err,
-                     int64_t chunk, int nch, double* hpart, const double* g_exp, const double2* g_log) {
+                     int64_t chunk, int nch, double* hpart, const double* g_exp, const double2* g_log,
+                     int c_updated) {
   extern __shared__ __align__(128) unsigned char smem[];
   if (*err != kNoError) return;
   load_tables(smem, g_exp, g_log);
@@ -396,7 +397,10 @@ __global__ void __launch_bounds__(kResidThreads)
     const int pos = it / nch, c = it - pos * nch;
     const int r = act_nxt[pos];
     const double beta = C[static_cast<int64_t>(r) * ldc + m] / cmm;
-    const double su = kUScale / sqrt(C[static_cast<int64_t>(r) * ldc + r]);
+    const double crr = c_updated ? C[static_cast<int64_t>(r) * ldc + r]
+                                 : gram_update_entry(C[static_cast<int64_t>(r) * ldc + r], C[static_cast<int64_t>(r) * ldc + m],
+                                                     C[static_cast<int64_t>(m) * ldc + r], cmm);
+    const double su = kUScale / sqrt(crr);
     double2* wr = reinterpret_cast<double2*>(W + static_cast<int64_t>(r) * ldw);
     const int64_t t0 = c * chunk, t1 = lmin(n, t0 + chunk);  // samples; chunk is even
     EdeAcc acc;
@@ -581,7 +585,7 @@ int resid_chunks(int64_t n) { return static_cast<int>((n + kResidChunk - 1) / kR
 
 void launch_resid_ent(double* W, int64_t ldw, int64_t n, const double* C, int64_t ldc, const int* act_nxt, int ur,
                       const RoundState* rs, int* nz, int tag, const unsigned long long* err, double* hpart,
-                      const double* g_exp, const double2* g_log, cudaStream_t s) {
+                      const double* g_exp, const double2* g_log, cudaStream_t s, bool C_updated) {
   static DeviceCache gridc;
   const int grid = gridc.get([] {
     cudaFuncSetAttribute(resid_ent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTableBytes);
@@ -595,7 +599,7 @@ void launch_resid_ent(double* W, int64_t ldw, int64_t n, const double* C, int64_
   const int need = (ur * nch + kResidThreads / 32 - 1) / (kResidThreads / 32);
   const int g = need < grid ? need : grid;
   resid_ent_kernel<<<g, kResidThreads, kTableBytes, s>>>(W, ldw, n, C, ldc, act_nxt, ur, rs, nz, tag, err,
-                                                        kResidChunk, nch, hpart, g_exp, g_log);
+                                                        kResidChunk, nch, hpart, g_exp, g_log, C_updated ? 1 : 0);
 }
 
 void launch_hfin(const double* hpart, int64_t n, const double* C, int64_t ldc, const int* act, int u, double* H,

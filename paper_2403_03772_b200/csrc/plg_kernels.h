@@ -167,9 +167,11 @@ void launch_colent(const double* W, int64_t ldw, int64_t n, const double* C, int
 // H (and runs colent's zero-variance check). Rounds >= 1 of causal_order use this pair.
 constexpr int64_t kResidChunk = 1024;
 int resid_chunks(int64_t n);
+// C_updated: C already holds the updated Gram (in-place update before this launch); else C is
+// the pre-update Gram and each column's new C_rr is recomputed (gram_update_entry).
 void launch_resid_ent(double* W, int64_t ldw, int64_t n, const double* C, int64_t ldc, const int* act_nxt, int ur,
                       const RoundState* rs, int* nz, int tag, const unsigned long long* err, double* hpart,
-                      const double* g_exp, const double2* g_log, cudaStream_t s);
+                      const double* g_exp, const double2* g_log, cudaStream_t s, bool C_updated = true);
 void launch_hfin(const double* hpart, int64_t n, const double* C, int64_t ldc, const int* act, int u, double* H,
                  const int* nz, const int* col_var, int round, unsigned long long* err, cudaStream_t s);
 
@@ -291,8 +293,16 @@ void launch_commit(const double* k, const int* act_cur, int* act_nxt, int u, con
                    const unsigned long long* err, cudaStream_t s, double* round_k = nullptr,
                    const double* lb = nullptr, double* round_second = nullptr);
 
-// Rank-1 Schur update of the remaining Gram block.
-void launch_update_gram(double* C, int64_t ldc, const int* act_nxt, int ur, const RoundState* rs,
+// Rank-1 Schur update of the remaining Gram block: Cn_rs = C_rs - C_rm C_ms / C_mm (Cn == C:
+// in place; else the next round's buffer of a ping-pong pair).
+__host__ __device__ inline double gram_update_entry(double c_rs, double c_rm, double c_ms, double c_mm) {
+#ifdef __CUDA_ARCH__
+  return __dsub_rn(c_rs, __ddiv_rn(__dmul_rn(c_rm, c_ms), c_mm));
+#else
+  return c_rs - (c_rm * c_ms) / c_mm;
+#endif
+}
+void launch_update_gram(const double* C, double* Cn, int64_t ldc, const int* act_nxt, int ur, const RoundState* rs,
                         const unsigned long long* err, cudaStream_t s);
 
 

@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(kCommitThreads)
 
 // C_rs <- C_rs - (C_rm C_sm) / C_mm for the remaining r, s (bit-symmetric: the product
 // commutes). This is the Gram of the residualised columns (regress_out, ordering.cpp:178-211).
-__global__ void update_gram_kernel(double* C, int64_t ldc, const int* act_nxt, int ur,
+__global__ void update_gram_kernel(const double* C, double* Cn, int64_t ldc, const int* act_nxt, int ur,
                                    const RoundState* rs, const unsigned long long* err) {
   if (*err != kNoError) return;
   const int a = blockIdx.y * blockDim.y + threadIdx.y;
@@ -278,12 +278,13 @@ __global__ void update_gram_kernel(double* C, int64_t ldc, const int* act_nxt, i
   if (a >= ur || b >= ur) return;
   const int m = rs->chosen_col;
   const int r = act_nxt[a], s = act_nxt[b];
-  const double cmm = C[static_cast<int64_t>(m) * ldc + m];
   // C_sm read from row m (C is bit-symmetric): contiguous over s, where column m would be a
-  // strided gather; the product commutes, so C stays bit-symmetric
-  const double prod = C[static_cast<int64_t>(r) * ldc + m] * C[static_cast<int64_t>(m) * ldc + s];
-  const double v = C[static_cast<int64_t>(r) * ldc + s] - prod / cmm;
-  C[static_cast<int64_t>(r) * ldc + s] = v;
+  // strided gather; the product commutes, so C stays bit-symmetric. Cn may be C (in place)
+  // or the other buffer of a ping-pong pair (resid_ent then recomputes C_rr itself,
+  // gram_update_entry, with these exact operations).
+  Cn[static_cast<int64_t>(r) * ldc + s] =
+      gram_update_entry(C[static_cast<int64_t>(r) * ldc + s], C[static_cast<int64_t>(r) * ldc + m],
+                        C[static_cast<int64_t>(m) * ldc + s], C[static_cast<int64_t>(m) * ldc + m]);
 }
 
 // regress_out (ordering.cpp:178-211 -> kernels.cpp:106-121) with the reference's sums.
@@ -352,11 +353,11 @@ void launch_commit(const double* k, const int* act_cur, int* act_nxt, int u, con
                                              rs, err, round_k, lb, round_second);
 }
 
-void launch_update_gram(double* C, int64_t ldc, const int* act_nxt, int ur, const RoundState* rs,
+void launch_update_gram(const double* C, double* Cn, int64_t ldc, const int* act_nxt, int ur, const RoundState* rs,
                         const unsigned long long* err, cudaStream_t s) {
   const dim3 blk(32, 8);
   const dim3 grd((ur + 31) / 32, (ur + 7) / 8);
-  update_gram_kernel<<<grd, blk, 0, s>>>(C, ldc, act_nxt, ur, rs, err);
+  update_gram_kernel<<<grd, blk, 0, s>>>(C, Cn, ldc, act_nxt, ur, rs, err);
 }
 
 
