@@ -83,6 +83,17 @@ for prune in (True, False):
     out.append({"order": order, "k": [float(v).hex() for v in eng.round_k()]})
 c, s = eng.search(X, list(range(d)))
 out.append({"chosen": c, "scores": [float(v).hex() for v in s]})
+# a device-side error mid-order (an exact duplicate column: the round after its twin is
+# chosen raises ZeroVariance) must surface on every rank, collectively, without a hang
+Xd = np.asfortranarray(X.copy())
+Xd[:, d - 3] = Xd[:, 5]
+try:
+    eng.causal_order(Xd)
+    out.append({"error": None})
+except plg.Error as e:
+    out.append({"error": e.code, "col": e.col})
+order = eng.causal_order(X)  # the context stays usable
+out.append({"after_error": order == out[0]["order"]})
 print(json.dumps(out))
 """
 
@@ -111,6 +122,12 @@ def test_p2p_ranks_across_processes(plg, tmp_path, world):
         ref.append({"order": local.causal_order(X), "k": [float(v).hex() for v in local.round_k()]})
     c, s = local.search(X, list(range(d)))
     ref.append({"chosen": c, "scores": [float(v).hex() for v in s]})
+    Xd = np.asfortranarray(X.copy())
+    Xd[:, d - 3] = Xd[:, 5]
+    with pytest.raises(plg.Error) as e:
+        local.causal_order(Xd)
+    ref.append({"error": e.value.code, "col": e.value.col})
+    ref.append({"after_error": True})
     for out in outs:
         assert out == ref
 
