@@ -244,6 +244,7 @@ struct plg_ctx {
     cudaGraphExec_t exec = nullptr;
     int64_t launches = 0, pairs_done = 0, resid_bytes = 0;
     bool gram_ready = false;
+    int seen = 0;  // calls with this key so far
   } graph;
 
   size_t ev_pairs = 0;  // timing intervals recorded by this call (ev[3 + 2 i], ev[4 + 2 i])
@@ -879,8 +880,8 @@ void p2p_end_barrier(plg_ctx* c) {
 }
 
 // Graph replay of the round loop (causal_order_impl). Key: the shape, the engine knobs that
-// shape the launch sequence, and every buffer address the launches bake in. The first call of
-// a key runs the loop directly; the second captures it (stream capture of the main stream;
+// shape the launch sequence, and every buffer address the launches bake in. The first two calls
+// of a key run the loop directly; the third captures it (stream capture of the main stream;
 // the side stream joins through its events) and replays it; later calls only replay.
 template <class Loop>
 int run_rounds_graph(plg_ctx* c, int d, int64_t n, int rounds, bool prune, Loop&& run_loop, plg_status* st) {
@@ -906,13 +907,15 @@ int run_rounds_graph(plg_ctx* c, int d, int64_t n, int rounds, bool prune, Loop&
     c->gram_ready = g.gram_ready;
     return 0;
   }
-  if (!same) {  // a new key: run directly, capture on the next call with this key
+  if (!same) {  // a new key: run directly; capture once the key has been seen twice
     if (g.exec) cudaGraphExecDestroy(g.exec);
     g = plg_ctx::GraphCache{};
     g.key = key;
     g.knobs = knobs;
-    return run_loop();
   }
+  // Capturing and instantiating a fit's ~40 000 launches costs ~0.5-2 s, so only a shape that
+  // keeps coming back (third call) is captured; one-off and two-off calls launch directly.
+  if (++g.seen < 3) return run_loop();
   const int64_t l0 = c->launches, p0 = c->pairs_done, b0 = c->resid_bytes;
   PLG_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
   const bool gr0 = c->gram_ready;

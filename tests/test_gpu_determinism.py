@@ -58,7 +58,7 @@ import numpy as np
 import paper_2403_03772_b200 as plg
 eng = plg.Engine(0)
 out = []
-for seed in (21, 22, 23, 24, 25):  # one shape: call 1 runs directly, 2 captures, 3-5 replay
+for seed in (21, 22, 23, 24, 25, 26):  # one shape: calls 1-2 run directly, 3 captures, 4-6 replay
     dag = plg.gen_sparse_dag(220, avg_parents=2.0, seed=seed)
     X = plg.sample_lingam(dag, 2500, seed=seed, kind="laplace")
     order = eng.causal_order(X)

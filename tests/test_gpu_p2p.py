@@ -39,7 +39,7 @@ def test_p2p_self_exchange_matches_local(plg, prune):
         e.set_prune(prune)
     o_local = local.causal_order(X)
     k_local = [float(v).hex() for v in local.round_k()]
-    for _ in range(3):  # direct, graph capture, graph replay
+    for _ in range(4):  # direct, direct, graph capture, graph replay
         assert peer.causal_order(X) == o_local
         assert [float(v).hex() for v in peer.round_k()] == k_local
     c1, s1 = local.search(X, list(range(260)))
