@@ -355,7 +355,10 @@ def run_reference(args, world, rank):
     for _ in range(args.warmup):  # warm-up: one small faithful search round (threads, page cache)
         S = min(16, d)
         oracle_lib.search_causal_order(np.asfortranarray(X[:, :S]), list(range(S)), workers=os.cpu_count() or 1)
-    samples = [cpu_baseline(X, target_seconds=args.cpu_seconds) for _ in range(max(1, args.steps))]
+    # each step one bounded sample; the per-step budget shrinks with K so that the whole arm
+    # stays within a few minutes (the extrapolation only needs two search rounds)
+    per_step = min(args.cpu_seconds, max(3.0, 90.0 / max(1, args.steps)))
+    samples = [cpu_baseline(X, target_seconds=per_step) for _ in range(max(1, args.steps))]
     rate = float(np.median([s["value"] for s in samples]))
     wall = pair_evals(d) / rate
     line = {
