@@ -135,3 +135,46 @@ def test_sharded_round_matches_single_process(world, d, oracle):
         assert chosen == chosen_ref
         k = np.frombuffer(kb)
         assert (-k).tobytes() == scores_ref.tobytes()
+
+
+def _peer_setup_worker(rank, world, port, q):
+    # cli._setup_gpus' peer-memory path on CPU: the engine's init_peer is replaced by a stand-in
+    # that hands its 64-byte "IPC handle" to the CLI's allgather and records what comes back
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    import sys
+
+    sys.path.insert(0, ROOT)
+    from paper_2403_03772_b200 import cli
+
+    got = {}
+
+    def fake_init_peer(device, rnk, wld, max_dims, allgather):
+        got.update(device=device, rank=rnk, world=wld, max_dims=max_dims,
+                   handles=allgather(bytes([rnk]) * 64))
+
+    cli._core.init_peer = fake_init_peer
+    try:
+        cli._setup_gpus(world, 37, "p2p")
+        q.put((rank, got["device"], got["rank"], got["world"], got["max_dims"], [h[0] for h in got["handles"]],
+               [len(h) for h in got["handles"]]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_cli_peer_handle_exchange(world):
+    # every rank must receive every rank's handle, in rank order, through the host channel
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_peer_setup_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = sorted(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, device, rnk, wld, max_dims, firsts, lens in results:
+        assert (device, rnk, wld, max_dims) == (rank, rank, world, 37)
+        assert firsts == list(range(world)) and lens == [64] * world
