@@ -612,10 +612,9 @@ int search_round_pruned(plg_ctx* c, int64_t n, int64_t ldw, int d, int u, const 
       PLG_CUDA(plg::launch_prune_pairs(a, c->stream));
       pair_timer_end(c, tm);
       plg::launch_p2p_signal(a.peers, c->err.p, -1, c->stream);
-      plg::launch_p2p_wait(a.peers, c->stream);
       ++c->xchg;
-      plg::launch_prune_scatter(a, 1, 1, c->stream);  // res[k] = entry k
-      c->launches += 4;
+      plg::launch_prune_scatter(a, 1, 1, c->stream, true);  // waits for every rank; res[k] = entry k
+      c->launches += 3;
       a.res = nullptr;
       a.shard_world = 0;
     } else if (shards == 1 && !c->force_nccl) {

@@ -279,7 +279,8 @@ void launch_prune_scan(const PruneArgs& a, cudaStream_t s);
 cudaError_t launch_prune_pairs(const PruneArgs& a, cudaStream_t s);  // cooperative launch result
 // multi-rank: all ranks' results (res, `world` slots of `slot` entries; entry k of the list
 // sits at (k / cnt) slot + k % cnt with cnt = ceil(total / world)) into Md / KN
-void launch_prune_scatter(const PruneArgs& a, int world, int slot, cudaStream_t s);
+// p2p_wait: peer-memory contexts, wait for every rank's signal of this stage first
+void launch_prune_scatter(const PruneArgs& a, int world, int slot, cudaStream_t s, bool p2p_wait = false);
 // pass 0: every row's partial k L[] and k* over the top rows; 1: alive rows' L[]; 2: exact k[]
 // of the top and alive rows (+inf for pruned rows)
 void launch_prune_bound(const PruneArgs& a, int pass, cudaStream_t s);

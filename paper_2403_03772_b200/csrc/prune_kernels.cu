@@ -1109,7 +1109,11 @@ __global__ void __launch_bounds__(kListThreads, 2) prune_pairs_fine_kernel(const
 }
 
 // ---- scatter (multi-rank): every rank's results of the stage's list into Md / KN ----
-__global__ void prune_scatter_kernel(const PruneArgs a, int world, int slot) {
+__global__ void prune_scatter_kernel(const PruneArgs a, int world, int slot, int p2p_wait) {
+  if (p2p_wait) {  // peer memory: every rank's entries of this stage must be in res first
+    if (threadIdx.x == 0) p2p_wait_dev(a.peers);
+    __syncthreads();
+  }
   const int total = a.off[a.u];
   const int cnt = (total + world - 1) / world;
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < total; k += gridDim.x * blockDim.x) {
@@ -1228,8 +1232,8 @@ cudaError_t launch_prune_pairs(const PruneArgs& a, cudaStream_t s) {
   return launch_pairs_cfg<false, 5>(a, s);  // 256-bit loads: LDG.E.ENL2.256
 }
 
-void launch_prune_scatter(const PruneArgs& a, int world, int slot, cudaStream_t s) {
-  prune_scatter_kernel<<<148 * 4, 256, 0, s>>>(a, world, slot);
+void launch_prune_scatter(const PruneArgs& a, int world, int slot, cudaStream_t s, bool p2p_wait) {
+  prune_scatter_kernel<<<148 * 4, 256, 0, s>>>(a, world, slot, p2p_wait ? 1 : 0);
 }
 
 void launch_prune_bound(const PruneArgs& a, int pass, cudaStream_t s) {
