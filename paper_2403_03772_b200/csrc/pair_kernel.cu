@@ -226,8 +226,7 @@ __global__ void finalize_kernel(const PairLaunch a) {
   double* tile = a.epack + static_cast<int64_t>(a.tile_begin + tl) * 2 * kTilePairs;
   if (a.peers.n > 0) {  // every rank's copy of the table (peer memory), then p2p_signal
     peer_store(a.peers, &tile[x * kBT + y], e1);
-    peer_store(a.peers, &tile[kTilePairs + y * kBT + x], e2);
-    __threadfence_system();
+    peer_store(a.peers, &tile[kTilePairs + y * kBT + x], e2);  // published by p2p_signal after this kernel
     return;
   }
   tile[x * kBT + y] = e1;

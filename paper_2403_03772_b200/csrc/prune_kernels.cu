@@ -860,8 +860,7 @@ __device__ __forceinline__ void finalize_chunk(const PruneArgs& a, const double*
   store_pair(a, p, q, mpq);
   if (a.res) {
     if (a.peers.n > 0) {  // peer memory: entry k of the stage list at res[k] of every rank
-      peer_store(a.peers, &a.res[base + kk], mpq);
-      __threadfence_system();
+      peer_store(a.peers, &a.res[base + kk], mpq);  // published by p2p_signal after this kernel
     } else {
       a.res[a.res_base + (base + kk - kb)] = mpq;  // multi-rank (NCCL): this rank's slot
     }
@@ -895,8 +894,7 @@ __device__ __forceinline__ void finalize_chunk_fine(const PruneArgs& a, const do
   store_pair(a, p, q, mpq);
   if (a.res) {
     if (a.peers.n > 0) {  // peer memory: entry k of the stage list at res[k] of every rank
-      peer_store(a.peers, &a.res[base + kk], mpq);
-      __threadfence_system();
+      peer_store(a.peers, &a.res[base + kk], mpq);  // published by p2p_signal after this kernel
     } else {
       a.res[a.res_base + (base + kk - kb)] = mpq;  // multi-rank (NCCL): this rank's slot
     }
