@@ -333,6 +333,8 @@ __global__ void __launch_bounds__(kSelThreads) prune_select_kernel(const PruneAr
   };
   __shared__ int s_warp[kSelThreads / 32];
   __shared__ int s_cut[2];  // boundary bin, entries of it to take
+  __shared__ unsigned long long s_pw[kSelThreads];  // per-thread partial weights of its bins
+  __shared__ int s_pn[kSelThreads];                 // ... and entry counts
   extern __shared__ double s_key[];  // cache_keys: per partner, its prediction or -1 (not eligible)
   const int u = a.u;
   const bool refine = (stage != kStageProbe);
@@ -404,18 +406,35 @@ __global__ void __launch_bounds__(kSelThreads) prune_select_kernel(const PruneAr
       }
     }
     __syncthreads();
+    // Partial sums of kPerT consecutive bins per thread (top-down), in parallel: warp 0's cut
+    // search then walks 8 thread partials and at most kPerT bins instead of 65 bins per lane
+    // (it held the other warps at the barrier for ~20% of the kernel). Integer sums: the cut
+    // does not depend on the partition.
+    constexpr int kPerT = (kBins + kSelThreads - 1) / kSelThreads;  // 9
+    {
+      const int hiT = kBins - 1 - static_cast<int>(threadIdx.x) * kPerT;
+      unsigned long long pw = 0;
+      int pn = 0;
+      for (int b = hiT; b > hiT - kPerT && b >= 0; --b) {
+        if (deficit) pw += wt(b);
+        pn += hist[b];
+      }
+      s_pw[threadIdx.x] = pw;
+      s_pn[threadIdx.x] = pn;
+    }
+    __syncthreads();
     if (threadIdx.x < 32) {
       // Suffix scan from the top bin (warp 0): the bin where the cumulative weight reaches
       // need; returns false when the total falls short. cnt_above = entries in higher bins.
       auto find_cut = [&](bool weighted, unsigned long long need_total, int& bin, int& take, int& cnt_above) -> bool {
         const int lane = threadIdx.x;
-        constexpr int per = (kBins + 31) / 32;
-        const int hi = kBins - 1 - lane * per;  // lane covers bins (hi - per, hi]
+        constexpr int kT = kSelThreads / 32;  // thread partials per lane
         unsigned long long own = 0;
         int own_n = 0;
-        for (int b = hi; b > hi - per && b >= 0; --b) {
-          own += weighted ? wt(b) : static_cast<unsigned long long>(hist[b]);
-          own_n += hist[b];
+#pragma unroll
+        for (int j = 0; j < kT; ++j) {
+          own += weighted ? s_pw[lane * kT + j] : static_cast<unsigned long long>(s_pn[lane * kT + j]);
+          own_n += s_pn[lane * kT + j];
         }
         unsigned long long incl = own;
         int incl_n = own_n;
@@ -432,8 +451,15 @@ __global__ void __launch_bounds__(kSelThreads) prune_select_kernel(const PruneAr
         if (lane == src) {
           unsigned long long cum = incl - own;
           int cn = incl_n - own_n;
-          int b = hi;
-          for (;;) {
+          int t = lane * kT;
+          for (;; ++t) {  // the thread partial that reaches need
+            const unsigned long long wt_t = weighted ? s_pw[t] : static_cast<unsigned long long>(s_pn[t]);
+            if (cum + wt_t >= need_total) break;
+            cum += wt_t;
+            cn += s_pn[t];
+          }
+          int b = kBins - 1 - t * kPerT;
+          for (;;) {  // the bin within it
             const unsigned long long wb = weighted ? wt(b) : static_cast<unsigned long long>(hist[b]);
             if (cum + wb >= need_total) break;
             cum += wb;
