@@ -199,3 +199,20 @@ def test_sharded_schedule_matches_oracle_golden(world):
     k = np.array([float.fromhex(v) for v in r["k"]])
     k_ref = np.array([float.fromhex(v) for v in fx["winner_k"]])
     assert np.all(np.abs(k - k_ref) <= 1e-9 * np.abs(k_ref) + 1e-15)
+
+
+def test_long_columns_clamped_kernels():
+    # n > 90 000 selects the kernels whose exp(-2|u|) argument is clamped (|u| can leave
+    # the table's exponent range): pruned rounds against exhaustive rounds, bit for bit
+    r = _run(160, 120000, 4, "laplace", tileseg=True)
+    assert r["prune"]["order"] == r["full"]["order"]
+    assert r["prune"]["k"] == r["full"]["k"]
+
+
+def test_long_columns_match_oracle(plg):
+    import oracle_lib
+
+    dag = plg.gen_sparse_dag(36, avg_parents=2.0, seed=6)
+    X = plg.sample_lingam(dag, 120000, seed=6, kind="t3")
+    eng = plg.Engine(0)
+    assert eng.causal_order(X) == oracle_lib.causal_order(X, parallel=True, workers=os.cpu_count() or 1, fast=True)
