@@ -262,3 +262,30 @@ def test_pinv_fallback(plg, oracle):  # test_direct_lingam.cpp:96-113
     B_ref, pinv_ref = oracle.fit_weights(X, [0, 1, 2, 3])
     assert pinv and pinv_ref and np.all(np.isfinite(B))
     assert np.allclose(B, B_ref, atol=1e-6)
+
+
+def test_minimum_shapes(plg, oracle):
+    # small inputs against the oracle. Rank-deficient data (n = 2, or n <= d: after the data's
+    # rank is used up every residual is rounding noise) are excluded: there the reference
+    # raises only on an exactly zero residual and otherwise orders rounding noise, while the
+    # Gram route raises ZeroVariance as soon as a residual variance is not positive (DESIGN.md
+    # "Boundary"); both raise on exact duplicates (test_collinear_duplicate_raises).
+    rng = np.random.default_rng(31)
+    for n, d in ((3, 2), (5, 3), (4, 3), (9, 8), (140, 131)):
+        X = np.asfortranarray(rng.laplace(size=(n, d)) + rng.uniform(size=(n, d)))
+        try:
+            ref = oracle.causal_order(X)
+        except oracle.OracleError as e:  # e.g. a collinear pair at tiny n: same error expected
+            with pytest.raises(plg.Error) as g:
+                plg.causal_order(X)
+            assert g.value.code == e.code
+            continue
+        assert plg.causal_order(X) == ref, (n, d)
+    with pytest.raises(plg.Error) as e:
+        plg.causal_order(np.asfortranarray(rng.uniform(size=(1, 3))))
+    assert e.value.code == "TooFewSamples"
+    Xi = np.asfortranarray(rng.uniform(size=(10, 3)))
+    Xi[4, 1] = np.inf
+    with pytest.raises(plg.Error) as e:
+        plg.causal_order(Xi)
+    assert e.value.code == "NonFinite" and (e.value.row, e.value.col) == (4, 1)
