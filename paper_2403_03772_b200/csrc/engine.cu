@@ -3,12 +3,20 @@
 // causal_order (reference proj/src/ordering.cpp:213-244) runs here as:
 //   standardise once (bit-identical to the reference's round-0 standardize)
 //   Gram C = W^T W / n once
-//   per round (u active):  column entropies H -> pair kernel (this rank's tiles) ->
-//     finalize -> [ncclAllGather of entropy tiles] -> k reduce -> argmin/commit ->
-//     rank-1 Gram update + in-place residualisation of the u-1 remaining columns
-// Everything is enqueued on one stream without host synchronisation; the host only
-// knows u = d - round, which fixes every grid. Errors are recorded on the device in the
-// reference's raising order and reported once at the end.
+//   round 0 (and rounds with u <= 128, search, PLG_PRUNE=0): exhaustive — column entropies
+//     H -> pair kernel (this rank's tiles) -> finalize -> [exchange of the entropy tiles]
+//     -> k reduce
+//   later rounds: exact pruned round (prune_kernels.cu) — predictions and probe selection
+//     on a side stream, then probe / refinement / full stages of pair lists, each sharded
+//     over the ranks and exchanged, exact k of the surviving rows
+//   then argmin/commit -> rank-1 Gram update (ping-pong pair, side stream) + in-place
+//     residualisation of the u-1 remaining columns fused with the next round's H sums
+// Exchanges: peer memory (plg_ctx_create_p2p: stores into every rank's IPC-mapped arena +
+// a device flag barrier) or NCCL (plg_ctx_create_dist). Everything is enqueued without host
+// synchronisation (except the NCCL path's full-stage list length); the host only knows
+// u = d - round, which fixes every grid, so the whole loop is captured once into a CUDA
+// graph and replayed for later calls of the same shape. Errors are recorded on the device
+// in the reference's raising order and reported once at the end.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
