@@ -304,3 +304,58 @@ def sample_lingam(dag, n: int, seed: int, noise=(0.0, 1.0), kind: str = "uniform
                                _dp(X)):
         raise MemoryError("sample_lingam")
     return X
+
+
+# ---- the reference's own code (oracle/_ref/libplingam_ref.so, oracle/Makefile.ref): the
+# unmodified proj/src/{kernels,ordering,types,error}.cpp against a minimal Eigen stand-in ----
+
+REF_LIB_PATH = os.path.join(ORACLE_DIR, "_ref", "libplingam_ref.so")
+_ref = None
+
+
+def ref_available() -> bool:
+    return os.path.exists(REF_LIB_PATH)
+
+
+def ref_lib():
+    global _ref
+    if _ref is None:
+        L = ctypes.CDLL(REF_LIB_PATH)
+        I64 = ctypes.POINTER(ctypes.c_int64)
+        L.ref_causal_order.argtypes = [_D, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _I, _I,
+                                       I64, I64]
+        L.ref_search.argtypes = [_D, ctypes.c_int64, ctypes.c_int32, _I, ctypes.c_int32, ctypes.c_int32, _I, _D, _I,
+                                 I64, I64]
+        _ref = L
+    return _ref
+
+
+def _ref_check(rc, code, row, col, what):
+    if rc:
+        raise OracleError(code.value, row.value, col.value, f"reference {what} failed")
+
+
+def ref_causal_order(X, parallel: bool = False, workers: int = 1):
+    """plingam::causal_order (proj/src/ordering.cpp:213-244), the reference's code itself."""
+    X = _mat(X)
+    n, d = X.shape
+    order = np.zeros(max(d, 1), dtype=np.int32)
+    code, row, col = ctypes.c_int32(0), ctypes.c_int64(0), ctypes.c_int64(0)
+    rc = ref_lib().ref_causal_order(_dp(X), n, d, int(parallel), workers, _ip(order), ctypes.byref(code),
+                                    ctypes.byref(row), ctypes.byref(col))
+    _ref_check(rc, code, row, col, "causal_order")
+    return [int(v) for v in order[:d]]
+
+
+def ref_search_causal_order(X, U, workers: int = 1):
+    """plingam::search_causal_order[_parallel] (proj/src/ordering.cpp:101-176)."""
+    X = _mat(X)
+    n, d = X.shape
+    Ua = np.ascontiguousarray(U, dtype=np.int32)
+    scores = np.zeros(d, dtype=np.float64)
+    chosen = ctypes.c_int32(-1)
+    code, row, col = ctypes.c_int32(0), ctypes.c_int64(0), ctypes.c_int64(0)
+    rc = ref_lib().ref_search(_dp(X), n, d, _ip(Ua), len(Ua), workers, ctypes.byref(chosen), _dp(scores),
+                              ctypes.byref(code), ctypes.byref(row), ctypes.byref(col))
+    _ref_check(rc, code, row, col, "search_causal_order")
+    return int(chosen.value), scores

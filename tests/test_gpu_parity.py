@@ -289,3 +289,24 @@ def test_minimum_shapes(plg, oracle):
     with pytest.raises(plg.Error) as e:
         plg.causal_order(Xi)
     assert e.value.code == "NonFinite" and (e.value.row, e.value.col) == (4, 1)
+
+
+def test_orders_match_reference_code(plg):
+    # the GPU against the reference's own code (oracle/_ref: proj/src compiled unmodified
+    # against an Eigen stand-in), not only against the restatement
+    import oracle_lib
+
+    if not oracle_lib.ref_available():
+        pytest.skip("oracle/_ref not built")
+    for seed in range(42000, 42010):  # C1's validation seeds (acceptance.cpp:39-69)
+        dag = plg.gen_two_level_dag(10, seed=seed)
+        X = plg.sample_lingam(dag, 10000, seed=seed)
+        assert plg.causal_order(X) == oracle_lib.ref_causal_order(X, True, 8), seed
+    rng = np.random.default_rng(77)
+    for _ in range(4):
+        d = 5 + int(rng.uniform() * 40)
+        X = random_matrix(rng, d, 800 + int(rng.uniform() * 2000))
+        assert plg.causal_order(X) == oracle_lib.ref_causal_order(X, True, 8)
+        c_ref, s_ref = oracle_lib.ref_search_causal_order(X, list(range(d)), workers=8)
+        c, s = plg.search_causal_order(X, list(range(d)))
+        assert c == c_ref and scores_close(s, s_ref)

@@ -467,3 +467,81 @@ def test_prefix_qr_oracle_matches_per_target(oracle):
     Bt, _ = oracle.fit_weights_targets(X, order, [5, 39])
     for p in (5, 39):
         assert np.array_equal(Bt[order[p]], B1[order[p]])
+
+
+# ---------------------------------------------------------------- the reference's own code
+# oracle/_ref/libplingam_ref.so: proj/src/{kernels,ordering,types,error}.cpp compiled
+# UNMODIFIED (oracle/Makefile.ref) against a minimal Eigen stand-in (oracle/eigen_shim, glibc
+# exp/log1p). The restatement must give the reference code's bits, not just its orders.
+
+def _ref():
+    import oracle_lib
+
+    if not oracle_lib.ref_available():
+        pytest.skip("oracle/_ref not built (needs /root/reference)")
+    return oracle_lib
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_restatement_bit_identical_to_reference_code(oracle, seed):
+    ref = _ref()
+    rng = np.random.default_rng(500 + seed)
+    d = 3 + int(rng.uniform() * 30)
+    X = random_matrix(rng, d, 200 + int(rng.uniform() * 1500))
+    U = sorted(rng.choice(d, size=max(2, d - 2), replace=False).tolist())
+    c1, s1 = oracle.search_causal_order(X, U)
+    c2, s2 = ref.ref_search_causal_order(X, U)
+    assert c1 == c2 and s1.tobytes() == s2.tobytes()
+    c3, s3 = ref.ref_search_causal_order(X, U, workers=4)  # the reference's threaded path
+    assert c3 == c1 and s3.tobytes() == s1.tobytes()
+    assert oracle.causal_order(X) == ref.ref_causal_order(X) == ref.ref_causal_order(X, True, 4)
+
+
+def test_fast_and_pruned_oracle_modes_match_reference_code(oracle):
+    ref = _ref()
+    import paper_2403_03772_b200 as plg
+
+    X = two_level_data(plg, 42003, 24, 2000)
+    r = ref.ref_causal_order(X, True, 8)
+    assert oracle.causal_order(X, parallel=True, workers=8, fast=True) == r
+    assert oracle.causal_order_pruned(X, workers=8)[0] == r
+
+
+def test_goldens_against_reference_code():
+    # C1 (BASELINE configs[0], the reference's own validation seeds): every golden order is
+    # the reference code's; C2: round 0's choice and scores
+    ref = _ref()
+    import json
+    import os
+
+    import paper_2403_03772_b200 as plg
+
+    here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    g1 = json.load(open(os.path.join(here, "c1_two_level.json")))
+    for case in g1["cases"][:20]:
+        dag = plg.gen_two_level_dag(10, seed=case["seed"])
+        X = plg.sample_lingam(dag, 10000, seed=case["seed"])
+        assert ref.ref_causal_order(X) == case["order"], case["seed"]
+    g2 = json.load(open(os.path.join(here, "c2_order.json")))
+    dag = plg.gen_sparse_dag(100, avg_parents=2.0, seed=1)
+    X = plg.sample_lingam(dag, 10000, seed=1, noise=(0.0, 1.0), kind="laplace")
+    c, s = ref.ref_search_causal_order(X, list(range(100)), workers=os.cpu_count() or 1)
+    assert c == g2["order"][0]
+    assert np.array_equal(s, np.array([float.fromhex(v) if isinstance(v, str) else v for v in g2["round0_scores"]]))
+
+
+def test_reference_code_error_paths(oracle):
+    ref = _ref()
+    rng = np.random.default_rng(15)
+    X = random_matrix(rng, 3, 50)
+    Xn = X.copy(order="F")
+    Xn[7, 2] = np.nan
+    for M in (Xn,):
+        with pytest.raises(ref.OracleError) as e1:
+            ref.ref_causal_order(M)
+        with pytest.raises(ref.OracleError) as e2:
+            oracle.causal_order(M)
+        assert (e1.value.code, e1.value.row, e1.value.col) == (e2.value.code, e2.value.row, e2.value.col)
+    with pytest.raises(ref.OracleError) as e:
+        ref.ref_search_causal_order(X, [0, 0])
+    assert e.value.code == "InvalidIndex"
