@@ -153,3 +153,20 @@ def test_bench_two_ranks_on_one_gpu(tmp_path):
     assert rec["n_gpus"] == 2 and "peer memory" in rec["config"]["parallelism"]
     assert rec["pruning"]["fraction_evaluated"] < 0.2 and rec["e2e"]["h2d_bytes_per_step"] > 0
     assert out.stderr.count("peer-memory exchange") == 2
+
+
+def test_p2p_two_ranks_c3_golden(tmp_path):
+    # a BASELINE config through the peer-memory exchange across two processes (sharing cuda:0):
+    # every rank's whole C3 order and every round's winning k against the committed golden
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", str(port),
+                          os.path.join(ROOT, "tools", "p2p_scale_check.py"), "--config", "c3", "--shared-gpu"],
+                         capture_output=True, text=True, timeout=900, cwd=str(tmp_path))
+    assert out.returncode == 0, out.stderr[-3000:]
+    rec = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert rec["all_ok"] and rec["k_bits_equal_across_ranks"], rec
