@@ -9,6 +9,11 @@ script), but it simulates the product's policy and finer "stepwise" policies sid
           (deficit cut: strongest predicted partners until their predicted sum reaches
           beta x (k* - L_p); all remaining partners if the prediction falls short), then
           full rows for the survivors
+  screen  the ladder's probe (exact), then refinement stages whose pairs are screened: a
+          screened pair gives row p only min(0, M_pq + W)^2 (W: the screening kernel's error
+          bound, constant here), then optionally a screened full stage (every remaining
+          partner of the alive rows), then the exact full stage (rows still alive: every
+          partner not yet exact). Spec screen:R:T:fracs:beta:W:sfull
   step    after the same probe, every alive row takes its strongest unevaluated predicted
           partners in steps of at most S (deficit cut, at least s_min; S when the predictions
           fall short of the deficit) and is re-tested after each step, until it is pruned or
@@ -45,9 +50,11 @@ class Policy:
         self.kind = kind
         vals = rest.split(":")
         self.R, self.T = int(vals[0]), int(vals[1])
-        if kind == "ladder":
+        if kind in ("ladder", "screen"):
             self.fracs = [float(x) for x in vals[2].split(",")]
             self.beta = float(vals[3]) if len(vals) > 3 else 1.1
+            self.W = float(vals[4]) if len(vals) > 4 else 0.0
+            self.sfull = int(vals[5]) if len(vals) > 5 else 0
         else:
             self.S, self.smin = int(vals[2]), int(vals[3])
             self.beta = float(vals[4]) if len(vals) > 4 else 1.1
@@ -57,6 +64,7 @@ class Policy:
         self.stages = 0
         self.rounds = 0
         self.bad = 0
+        self.scr = 0.0  # screened pairs (screen policy)
 
     def _take(self, order_row, K_row, ev_row, need, cap):
         """strongest unevaluated partners (order_row: partner indices by prediction, strongest
@@ -93,7 +101,47 @@ class Policy:
         alive = L <= thr
         alive[top] = False
         stages = 1
-        if self.kind == "ladder":
+        if self.kind == "screen":
+            Mrow = self.M  # row p's M_pq
+            Cs = np.minimum(Mrow + self.W, 0.0) ** 2  # lower bound of row p's contribution from a screened pair
+            sc = np.zeros((u, u), dtype=bool)
+
+            def lower():
+                return np.where(ev, C, np.where(sc, Cs, 0.0)).sum(1)
+
+            prev = 0.0
+            for f in self.fracs:
+                idx = np.nonzero(alive)[0]
+                if idx.size:
+                    cap = max(1, int((f - prev) * u))
+                    orders = np.argsort(-K[idx], axis=1, kind="stable")
+                    done = ev | sc
+                    for i, pp in enumerate(idx):
+                        sel = self._take(orders[i], K[pp], done[pp], self.beta * (thr - L[pp]), cap)
+                        sel = sel[sel != pp]
+                        sc[pp, sel] = True
+                        sc[sel, pp] = True
+                    np.fill_diagonal(sc, False)
+                    L = lower()
+                    alive &= L <= thr
+                stages += 1
+                prev = f
+            if self.sfull:
+                idx = np.nonzero(alive)[0]
+                sc[idx, :] = True
+                sc[:, idx] = True
+                np.fill_diagonal(sc, False)
+                L = lower()
+                alive &= L <= thr
+                stages += 1
+            idx = np.nonzero(alive)[0]
+            ev[idx, :] = True
+            ev[:, idx] = True
+            np.fill_diagonal(ev, False)
+            stages += 1
+            self.scr += np.triu(sc & ~ev, 1).sum() + np.triu(sc & ev, 1).sum()
+            ev_all = ev | sc
+        elif self.kind == "ladder":
             prev = 0.0
             for f in self.fracs:
                 idx = np.nonzero(alive)[0]
@@ -135,6 +183,8 @@ class Policy:
                 stages += 1
                 if stages > 10000:
                     break
+        if self.kind != "screen":
+            ev_all = ev
         tot = np.triu(ev, 1).sum()
         full_rows = ev.sum(1) == u - 1
         if not (full_rows[best] or best in set(top.tolist())):
@@ -144,7 +194,7 @@ class Policy:
         self.stages += stages
         self.rounds += 1
         sub = self.known[np.ix_(act, act)]
-        sub[ev] = C[ev]
+        sub[ev_all] = C[ev_all]
         self.known[np.ix_(act, act)] = sub
         return {"frac": float(tot / (u * (u - 1) / 2)), "stages": stages}
 
@@ -166,6 +216,8 @@ class Sim:
         np.fill_diagonal(M, 0.0)
         C = np.minimum(M, 0.0) ** 2
         best = int(np.argmin(k))
+        for p in self.policies:
+            p.M = M
         res = [p.round(u, act, C, k, best) for p in self.policies] if rnd > 0 else []
         if rnd == 0:  # round 0 is exhaustive in the product: every pair becomes known
             for p in self.policies:
@@ -216,6 +268,7 @@ def main():
     assert rc == 0, st.msg
     out = {"config": args.config, "d": d, "n": n, "seconds": time.time() - t0,
            "policies": [{"spec": p.spec, "weighted_frac_pairs": p.pairs / max(p.full, 1),
+                         "exact_pairs": float(p.pairs), "screened_pairs": float(p.scr),
                          "stages_per_round": p.stages / max(p.rounds, 1), "winner_lost": p.bad}
                         for p in policies],
            "log": sim.log}
