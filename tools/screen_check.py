@@ -1,8 +1,8 @@
-"""Screened refinement stages against the goldens (analysis): for each config, the causal
-order with the current engine knobs (PLG_SCREEN, PLG_SCREEN_SEGLEN, ...), checked against
+"""An engine variant against the goldens (analysis): for each config, the causal order with
+the engine knobs of the environment (or an experimental build, e.g. the screening patch in
+profiles/r2_screening_experiment.patch with PLG_SCREEN=1), checked against
 tests/golden/<config>_order_full.json (order; every round's winning k within 1e-9 rel.),
-with the median device time and the pair counts (engine knobs from the environment, e.g. an
-experimental variant applied from a patch).
+with the median device time and the pair counts.
 
     python tools/screen_check.py --configs c3,c5 --reps 3
 """
