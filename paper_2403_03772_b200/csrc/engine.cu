@@ -262,6 +262,7 @@ struct plg_ctx {
   int tag_round = 0, tag_stage = -1;
   std::vector<double> last_k, last_second;  // per round of the last causal_order: winner's k, runner-up's
   int64_t resid_bytes = 0;    // algorithmic HBM bytes of the residualisations of this call
+  double emu_ms = 0.0;        // detail timing: emulated-rank bookkeeping launches (PLG_EMULATE_WORLD)
 
   cudaError_t events(size_t count) {
     while (ev.size() < count) {
@@ -662,8 +663,11 @@ int search_round_pruned(plg_ctx* c, int64_t n, int64_t ldw, int d, int u, const 
           a.k_end = ke;
           a.res_base = kb;  // = r * slot
         }
-        if (r > (real ? c->rank : 0))  // emulated ranks share one set of fetch counters
+        if (r > (real ? c->rank : 0)) {  // emulated ranks share one set of fetch counters
+          const size_t te = pair_timer_begin(c, 2);  // emulation-only cost (kind 2: not pair time)
           PLG_CUDA(cudaMemsetAsync(c->pwork.p, 0, (slot / c->prune_batch + 2) * sizeof(int), c->stream));
+          pair_timer_end(c, te);
+        }
         const size_t tm = pair_timer_begin(c);
         PLG_CUDA(plg::launch_prune_pairs(a, c->stream));
         pair_timer_end(c, tm);
@@ -826,10 +830,13 @@ void finish_stats(plg_ctx* c, int64_t n, int d, int rounds, bool host_in) {
   }
   double pair_ms = 0.0, resid_ms = 0.0;
   int64_t pl = 0;
+  c->emu_ms = 0.0;
   for (size_t i = 0; i < c->ev_pairs; ++i) {
     if (cudaEventElapsedTime(&ms, c->ev[3 + 2 * i], c->ev[4 + 2 * i]) != cudaSuccess) continue;
     if (c->ev_kind[i] == 1) {
       resid_ms += ms;
+    } else if (c->ev_kind[i] == 2) {
+      c->emu_ms += ms;  // an emulated rank schedule's own overhead (not pair evaluation)
     } else {
       pair_ms += ms;
       ++pl;
@@ -1094,21 +1101,28 @@ int causal_order_impl(plg_ctx* c, const double* dX, int64_t ldx, int64_t n, int 
   if (stage_log && prune) {
     std::vector<int> lens(static_cast<size_t>(d) * plg::kMaxPruneStages);
     PLG_CUDA(cudaMemcpy(lens.data(), c->stage_log.p, lens.size() * sizeof(int), cudaMemcpyDeviceToHost));
-    std::vector<float> ms_of(lens.size(), -1.f);
+    // per (round, stage): pair-list launch time summed over the stage's launches, and the
+    // longest single launch (an emulated W-rank schedule runs one launch per rank slice, so
+    // the maximum is the stage's pair time on the slowest rank: tools/scale_projection.py)
+    std::vector<float> ms_of(lens.size(), -1.f), ms_max(lens.size(), -1.f);
     for (size_t i = 0; i < c->ev_pairs && i < c->ev_tag.size(); ++i) {
       const int t = c->ev_tag[i];
       if (t < 0) continue;
       const size_t slot = static_cast<size_t>(t / 16) * plg::kMaxPruneStages + t % 16;
       float ms = 0.f;
-      if (slot < ms_of.size() && cudaEventElapsedTime(&ms, c->ev[3 + 2 * i], c->ev[4 + 2 * i]) == cudaSuccess)
+      if (slot < ms_of.size() && cudaEventElapsedTime(&ms, c->ev[3 + 2 * i], c->ev[4 + 2 * i]) == cudaSuccess) {
         ms_of[slot] = (ms_of[slot] < 0.f ? 0.f : ms_of[slot]) + ms;
+        ms_max[slot] = std::max(ms_max[slot], ms);
+      }
     }
     if (FILE* f = std::fopen(stage_log, "w")) {
       for (int r = 0; r < rounds; ++r)
         for (int s = 0; s < plg::kMaxPruneStages; ++s) {
           const size_t slot = static_cast<size_t>(r) * plg::kMaxPruneStages + s;
-          if (lens[slot] >= 0) std::fprintf(f, "%d %d %d %d %.5f\n", r, d - r, s, lens[slot], ms_of[slot]);
+          if (lens[slot] >= 0)
+            std::fprintf(f, "%d %d %d %d %.5f %.5f\n", r, d - r, s, lens[slot], ms_of[slot], ms_max[slot]);
         }
+      std::fprintf(f, "# emulate_world %d emu_ms %.5f\n", c->emulate_world, c->emu_ms);
       std::fclose(f);
     }
   }

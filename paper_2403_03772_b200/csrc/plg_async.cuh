@@ -8,6 +8,13 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// GPU-scope release / acquire fences for the last-finisher pattern (a warp's partial sums
+// released before its counter increment; the warp that completes the count acquires them).
+// __threadfence() is fence.sc, which also invalidates the SM's L1 (CCTL.IVALL) on every call;
+// the release side needs neither (MEMBAR.ALL.GPU only).
+__device__ __forceinline__ void fence_release_gpu() { asm volatile("fence.release.gpu;" ::: "memory"); }
+__device__ __forceinline__ void fence_acquire_gpu() { asm volatile("fence.acquire.gpu;" ::: "memory"); }
+
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
 }

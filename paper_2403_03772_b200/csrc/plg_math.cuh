@@ -83,18 +83,41 @@ constexpr int kMinScaledK = -100 * kExpN;
 
 // Fill the shared-memory tables (every thread of the block, then __syncthreads()).
 // g_exp: kExpN doubles; g_log: kLogMasterN double2 (host-computed in long double).
+// Every thread issues all of its master-copy loads before its first shared store (one L2
+// round trip per launch instead of one per entry batch: the fill sits at the start of every
+// launch, before any work item, and each pair-list launch pays it).
+__device__ __forceinline__ double2 log_master_row(const double2* g_log, int row) {
+  double2 v = make_double2(0.0, 0.0);
+  if (row == 0) v = g_log[kLogMasterN - 1];
+  else if (row >= 128) v = g_log[row - 128];
+  return v;
+}
 __device__ __forceinline__ void load_tables_into(unsigned char* exp_tab, unsigned char* log_tab, const double* g_exp,
                                                  const double2* g_log) {
   double* e = reinterpret_cast<double*>(exp_tab);
-  for (int i = threadIdx.x; i < kExpN * kExpRep; i += blockDim.x) e[i] = g_exp[i / kExpRep];
   double2* l = reinterpret_cast<double2*>(log_tab);
-  for (int i = threadIdx.x; i < kLogRows * kLogRep; i += blockDim.x) {
-    const int row = i / kLogRep;
-    double2 v = make_double2(0.0, 0.0);
-    if (row == 0) v = g_log[kLogMasterN - 1];
-    else if (row >= 128) v = g_log[row - 128];
-    l[i] = v;
+  constexpr int kNe = kExpN * kExpRep, kNl = kLogRows * kLogRep;  // 2048 each
+  constexpr int kPer = 8;
+  const int bd = blockDim.x;
+  if (bd * kPer >= kNe && bd * kPer >= kNl) {
+    double ev[kPer];
+    double2 lv[kPer];
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int i = threadIdx.x + k * bd;
+      if (i < kNe) ev[k] = g_exp[i / kExpRep];
+      if (i < kNl) lv[k] = log_master_row(g_log, i / kLogRep);
+    }
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int i = threadIdx.x + k * bd;
+      if (i < kNe) e[i] = ev[k];
+      if (i < kNl) l[i] = lv[k];
+    }
+    return;
   }
+  for (int i = threadIdx.x; i < kNe; i += bd) e[i] = g_exp[i / kExpRep];
+  for (int i = threadIdx.x; i < kNl; i += bd) l[i] = log_master_row(g_log, i / kLogRep);
 }
 __device__ __forceinline__ void load_tables(unsigned char* s_tab, const double* g_exp,
                                             const double2* g_log) {

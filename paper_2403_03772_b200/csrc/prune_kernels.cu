@@ -1002,13 +1002,13 @@ __global__ void __launch_bounds__(kListThreads, 2) prune_pairs_kernel(const Prun
         __stcg(dst, make_double2(acc_lc(acc1), acc_pdf(acc1)));
         __stcg(dst + 1, make_double2(acc_lc(acc2), acc_pdf(acc2)));
       }
-      __threadfence();  // release this segment's partials before counting it
+      fence_release_gpu();  // release this segment's partials before counting it (no L1 invalidation)
       __syncwarp();
       int last = 0;
       if (lane == 0) last = (atomicAdd(&a.done[chunk], 1) == a.nseg - 1);
       last = __shfl_sync(0xffffffffu, last, 0);
       if (last) {
-        __threadfence();  // acquire the other segments' partials
+        fence_acquire_gpu();  // acquire the other segments' partials
         finalize_chunk(a, a.part, base, m, chunk, lane, kb);
         if (lane == 0) a.done[chunk] = 0;  // ready for the next batch / launch
       }
@@ -1116,14 +1116,14 @@ __global__ void __launch_bounds__(kListThreads, 2) prune_pairs_fine_kernel(const
         __stcg(dst, make_double2(acc_lc(acc1), acc_pdf(acc1)));
         __stcg(dst + 1, make_double2(acc_lc(acc2), acc_pdf(acc2)));
       }
-      __threadfence();  // release this segment's partials before counting it
+      fence_release_gpu();  // release this segment's partials before counting it (no L1 invalidation)
       __syncwarp();
       nseg = kFine ? vseg[1] : a.nseg;
       int last = 0;
       if (lane == 0) last = (atomicAdd(&a.done[chunk], 1) == nseg - 1);
       last = __shfl_sync(0xffffffffu, last, 0);
       if (last) {
-        __threadfence();  // acquire the other segments' partials
+        fence_acquire_gpu();  // acquire the other segments' partials
         finalize_chunk_fine(a, a.part, base, m, chunk, lane, kb, nseg,
                        kFine ? static_cast<int64_t>(*vps) : static_cast<int64_t>(a.batch));
         if (lane == 0) a.done[chunk] = 0;  // ready for the next batch / launch

@@ -44,7 +44,9 @@ def main():
         rounds[int(r)] = (int(u), float(ms))
     stages = defaultdict(dict)
     for line in open(slog):
-        r, u, s, n, ms = line.split()
+        if line.startswith("#"):
+            continue
+        r, u, s, n, ms = line.split()[:5]
         stages[int(r)][int(s)] = (int(n), float(ms))
     edges = [int(x) for x in args.buckets.split(",")]
     print(f"{'u range':>12} {'rounds':>6} {'dev ms':>9} {'pair ms':>9} {'other ms':>9} "
