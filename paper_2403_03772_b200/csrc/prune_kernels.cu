@@ -960,11 +960,10 @@ __global__ void __launch_bounds__(kListThreads, 2) prune_pairs_kernel(const Prun
     const int m = min(a.batch, total - b * a.batch);
     const int chunks = (m + 31) / 32;
     const int items = chunks * a.nseg;
-    while (!skip) {
-      int it = 0;
-      if (lane == 0) it = atomicAdd(&a.work[b], 1);
-      it = __shfl_sync(0xffffffffu, it, 0);
-      if (it >= items) break;
+    int it = 0;
+    if (lane == 0 && !skip) it = atomicAdd(&a.work[b], 1);
+    it = __shfl_sync(0xffffffffu, it, 0);
+    while (!skip && it < items) {
       int chunk, seg;
       if (a.seg_major) {  // a sample window of every chunk at a time: column slices stay in L2
         seg = it / chunks;
@@ -1004,9 +1003,14 @@ __global__ void __launch_bounds__(kListThreads, 2) prune_pairs_kernel(const Prun
       }
       fence_release_gpu();  // release this segment's partials before counting it (no L1 invalidation)
       __syncwarp();
-      int last = 0;
-      if (lane == 0) last = (atomicAdd(&a.done[chunk], 1) == a.nseg - 1);
+      // the segment count and the next item's fetch go out together: one L2 round trip per item
+      int last = 0, next = 0;
+      if (lane == 0) {
+        last = (atomicAdd(&a.done[chunk], 1) == a.nseg - 1);
+        next = atomicAdd(&a.work[b], 1);
+      }
       last = __shfl_sync(0xffffffffu, last, 0);
+      it = __shfl_sync(0xffffffffu, next, 0);
       if (last) {
         fence_acquire_gpu();  // acquire the other segments' partials
         finalize_chunk(a, a.part, base, m, chunk, lane, kb);
@@ -1072,10 +1076,10 @@ __global__ void __launch_bounds__(kListThreads, 2) prune_pairs_fine_kernel(const
     const int base = kb + b * a.batch;
     const int m = min(a.batch, total - b * a.batch);
     const int chunks = (m + 31) / 32;
+    int it = 0;
+    if (lane == 0 && !skip) it = atomicAdd(&a.work[b], 1);
+    it = __shfl_sync(0xffffffffu, it, 0);
     while (!skip) {
-      int it = 0;
-      if (lane == 0) it = atomicAdd(&a.work[b], 1);
-      it = __shfl_sync(0xffffffffu, it, 0);
       int nseg = kFine ? vseg[1] : a.nseg;
       if (it >= chunks * nseg) break;
       int chunk, seg;
@@ -1119,9 +1123,13 @@ __global__ void __launch_bounds__(kListThreads, 2) prune_pairs_fine_kernel(const
       fence_release_gpu();  // release this segment's partials before counting it (no L1 invalidation)
       __syncwarp();
       nseg = kFine ? vseg[1] : a.nseg;
-      int last = 0;
-      if (lane == 0) last = (atomicAdd(&a.done[chunk], 1) == nseg - 1);
+      int last = 0, next = 0;
+      if (lane == 0) {  // the segment count and the next item's fetch in one round trip
+        last = (atomicAdd(&a.done[chunk], 1) == nseg - 1);
+        next = atomicAdd(&a.work[b], 1);
+      }
       last = __shfl_sync(0xffffffffu, last, 0);
+      it = __shfl_sync(0xffffffffu, next, 0);
       if (last) {
         fence_acquire_gpu();  // acquire the other segments' partials
         finalize_chunk_fine(a, a.part, base, m, chunk, lane, kb, nseg,
