@@ -350,6 +350,26 @@ void parse_prune_env(plg_ctx* ctx) {
   if (const char* v = std::getenv("PLG_GRAPHS")) ctx->use_graphs = std::atoi(v) != 0;
 }
 
+// Refinement ladder of a multi-rank context. Every stage costs each rank the pair-list
+// launch's fixed ~43 us plus its selection, scan and bound launches whatever its slice, so
+// with the pairs split 8 ways fewer, larger stages win: one refinement step to a quarter of
+// the row, and two probe suspects per row. C5 projected on one B200
+// (tools/scale_projection.py, profiles/r2_scale_projection.jsonl): 1 036 ms against 1 101 ms
+// with the single-GPU ladder at 8 ranks, but 1 412 / 2 166 ms against 1 381 / 1 960 ms at
+// 4 / 2 ranks, hence from 8 ranks (PLG_RANK_LADDER_MIN_WORLD overrides the threshold). The
+// ladder only chooses which pairs are evaluated: the order and every winning k keep their
+// bits. PLG_PRUNE overrides it.
+void multi_rank_ladder(plg_ctx* ctx) {
+  static const int min_world = [] {
+    const char* v = std::getenv("PLG_RANK_LADDER_MIN_WORLD");
+    return v ? std::max(2, std::atoi(v)) : 8;
+  }();
+  if (ctx->world < min_world || std::getenv("PLG_PRUNE")) return;
+  ctx->prune_R = 3;
+  ctx->prune_T = 2;
+  ctx->prune_fracs = {0.25};
+}
+
 int ctx_init(plg_ctx* ctx, int device, plg_status* st) {
   ctx->device = device;
   parse_prune_env(ctx);
@@ -1243,6 +1263,7 @@ int plg_ctx_create_dist(int32_t device, int32_t rank, int32_t world, const void*
   }
   c->rank = rank;
   c->world = world;
+  multi_rank_ladder(c);
   *out = c;
   return ok(st);
 }
@@ -1260,6 +1281,7 @@ int plg_ctx_create_p2p(int32_t device, int32_t rank, int32_t world, int32_t max_
   if (!rc) {
     c->rank = rank;
     c->world = world;
+    multi_rank_ladder(c);
     c->p2p = true;
     c->p2p_max_dims = max_dims;
     // pres: one stage list (u (u - 1) entries + slack); epack: every tile of round 0 at the

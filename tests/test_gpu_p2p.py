@@ -6,9 +6,11 @@ B200 two ways:
 
 * a one-rank peer context routes every exchange through its own arena (in-process): same
   order and winning-k bits as a local context, pruned and exhaustive rounds, search scores;
-* two and three processes on the same GPU, each a rank of a world-2/3 context, arenas mapped across
-  processes with CUDA IPC (the mechanism used between GPUs over NVLink), handles exchanged
-  through files: every rank returns the single-rank order and winning-k bits.
+* two, three and four processes on the same GPU, each a rank of a world-2/3/4 context, arenas
+  mapped across processes with CUDA IPC (the mechanism used between GPUs over NVLink), handles
+  exchanged through files: every rank returns the single-rank order and winning-k bits (at
+  four ranks with the multi-rank refinement ladder, which changes only which pairs are
+  evaluated).
 """
 
 import json
@@ -98,11 +100,13 @@ print(json.dumps(out))
 """
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 4])  # 4: with the multi-rank refinement ladder (engine.cu multi_rank_ladder)
 def test_p2p_ranks_across_processes(plg, tmp_path, world):
     d, n, seed = 200, 2000, 29
     src = _RANK % (ROOT, d, n, seed)
-    procs = [subprocess.Popen([sys.executable, "-c", src, str(r), str(world), str(tmp_path)],
+    # at 4 ranks the multi-rank refinement ladder (default from 8 ranks) is switched on
+    env = dict(os.environ, PLG_RANK_LADDER_MIN_WORLD="4") if world == 4 else None
+    procs = [subprocess.Popen([sys.executable, "-c", src, str(r), str(world), str(tmp_path)], env=env,
                               stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True) for r in range(world)]
     outs = []
     for p in procs:

@@ -114,14 +114,14 @@ def main():
             raise SystemExit(f"child failed: {cmd}")
         return json.loads([x for x in p.stdout.splitlines() if x.startswith("{")][-1])
 
-    # the single-GPU base and the exchange cost use the default segmentation; PLG_PRUNE_SEGLEN
-    # (if set) applies to the emulated W-rank runs only
-    seg = os.environ.pop("PLG_PRUNE_SEGLEN", None)
+    # the single-GPU base and the exchange cost use the default engine; PLG_PRUNE_SEGLEN and
+    # PLG_PRUNE (the refinement ladder), if set, apply to the emulated W-rank runs only
+    emu_env = {k: os.environ.pop(k) for k in ("PLG_PRUNE_SEGLEN", "PLG_PRUNE") if k in os.environ}
+    seg = emu_env or None
     base = run(1)
     base["graph_ms"] = run(1, graph=True)["graph_ms"]
     peer = run(1, peer=True)
-    if seg is not None:
-        os.environ["PLG_PRUNE_SEGLEN"] = seg
+    os.environ.update(emu_env)
     peer_overhead = max(0.0, peer["total_ms"] - base["total_ms"])
     per_stage_xchg = peer_overhead / max(1, base["stages"])
     # Base: the production single-GPU device time (graph-replayed, no per-launch events).
@@ -133,10 +133,12 @@ def main():
         r = base if (w == 1 and seg is None) else run(w)
         assert r["order_head"] == base["order_head"], "emulated schedule changed the order"
         xchg = 0.0 if w == 1 else r["stages"] * (per_stage_xchg + args.nvlink_us * 1e-3)
+        # (per-stage exchange cost measured with the default ladder, charged per stage of this one)
         t = t1 - base["stage_sum_ms"] + r["stage_max_ms"] - base["round0_ms"] * (1.0 - 1.0 / w) + xchg
         t_detail = (r["total_ms"] - (r["stage_sum_ms"] - r["stage_max_ms"]) - r["emu_ms"]
                     - r["round0_ms"] * (1.0 - 1.0 / w) + xchg)
         print(json.dumps({"config": args.config, "world": w, "seg_len": os.environ.get("PLG_PRUNE_SEGLEN", "128"),
+                          "ladder": os.environ.get("PLG_PRUNE", "default"),
                           "projected_ms": round(t, 2), "speedup_vs_1": round(t1 / t, 3),
                           "base_graph_ms": round(t1, 2), "projected_ms_detail_basis": round(t_detail, 2),
                           "total_ms_emulated": round(r["total_ms"], 2),
