@@ -210,6 +210,8 @@ struct plg_ctx {
   int prune_R = 3;
   int prune_T = 1;
   std::vector<double> prune_fracs{0.05, 0.25};
+  bool ladder_env = false;         // PLG_PRUNE gave the ladder: used for every round
+  double ladder_switch = 5e5;      // PLG_LADDER_SWITCH: rounds with u^2 / ranks below it use the short ladder
   bool prune_tile_seg = false;  // PLG_PRUNE_TILESEG=1: the exhaustive rounds' segmentation (bit-identity tests)
   int emulate_world = 1;        // PLG_EMULATE_WORLD=W (tests): a single rank runs the W-rank shard schedule
   double prune_beta = 1.1;      // PLG_PRUNE_BETA > 0: hybrid refinement (deficit cut when smaller than the step)
@@ -329,6 +331,7 @@ void parse_prune_env(plg_ctx* ctx) {
       if (sscanf(v, "%d:%d:%n", &R, &T, &used) == 2 && R >= 1 && T >= 1) {
         ctx->prune_R = R;
         ctx->prune_T = T;
+        ctx->ladder_env = true;
         ctx->prune_fracs.clear();
         const char* f = v + used;
         while (*f) {
@@ -342,32 +345,13 @@ void parse_prune_env(plg_ctx* ctx) {
     }
   }
   if (const char* v = std::getenv("PLG_PRUNE_TILESEG")) ctx->prune_tile_seg = !strcmp(v, "1");
+  if (const char* v = std::getenv("PLG_LADDER_SWITCH")) ctx->ladder_switch = std::atof(v);
   if (const char* v = std::getenv("PLG_EMULATE_WORLD")) ctx->emulate_world = std::max(1, std::atoi(v));
   if (const char* v = std::getenv("PLG_PRUNE_BETA")) ctx->prune_beta = std::atof(v);
   if (const char* v = std::getenv("PLG_PRUNE_SUB")) ctx->prune_sub = std::max<int64_t>(0, std::atoll(v));
   if (const char* v = std::getenv("PLG_PRUNE_MIN_U")) ctx->prune_min_u = std::max(8, std::atoi(v));
   if (const char* v = std::getenv("PLG_PRUNE_BATCH")) ctx->prune_batch = std::max(64, std::atoi(v) / 32 * 32);
   if (const char* v = std::getenv("PLG_GRAPHS")) ctx->use_graphs = std::atoi(v) != 0;
-}
-
-// Refinement ladder of a multi-rank context. Every stage costs each rank the pair-list
-// launch's fixed ~43 us plus its selection, scan and bound launches whatever its slice, so
-// with the pairs split 8 ways fewer, larger stages win: one refinement step to a quarter of
-// the row, and two probe suspects per row. C5 projected on one B200
-// (tools/scale_projection.py, profiles/r2_scale_projection.jsonl): 1 036 ms against 1 101 ms
-// with the single-GPU ladder at 8 ranks, but 1 412 / 2 166 ms against 1 381 / 1 960 ms at
-// 4 / 2 ranks, hence from 8 ranks (PLG_RANK_LADDER_MIN_WORLD overrides the threshold). The
-// ladder only chooses which pairs are evaluated: the order and every winning k keep their
-// bits. PLG_PRUNE overrides it.
-void multi_rank_ladder(plg_ctx* ctx) {
-  static const int min_world = [] {
-    const char* v = std::getenv("PLG_RANK_LADDER_MIN_WORLD");
-    return v ? std::max(2, std::atoi(v)) : 8;
-  }();
-  if (ctx->world < min_world || std::getenv("PLG_PRUNE")) return;
-  ctx->prune_R = 3;
-  ctx->prune_T = 2;
-  ctx->prune_fracs = {0.25};
 }
 
 int ctx_init(plg_ctx* ctx, int device, plg_status* st) {
@@ -531,6 +515,31 @@ int search_round(plg_ctx* c, int64_t n, int64_t ldw, int ldc, int u, const int* 
 // One exact pruned round (prune_kernels.cu): same chosen root and winner-k bits as
 // search_round, evaluating only the pairs needed to prove the argmin. Needs KN from an
 // earlier round of the same run.
+// The refinement ladder of one pruned round. Every stage costs each rank a pair-list launch
+// with a fixed ~43 us (its end-of-launch drain, profiles/r2_list_launch_cost.md) plus its
+// selection, scan and bound launches, whatever the rank's share of the list; a stage's pair
+// work is ~u^2 / ranks. Where that work is small — u^2 / ranks < ladder_switch — fewer, larger
+// stages win: the short ladder (three top rows, two probe suspects per row, one refinement
+// step to a quarter of the row) evaluates more pairs in 3 stages instead of 4. Measured on
+// one B200: C3 494 -> 454 ms, C4 89 -> 74 ms, C5 3 001 -> 2 988 ms (tools/ab_time.py), and
+// under tools/scale_projection.py (profiles/r2_scale_ladders.jsonl) C5 at 8 ranks 1 036 vs
+// 1 101 ms, C3 at 2 / 4 / 8 ranks 407 / 342 / 293 vs 423 / 378 / 367 ms. The ladder only
+// chooses which pairs are evaluated; each pair's bits are a function of (u, n) — except in the
+// short-list kernel, whose segmentation follows the list's length — so where that kernel runs
+// the switch ignores the rank count, and the order and every winning k stay bit-identical for
+// any number of ranks. A ladder given by PLG_PRUNE is used for every round.
+struct RoundLadder {
+  int R, T;
+  const std::vector<double>* fracs;
+};
+RoundLadder round_ladder(const plg_ctx* c, int64_t n, int u, int fine_items) {
+  static const std::vector<double> kShortFracs{0.25};
+  const int shards = c->world > 1 ? c->world : c->emulate_world;
+  const int per = plg::prune_short_list_kernel(u, n, fine_items) ? 1 : shards;
+  if (!c->ladder_env && static_cast<double>(u) * u / per < c->ladder_switch) return {3, 2, &kShortFracs};
+  return {c->prune_R, c->prune_T, &c->prune_fracs};
+}
+
 int search_round_pruned(plg_ctx* c, int64_t n, int64_t ldw, int d, int u, const int* act_cur, int round,
                         plg_status* st, bool h_from_resid = true) {
   // The predictions, the top rows and the probe selection need the Gram update, the active
@@ -601,7 +610,8 @@ int search_round_pruned(plg_ctx* c, int64_t n, int64_t ldw, int d, int u, const 
   a.state_in = sa;
   a.state_out = sa;
   plg::launch_prune_predict(a, ps);
-  plg::launch_prune_top(a, c->prune_R, ps);
+  const RoundLadder lad = round_ladder(c, n, u, a.fine_items);
+  plg::launch_prune_top(a, lad.R, ps);
   c->launches += 2;
   int stage_idx = 0;
   const int shards = c->world > 1 ? c->world : c->emulate_world;
@@ -660,7 +670,7 @@ int search_round_pruned(plg_ctx* c, int64_t n, int64_t ldw, int d, int u, const 
       // synchronisation; the full stage reads the length first (plg_plan_list_shard).
       const bool real = c->world > 1 || c->force_nccl;  // else: emulated ranks, one after the other
       int64_t bound = -1;
-      if (kind == plg::kStageProbe) bound = static_cast<int64_t>(c->prune_R + c->prune_T) * u;
+      if (kind == plg::kStageProbe) bound = static_cast<int64_t>(lad.R + lad.T) * u;
       else if (kind == plg::kStageRefine && m > 0) bound = static_cast<int64_t>(u) * m;
       int32_t slot = 0, kb = 0, ke = 0, total = -1;
       if (bound >= 0) {
@@ -715,11 +725,11 @@ int search_round_pruned(plg_ctx* c, int64_t n, int64_t ldw, int d, int u, const 
     }
     return 0;
   };
-  if (int rc = stage(plg::kStageProbe, c->prune_T, 0.0, 0)) return rc;
+  if (int rc = stage(plg::kStageProbe, lad.T, 0.0, 0)) return rc;
   // refinement ladder: values < 1 are cumulative fractions of the row (count mode: the step
   // to the next fraction), values >= 1 deficit multipliers (prune_kernels.cu select)
   double prev = 0.0;
-  for (double f : c->prune_fracs) {
+  for (double f : *lad.fracs) {
     if (f >= 1.0) {
       if (int rc = stage(plg::kStageRefine, 0, f, 1)) return rc;
     } else {
@@ -931,6 +941,8 @@ int run_rounds_graph(plg_ctx* c, int d, int64_t n, int rounds, bool prune, Loop&
                                c->p2p ? 1.0 : 0.0, static_cast<double>(c->world), static_cast<double>(c->rank)};
   key.push_back(c->arena);
   for (double f : c->prune_fracs) knobs.push_back(f);
+  knobs.push_back(c->ladder_env ? -1.0 : c->ladder_switch);
+  knobs.push_back(static_cast<double>(c->emulate_world));
   plg_ctx::GraphCache& g = c->graph;
   const bool same = g.key == key && g.knobs == knobs;
   if (same && g.exec) {
@@ -1263,7 +1275,6 @@ int plg_ctx_create_dist(int32_t device, int32_t rank, int32_t world, const void*
   }
   c->rank = rank;
   c->world = world;
-  multi_rank_ladder(c);
   *out = c;
   return ok(st);
 }
@@ -1281,7 +1292,6 @@ int plg_ctx_create_p2p(int32_t device, int32_t rank, int32_t world, int32_t max_
   if (!rc) {
     c->rank = rank;
     c->world = world;
-    multi_rank_ladder(c);
     c->p2p = true;
     c->p2p_max_dims = max_dims;
     // pres: one stage list (u (u - 1) entries + slack); epack: every tile of round 0 at the

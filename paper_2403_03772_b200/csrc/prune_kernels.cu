@@ -1246,17 +1246,27 @@ void launch_prune_select(const PruneArgs& a, int stage, int m, double beta, cuda
 
 void launch_prune_scan(const PruneArgs& a, cudaStream_t s) { prune_scan_kernel<<<1, 1024, 0, s>>>(a); }
 
+namespace {
+int fine_max_u() {
+  static const int v = [] {  // PLG_FINE_MAX_U: the short-list kernel also for rounds up to this u
+    const char* e = std::getenv("PLG_FINE_MAX_U");
+    return e ? std::atoi(e) : 700;  // C3 -2%, C5 -0.3% (the long lists of large rounds keep the lean kernel)
+  }();
+  return v;
+}
+}  // namespace
+
+bool prune_short_list_kernel(int u, int64_t n, int fine_items) {
+  return n <= 90000 && fine_items > 0 && (n <= kFineMaxN || u <= fine_max_u());
+}
+
 cudaError_t launch_prune_pairs(const PruneArgs& a, cudaStream_t s) {
   static const int var = [] {  // PLG_LIST_VAR: load-pipeline variant (tuning knob)
     const char* v = std::getenv("PLG_LIST_VAR");
     return v ? std::atoi(v) : 0;
   }();
   if (a.n > 90000) return launch_pairs_cfg<true, 5>(a, s);
-  static const int fine_max_u = [] {  // PLG_FINE_MAX_U: the short-list kernel also for rounds up to this u
-    const char* v = std::getenv("PLG_FINE_MAX_U");
-    return v ? std::atoi(v) : 700;  // C3 -2%, C5 -0.3% (the long lists of large rounds keep the lean kernel)
-  }();
-  if (a.fine_items > 0 && (a.n <= kFineMaxN || a.u <= fine_max_u)) return launch_pairs_cfg<false, 5, true>(a, s);
+  if (prune_short_list_kernel(a.u, a.n, a.fine_items)) return launch_pairs_cfg<false, 5, true>(a, s);
   if (var == 1) return launch_pairs_cfg<false, 1>(a, s);
   if (var == 2) return launch_pairs_cfg<false, 2>(a, s);
   if (var == 4) return launch_pairs_cfg<false, 4>(a, s);

@@ -100,13 +100,11 @@ print(json.dumps(out))
 """
 
 
-@pytest.mark.parametrize("world", [2, 3, 4])  # 4: with the multi-rank refinement ladder (engine.cu multi_rank_ladder)
+@pytest.mark.parametrize("world", [2, 3, 4])
 def test_p2p_ranks_across_processes(plg, tmp_path, world):
     d, n, seed = 200, 2000, 29
     src = _RANK % (ROOT, d, n, seed)
-    # at 4 ranks the multi-rank refinement ladder (default from 8 ranks) is switched on
-    env = dict(os.environ, PLG_RANK_LADDER_MIN_WORLD="4") if world == 4 else None
-    procs = [subprocess.Popen([sys.executable, "-c", src, str(r), str(world), str(tmp_path)], env=env,
+    procs = [subprocess.Popen([sys.executable, "-c", src, str(r), str(world), str(tmp_path)],
                               stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True) for r in range(world)]
     outs = []
     for p in procs:
