@@ -211,7 +211,7 @@ struct plg_ctx {
   int prune_T = 1;
   std::vector<double> prune_fracs{0.05, 0.25};
   bool ladder_env = false;         // PLG_PRUNE gave the ladder: used for every round
-  double ladder_switch = 5e5;      // PLG_LADDER_SWITCH: rounds with u^2 / ranks below it use the short ladder
+  double ladder_switch = 5e5;      // PLG_LADDER_SWITCH: rounds with u^2 below it use the short ladder
   bool prune_tile_seg = false;  // PLG_PRUNE_TILESEG=1: the exhaustive rounds' segmentation (bit-identity tests)
   int emulate_world = 1;        // PLG_EMULATE_WORLD=W (tests): a single rank runs the W-rank shard schedule
   double prune_beta = 1.1;      // PLG_PRUNE_BETA > 0: hybrid refinement (deficit cut when smaller than the step)
@@ -515,28 +515,27 @@ int search_round(plg_ctx* c, int64_t n, int64_t ldw, int ldc, int u, const int* 
 // One exact pruned round (prune_kernels.cu): same chosen root and winner-k bits as
 // search_round, evaluating only the pairs needed to prove the argmin. Needs KN from an
 // earlier round of the same run.
-// The refinement ladder of one pruned round. Every stage costs each rank a pair-list launch
-// with a fixed ~43 us (its end-of-launch drain, profiles/r2_list_launch_cost.md) plus its
-// selection, scan and bound launches, whatever the rank's share of the list; a stage's pair
-// work is ~u^2 / ranks. Where that work is small — u^2 / ranks < ladder_switch — fewer, larger
-// stages win: the short ladder (three top rows, two probe suspects per row, one refinement
-// step to a quarter of the row) evaluates more pairs in 3 stages instead of 4. Measured on
-// one B200: C3 494 -> 454 ms, C4 89 -> 74 ms, C5 3 001 -> 2 988 ms (tools/ab_time.py), and
-// under tools/scale_projection.py (profiles/r2_scale_ladders.jsonl) C5 at 8 ranks 1 036 vs
-// 1 101 ms, C3 at 2 / 4 / 8 ranks 407 / 342 / 293 vs 423 / 378 / 367 ms. The ladder only
-// chooses which pairs are evaluated; each pair's bits are a function of (u, n) — except in the
-// short-list kernel, whose segmentation follows the list's length — so where that kernel runs
-// the switch ignores the rank count, and the order and every winning k stay bit-identical for
-// any number of ranks. A ladder given by PLG_PRUNE is used for every round.
+// The refinement ladder of one pruned round. Every stage costs a pair-list launch with a
+// fixed ~43 us (its end-of-launch drain, profiles/r2_list_launch_cost.md) plus its selection,
+// scan and bound launches; a stage's pair work is ~u^2. Where that work is small — u^2 <
+// ladder_switch — fewer, larger stages win: the short ladder (three top rows, two probe
+// suspects per row, one refinement step to a quarter of the row) evaluates a few more pairs
+// in 3 stages instead of 4. Measured on one B200 (tools/ab_time.py): C3 494 -> 452 ms,
+// C4 89 -> 72 ms, C5 3 011 -> 2 984 ms. The ladder only chooses which pairs are evaluated.
+// The rule ignores the rank count on purpose: at 8 ranks the short ladder would also win for
+// larger rounds (u^2 / 8 < ladder_switch; C5 projected 1 036 vs 1 101 ms, C3 293 vs 367 ms,
+// profiles/r2_scale_ladders.jsonl), but the evaluated pairs feed the next rounds'
+// predictions, hence their lists, hence the short-list kernel's list-length-dependent
+// segmentation — a rank-dependent ladder would make the winning k of later rounds differ
+// across rank counts in the last bits. With this rule the order and every winning k are
+// bit-identical for any number of ranks. A ladder given by PLG_PRUNE is used for every round.
 struct RoundLadder {
   int R, T;
   const std::vector<double>* fracs;
 };
-RoundLadder round_ladder(const plg_ctx* c, int64_t n, int u, int fine_items) {
+RoundLadder round_ladder(const plg_ctx* c, int u) {
   static const std::vector<double> kShortFracs{0.25};
-  const int shards = c->world > 1 ? c->world : c->emulate_world;
-  const int per = plg::prune_short_list_kernel(u, n, fine_items) ? 1 : shards;
-  if (!c->ladder_env && static_cast<double>(u) * u / per < c->ladder_switch) return {3, 2, &kShortFracs};
+  if (!c->ladder_env && static_cast<double>(u) * u < c->ladder_switch) return {3, 2, &kShortFracs};
   return {c->prune_R, c->prune_T, &c->prune_fracs};
 }
 
@@ -610,7 +609,7 @@ int search_round_pruned(plg_ctx* c, int64_t n, int64_t ldw, int d, int u, const 
   a.state_in = sa;
   a.state_out = sa;
   plg::launch_prune_predict(a, ps);
-  const RoundLadder lad = round_ladder(c, n, u, a.fine_items);
+  const RoundLadder lad = round_ladder(c, u);
   plg::launch_prune_top(a, lad.R, ps);
   c->launches += 2;
   int stage_idx = 0;

@@ -46,9 +46,11 @@ print(json.dumps(out))
 """
 
 
-def _run(d, n, seed, kind, tileseg, emulate_world=1, batch=None):
+def _run(d, n, seed, kind, tileseg, emulate_world=1, batch=None, extra_env=None):
     env = dict(os.environ, PLG_PRUNE_TILESEG="1" if tileseg else "0", PLG_EMULATE_WORLD=str(emulate_world))
     env.pop("PLG_PRUNE", None)
+    env.pop("PLG_LADDER_SWITCH", None)
+    env.update(extra_env or {})
     if batch:
         env["PLG_PRUNE_BATCH"] = str(batch)
     out = subprocess.run([sys.executable, "-c", _CHILD % (ROOT, d, n, seed, kind)], env=env,
@@ -93,6 +95,32 @@ def test_pruned_rounds_sharded_schedule(world):
     r = _run(300, 4000, 7, "laplace", tileseg=True, emulate_world=world)
     assert r["prune"]["order"] == r["full"]["order"]
     assert r["prune"]["k"] == r["full"]["k"]
+
+
+def test_default_segmentation_bit_identical_across_rank_counts():
+    # The multi-rank schedule with the default segmentation (short-list kernel below u = 700,
+    # whose segmentation follows each list's length; long-column kernel above it, n > 4 096)
+    # and the per-round ladder (engine.cu round_ladder, chosen from u alone): 1 and 8
+    # (emulated) ranks evaluate the same lists, so the order and every winning k are
+    # bit-identical.
+    r1 = _run(900, 5000, 13, "laplace", tileseg=False)
+    r8 = _run(900, 5000, 13, "laplace", tileseg=False, emulate_world=8)
+    assert r1["prune"]["order"] == r8["prune"]["order"] == r1["full"]["order"]
+    assert r1["prune"]["k"] == r8["prune"]["k"]
+    assert r1["prune"]["pairs"] == r8["prune"]["pairs"]
+
+
+def test_ladder_switch_off_same_order():
+    # PLG_LADDER_SWITCH=0: every round on the four-stage ladder. Different pair lists in the
+    # short-list kernel (n <= 4 096) give different sample segmentations, so the winning k
+    # agree to rounding and the order is the same.
+    on = _run(400, 3000, 17, "laplace", tileseg=False)
+    off = _run(400, 3000, 17, "laplace", tileseg=False, extra_env={"PLG_LADDER_SWITCH": "0"})
+    assert on["prune"]["order"] == off["prune"]["order"] == on["full"]["order"]
+    k_on = np.array([float.fromhex(v) for v in on["prune"]["k"]])
+    k_off = np.array([float.fromhex(v) for v in off["prune"]["k"]])
+    assert np.all(np.abs(k_on - k_off) <= 1e-9 * np.abs(k_off) + 1e-15)
+    assert on["prune"]["pairs"] != off["prune"]["pairs"]
 
 
 _ERR_CHILD = r"""
