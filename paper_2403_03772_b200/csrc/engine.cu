@@ -211,6 +211,8 @@ struct plg_ctx {
   int prune_T = 1;
   std::vector<double> prune_fracs{0.05, 0.25};
   bool ladder_env = false;         // PLG_PRUNE gave the ladder: used for every round
+  int short_R = 3, short_T = 2;    // the short ladder of small rounds (PLG_SHORT_LADDER=R:T:f1,...)
+  std::vector<double> short_fracs{0.25};
   double ladder_switch = 5e5;      // PLG_LADDER_SWITCH: rounds with u^2 below it use the short ladder
   bool prune_tile_seg = false;  // PLG_PRUNE_TILESEG=1: the exhaustive rounds' segmentation (bit-identity tests)
   int emulate_world = 1;        // PLG_EMULATE_WORLD=W (tests): a single rank runs the W-rank shard schedule
@@ -322,28 +324,30 @@ int make_tables(plg_ctx* ctx, plg_status* st) {
   return 0;
 }
 
+// "R:T:f1,f2,..." -> top rows, probe suspects, refinement steps; false if malformed
+bool parse_ladder(const char* v, int& R, int& T, std::vector<double>& fracs) {
+  int r = 0, t = 0, used = 0;
+  if (sscanf(v, "%d:%d:%n", &r, &t, &used) != 2 || r < 1 || t < 1) return false;
+  R = r;
+  T = t;
+  fracs.clear();
+  const char* f = v + used;
+  while (*f) {
+    char* end = nullptr;
+    const double x = strtod(f, &end);
+    if (end == f) break;
+    if (x > 0.0) fracs.push_back(x);
+    f = (*end == ',') ? end + 1 : end;
+  }
+  return true;
+}
+
 void parse_prune_env(plg_ctx* ctx) {
   if (const char* v = std::getenv("PLG_PRUNE")) {
-    if (!strcmp(v, "0")) {
-      ctx->prune = false;
-    } else {
-      int R = 0, T = 0, used = 0;
-      if (sscanf(v, "%d:%d:%n", &R, &T, &used) == 2 && R >= 1 && T >= 1) {
-        ctx->prune_R = R;
-        ctx->prune_T = T;
-        ctx->ladder_env = true;
-        ctx->prune_fracs.clear();
-        const char* f = v + used;
-        while (*f) {
-          char* end = nullptr;
-          const double x = strtod(f, &end);
-          if (end == f) break;
-          if (x > 0.0) ctx->prune_fracs.push_back(x);
-          f = (*end == ',') ? end + 1 : end;
-        }
-      }
-    }
+    if (!strcmp(v, "0")) ctx->prune = false;
+    else if (parse_ladder(v, ctx->prune_R, ctx->prune_T, ctx->prune_fracs)) ctx->ladder_env = true;
   }
+  if (const char* v = std::getenv("PLG_SHORT_LADDER")) parse_ladder(v, ctx->short_R, ctx->short_T, ctx->short_fracs);
   if (const char* v = std::getenv("PLG_PRUNE_TILESEG")) ctx->prune_tile_seg = !strcmp(v, "1");
   if (const char* v = std::getenv("PLG_LADDER_SWITCH")) ctx->ladder_switch = std::atof(v);
   if (const char* v = std::getenv("PLG_EMULATE_WORLD")) ctx->emulate_world = std::max(1, std::atoi(v));
@@ -534,8 +538,7 @@ struct RoundLadder {
   const std::vector<double>* fracs;
 };
 RoundLadder round_ladder(const plg_ctx* c, int u) {
-  static const std::vector<double> kShortFracs{0.25};
-  if (!c->ladder_env && static_cast<double>(u) * u < c->ladder_switch) return {3, 2, &kShortFracs};
+  if (!c->ladder_env && static_cast<double>(u) * u < c->ladder_switch) return {c->short_R, c->short_T, &c->short_fracs};
   return {c->prune_R, c->prune_T, &c->prune_fracs};
 }
 
@@ -769,7 +772,7 @@ int reserve_run(plg_ctx* c, int64_t n, int ncols, int64_t ldw, plg_status* st) {
   PLG_CUDA(c->msd.reserve(2 * static_cast<size_t>(ncols)));
   PLG_CUDA(c->idx.reserve(ncols));
   PLG_CUDA(c->nz.reserve(ncols));
-  PLG_CUDA(c->events(3 + 2 * static_cast<size_t>(std::max(ncols, 1)) * (4 + c->prune_fracs.size())));
+  PLG_CUDA(c->events(3 + 2 * static_cast<size_t>(std::max(ncols, 1)) * (4 + std::max(c->prune_fracs.size(), c->short_fracs.size()))));
   return 0;
 }
 
@@ -941,6 +944,9 @@ int run_rounds_graph(plg_ctx* c, int d, int64_t n, int rounds, bool prune, Loop&
   key.push_back(c->arena);
   for (double f : c->prune_fracs) knobs.push_back(f);
   knobs.push_back(c->ladder_env ? -1.0 : c->ladder_switch);
+  knobs.push_back(static_cast<double>(c->short_R));
+  knobs.push_back(static_cast<double>(c->short_T));
+  for (double f : c->short_fracs) knobs.push_back(-f);
   knobs.push_back(static_cast<double>(c->emulate_world));
   plg_ctx::GraphCache& g = c->graph;
   const bool same = g.key == key && g.knobs == knobs;
