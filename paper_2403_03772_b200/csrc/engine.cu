@@ -218,7 +218,9 @@ struct plg_ctx {
   int emulate_world = 1;        // PLG_EMULATE_WORLD=W (tests): a single rank runs the W-rank shard schedule
   double prune_beta = 1.1;      // PLG_PRUNE_BETA > 0: hybrid refinement (deficit cut when smaller than the step)
   int64_t prune_sub = 0;        // PLG_PRUNE_SUB: samples of round 0's prediction pass (0: exhaustive round 0)
-  int prune_min_u = plg::kSmallU;  // PLG_PRUNE_MIN_U: rounds with more candidates are pruned
+  // PLG_PRUNE_MIN_U: rounds with more candidates are pruned. 64 with the short ladder of the
+  // small rounds (C3 453 -> 441-446 ms, C5 2 986 -> 2 979 ms against 128; tools/ab_time.py)
+  int prune_min_u = 64;
   int prune_batch = kPruneBatchDefault;  // PLG_PRUNE_BATCH (tests: small batches exercise the grid barrier)
   DevBuf<double> Md, KN, pk, L, ppart, pres;
   DevBuf<int> st0, st1, rowsel, off, pwork, pdone, crow, cand, alive;
@@ -776,12 +778,19 @@ int reserve_run(plg_ctx* c, int64_t n, int ncols, int64_t ldw, plg_status* st) {
   return 0;
 }
 
+// Rounds with more candidates than this are pruned. With the exhaustive rounds' segmentation
+// (PLG_PRUNE_TILESEG=1, which makes pruned and exhaustive rounds bit-identical) rounds with
+// u <= kSmallU stay exhaustive: their small-round kernel has a segmentation of its own.
+int prune_min_u(const plg_ctx* c) {
+  return c->prune_tile_seg ? std::max(c->prune_min_u, plg::kSmallU) : c->prune_min_u;
+}
+
 // Buffers of the pruned rounds (causal_order only).
 int reserve_prune(plg_ctx* c, int64_t n, int d, plg_status* st) {
   const size_t dd = static_cast<size_t>(d) * d;
   size_t nseg = static_cast<size_t>(prune_seg_plan(n).nseg);
   if (c->prune_tile_seg)
-    for (int u = d; u > c->prune_min_u; --u) nseg = std::max(nseg, static_cast<size_t>(seg_plan(u, n).nseg));
+    for (int u = d; u > prune_min_u(c); --u) nseg = std::max(nseg, static_cast<size_t>(seg_plan(u, n).nseg));
   PLG_CUDA(c->Md.reserve(dd));
   PLG_CUDA(c->KN.reserve(dd));
   // every KN entry is defined (round 0 fills the off-diagonal ones): the prediction pass reads
@@ -1014,7 +1023,7 @@ int causal_order_impl(plg_ctx* c, const double* dX, int64_t ldx, int64_t n, int 
   const int rounds = (max_rounds < 0) ? d - 1 : std::min(max_rounds, d - 1);
   // Exact pruning needs a previous exhaustive round's knowledge and pays off above the
   // replicated small-round size.
-  const bool prune = c->prune && !c->hook && d > c->prune_min_u + 1 && rounds > 1;
+  const bool prune = c->prune && !c->hook && d > prune_min_u(c) + 1 && rounds > 1;
   c->pairs_done = 0;
   if (prune) {
     if (int rc = reserve_prune(c, n, d, st)) return rc;
@@ -1050,7 +1059,7 @@ int causal_order_impl(plg_ctx* c, const double* dX, int64_t ldx, int64_t n, int 
       if (int rc = search_round(c, c->prune_sub, ldw, d, u, act_cur, r, st, c->KN.p, false)) return rc;
       c->pairs_done = before + (c->pairs_done - before) * c->prune_sub / n;  // in full-n pair units
       if (int rc = search_round_pruned(c, n, ldw, d, u, act_cur, r, st, false)) return rc;
-    } else if (prune && r > 0 && u > c->prune_min_u) {
+    } else if (prune && r > 0 && u > prune_min_u(c)) {
       if (int rc = search_round_pruned(c, n, ldw, d, u, act_cur, r, st)) return rc;
       pruned_round = true;
     } else if (int rc = search_round(c, n, ldw, d, u, act_cur, r, st, (prune && r == 0) ? c->KN.p : nullptr,
@@ -1067,7 +1076,7 @@ int causal_order_impl(plg_ctx* c, const double* dX, int64_t ldx, int64_t n, int 
       // Pruned next round: the Gram update goes to the other buffer of the ping-pong pair on
       // the side stream (followed there by the next round's predictions), concurrently with
       // the residualisation, which reads the pre-update Gram and recomputes each new C_rr.
-      const bool pingpong = prune && (u - 1) > c->prune_min_u;
+      const bool pingpong = prune && (u - 1) > prune_min_u(c);
       const double* Cold = c->Cr;
       if (pingpong) {
         double* Cnew = (c->Cr == c->C.p) ? c->C2.p : c->C.p;

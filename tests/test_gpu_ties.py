@@ -16,13 +16,16 @@ GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 
 def test_gaps_match_the_oracle_golden_c2(plg):
-    """C2 (all rounds exhaustive, u <= 128): the runner-up gap of every round equals the
-    faithful oracle's best-vs-second gap (golden round_gaps) to rounding."""
+    """C2 with exhaustive rounds (every runner-up k exact; the default prunes rounds with
+    u > 64, whose runner-up is a certified lower bound: next test): the runner-up gap of
+    every round equals the faithful oracle's best-vs-second gap (golden round_gaps) to
+    rounding."""
     with open(os.path.join(GOLDEN, "c2_order.json")) as f:
         g = json.load(f)
     dag = plg.gen_sparse_dag(100, avg_parents=2.0, seed=1)
     X = plg.sample_lingam(dag, 10000, seed=1, noise=(0.0, 1.0), kind="laplace")
     eng = plg.Engine(0)
+    eng.set_prune(False)
     assert eng.causal_order(X) == g["order"]
     k, second = np.array(eng.round_k()), np.array(eng.round_gaps())
     ref = np.array([v if v is not None else np.nan for v in g["round_gaps"]])
