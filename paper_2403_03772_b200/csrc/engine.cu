@@ -518,16 +518,14 @@ int search_round(plg_ctx* c, int64_t n, int64_t ldw, int ldc, int u, const int* 
   return 0;
 }
 
-// One exact pruned round (prune_kernels.cu): same chosen root and winner-k bits as
-// search_round, evaluating only the pairs needed to prove the argmin. Needs KN from an
-// earlier round of the same run.
 // The refinement ladder of one pruned round. Every stage costs a pair-list launch with a
 // fixed ~43 us (its end-of-launch drain, profiles/r2_list_launch_cost.md) plus its selection,
 // scan and bound launches; a stage's pair work is ~u^2. Where that work is small — u^2 <
 // ladder_switch — fewer, larger stages win: the short ladder (three top rows, two probe
 // suspects per row, one refinement step to a quarter of the row) evaluates a few more pairs
 // in 3 stages instead of 4. Measured on one B200 (tools/ab_time.py): C3 494 -> 452 ms,
-// C4 89 -> 72 ms, C5 3 011 -> 2 984 ms. The ladder only chooses which pairs are evaluated.
+// C4 89 -> 72 ms, C5 3 011 -> 2 984 ms (before pruning started at u > 64). The ladder only
+// chooses which pairs are evaluated.
 // The rule ignores the rank count on purpose: at 8 ranks the short ladder would also win for
 // larger rounds (u^2 / 8 < ladder_switch; C5 projected 1 036 vs 1 101 ms, C3 293 vs 367 ms,
 // profiles/r2_scale_ladders.jsonl), but the evaluated pairs feed the next rounds'
@@ -544,6 +542,9 @@ RoundLadder round_ladder(const plg_ctx* c, int u) {
   return {c->prune_R, c->prune_T, &c->prune_fracs};
 }
 
+// One exact pruned round (prune_kernels.cu): same chosen root and winner-k bits as
+// search_round, evaluating only the pairs needed to prove the argmin. Needs KN from an
+// earlier round of the same run.
 int search_round_pruned(plg_ctx* c, int64_t n, int64_t ldw, int d, int u, const int* act_cur, int round,
                         plg_status* st, bool h_from_resid = true) {
   // The predictions, the top rows and the probe selection need the Gram update, the active

@@ -277,9 +277,6 @@ void launch_prune_top(const PruneArgs& a, int R, cudaStream_t s);
 void launch_prune_select(const PruneArgs& a, int stage, int m, double beta, cudaStream_t s);
 void launch_prune_scan(const PruneArgs& a, cudaStream_t s);
 cudaError_t launch_prune_pairs(const PruneArgs& a, cudaStream_t s);  // cooperative launch result
-// true when launch_prune_pairs takes the short-list kernel, whose sample segmentation (and
-// with it each pair's bits) depends on the length of the list the pair is in
-bool prune_short_list_kernel(int u, int64_t n, int fine_items);
 // multi-rank: all ranks' results (res, `world` slots of `slot` entries; entry k of the list
 // sits at (k / cnt) slot + k % cnt with cnt = ceil(total / world)) into Md / KN
 // p2p_wait: peer-memory contexts, wait for every rank's signal of this stage first

@@ -1256,7 +1256,9 @@ int fine_max_u() {
 }
 }  // namespace
 
-bool prune_short_list_kernel(int u, int64_t n, int fine_items) {
+// true when launch_prune_pairs takes the short-list kernel, whose sample segmentation (and
+// with it each pair's bits) depends on the length of the list the pair is in
+static bool prune_short_list_kernel(int u, int64_t n, int fine_items) {
   return n <= 90000 && fine_items > 0 && (n <= kFineMaxN || u <= fine_max_u());
 }
 
